@@ -1,0 +1,179 @@
+/* shorsim_b200 — B200-native iterative-Shor engine, C ABI (the drop-in boundary).
+ *
+ * Replaces the reference's C++ class API for the hot path:
+ *   shorsim::IterativeShorEngine      /root/reference/proj/include/shorsim/statevector.hpp:169-191
+ *   shorsim::run_iterative_shor       .../statevector.hpp:164-165
+ *   per-gate step/measure API         .../statevector.hpp:68-133 (init_state, apply_oracle,
+ *                                     apply_phase, apply_hadamard_top, measure_top, reset_top)
+ *   build_permutation_plan (gather)   .../statevector.hpp:88, proj/src/statevector.cpp:133-154
+ * The C++ wrapper include/shorsim_b200.hpp re-exposes these with the reference's
+ * names and exception types; INTEGRATION.md shows how the reference's callers
+ * (proj/src/harness.cpp:121-133, :504-506) bind to it.
+ *
+ * Conventions: plain pointers and sizes only; no callbacks; no allocation
+ * crosses the boundary (caller owns every output buffer); u128 bit strings
+ * travel as two u64 words {lo, hi}. An engine is not thread-safe (as the
+ * reference's is not: its buffers are mutable); use one engine per thread.
+ *
+ * Status codes (mirror proj/include/shorsim/errors.hpp:8-43):
+ *   0 ok                    1 Error (norm drift > 1e-9, statevector.cpp:374-375)
+ *   2 ConfigError           3 CeilingExceededError (statevector.cpp:291-294)
+ *   4 DegenerateBranchError 5 BudgetExceededError
+ *   6 NotInvertibleError    (the gcd is reported in shs_last_error())
+ *   7 std::invalid_argument (layout / argument validation, statevector.cpp:65-72)
+ *   8 CUDA error / no device (the engine never falls back to the CPU)
+ */
+#ifndef SHORSIM_B200_H
+#define SHORSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SHS_OK 0
+#define SHS_ERROR 1
+#define SHS_CONFIG_ERROR 2
+#define SHS_CEILING_EXCEEDED 3
+#define SHS_DEGENERATE_BRANCH 4
+#define SHS_BUDGET_EXCEEDED 5
+#define SHS_NOT_INVERTIBLE 6
+#define SHS_INVALID_ARGUMENT 7
+#define SHS_CUDA_ERROR 8
+
+/* ErrorKind order of proj/include/shorsim/noise.hpp:13-20 */
+#define SHS_ERR_NONE 0
+#define SHS_ERR_AMPLITUDE_INIT 1
+#define SHS_ERR_PHASE_INIT 2
+#define SHS_ERR_CLASSICAL_MEASURE 3
+#define SHS_ERR_QUANTUM_MEASURE 4
+#define SHS_ERR_BITFLIP 5
+
+/* How p0/p1 are combined from the fixed 256-amplitude block partials
+ * (proj/src/statevector.cpp:16-40). KAHAN reproduces the reference's
+ * sequential compensated sum bit-for-bit; EXACT is the correctly rounded sum
+ * of the same partials (deterministic, shard-count independent, within 1 ulp
+ * of KAHAN). AUTO = KAHAN while the block count is small, EXACT beyond. */
+#define SHS_COMBINE_AUTO 0
+#define SHS_COMBINE_KAHAN 1
+#define SHS_COMBINE_EXACT 2
+
+/* FactoringProblem, proj/include/shorsim/problems.hpp:15-25 (p, q ride along
+ * for verification only and are not needed by the engine) */
+typedef struct {
+    uint64_t N;
+    uint64_t a;
+    uint32_t L; /* bit length of N; the engine keeps y < min(N, 2^L) */
+    uint32_t t; /* stages / classical bits */
+    uint64_t seed;
+} shs_problem;
+
+/* ErrorConfig, proj/include/shorsim/noise.hpp:29-37 */
+typedef struct {
+    int32_t kind;
+    double delta;
+    double px, py, pz;
+    int32_t has_pauli; /* PauliProbs present (quantum_measure only) */
+} shs_error;
+
+/* SimulatorOptions, proj/include/shorsim/statevector.hpp:154-159, plus the
+ * device-side knobs. shard_count / workers are validated exactly as the
+ * reference validates them but do not change results (as in the reference). */
+typedef struct {
+    uint32_t shard_count;   /* reference default 4 */
+    uint32_t workers;       /* reference default 1 (unused: the GPU grid replaces threads) */
+    uint32_t qubit_ceiling; /* reference default 26 */
+    int32_t check_norms;    /* reference default true */
+    int32_t device;         /* CUDA device ordinal */
+    int32_t combine;        /* SHS_COMBINE_* */
+} shs_options;
+
+/* StageTrace, proj/include/shorsim/statevector.hpp:135-141 */
+typedef struct {
+    uint32_t cbit;
+    double p1;
+    int32_t sampled_bit;
+    int32_t observed_bit;
+    uint8_t classical_flip;
+    uint8_t quantum_error_branch;
+} shs_stage_trace;
+
+typedef struct shs_engine shs_engine;
+
+/* Library defaults (SimulatorOptions{4, 1, 26, true} on device 0, AUTO). */
+void shs_default_options(shs_options* out);
+
+/* IterativeShorEngine::IterativeShorEngine, statevector.cpp:285-321. */
+int shs_engine_create(const shs_problem* problem, const shs_error* error,
+                      const shs_options* options, shs_engine** out);
+void shs_engine_destroy(shs_engine* engine);
+
+/* IterativeShorEngine::run, statevector.cpp:323-412. j / j_sampled = {lo, hi};
+ * trace may be NULL, else t entries. */
+int shs_engine_run(shs_engine* engine, uint64_t seed, uint64_t bitstring_index, uint64_t j[2],
+                   uint64_t j_sampled[2], shs_stage_trace* trace);
+
+/* count consecutive runs idx0 .. idx0+count-1; j receives 2*count words. */
+int shs_engine_run_batch(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
+                         uint64_t* j);
+
+/* IterativeShorEngine::stage_multipliers: a^(2^(t-1-s)) mod N, t entries. */
+int shs_engine_stage_multipliers(const shs_engine* engine, uint64_t* out);
+uint32_t shs_engine_stages(const shs_engine* engine);
+
+/* ---- step/measure API (forced measurement sequences, amplitude parity) ----
+ * The engine holds the state as in the reference after init_state / reset_top:
+ * g_x[y] = w_x * (sel[y] * inv), y < N (zero for N <= y < 2^L). */
+
+/* init_state, statevector.cpp:126-131 */
+int shs_state_init(shs_engine* engine);
+/* Stage s gates: apply_oracle(a_pow[s]) + apply_phase(s, prefix) +
+ * apply_hadamard_top + the |psi|^2 reduction (statevector.cpp:339-375).
+ * Returns the group masses p0, p1 (the reference's measure_top p1). */
+int shs_stage_probs(shs_engine* engine, uint32_t s, uint64_t prefix_lo, uint64_t prefix_hi,
+                    double* p0, double* p1);
+/* reset_top(src_group, reinit, p_source), statevector.cpp:263-283 / 384-401 */
+int shs_stage_collapse(shs_engine* engine, int32_t src_group, double p_source);
+/* post-Hadamard amplitudes of group x of the pending stage, y in [first, first+count),
+ * interleaved (re, im) */
+int shs_stage_read(shs_engine* engine, int32_t x, uint64_t first, uint64_t count,
+                   double* interleaved);
+/* current (post-init / post-reset) amplitudes g_x[y], interleaved (re, im) */
+int shs_state_read(shs_engine* engine, int32_t x, uint64_t first, uint64_t count,
+                   double* interleaved);
+/* 256-amplitude block partials of the pending stage: out[0..nb) S0, out[nb..2nb) S1 */
+int shs_stage_block_sums(shs_engine* engine, double* out);
+uint64_t shs_num_blocks(const shs_engine* engine);
+
+/* ExchangePlan::gather computed on the device: src[z] = a_inv(s) * z mod N for
+ * z in [first, first+count) (identity for a_pow = 1). */
+int shs_index_map(shs_engine* engine, uint32_t s, uint64_t first, uint64_t count,
+                  uint64_t* src_out);
+
+/* sample_measurement, statevector.cpp:236-256 (host-side, exported for tests):
+ * out = {sampled_bit, observed_bit, error_branch, classical_flip} */
+int shs_sample_measurement(double p1, uint64_t seed, uint32_t idx, uint32_t stage,
+                           const shs_error* error, int32_t out[4]);
+
+/* ---- instrumentation (bench / profiling) ---- */
+/* Per-kernel CUDA-event timing on the engine's stream. kind: 0 probs, 1 combine,
+ * 2 collapse. Returns accumulated milliseconds and launch counts since enable. */
+int shs_engine_set_timing(shs_engine* engine, int32_t enable);
+int shs_engine_kernel_times(const shs_engine* engine, double ms[3], uint64_t launches[3]);
+/* cudaStream_t the engine launches on (as void*) */
+void* shs_engine_stream(const shs_engine* engine);
+/* total kernels launched by this engine since creation */
+uint64_t shs_engine_launch_count(const shs_engine* engine);
+/* bytes of device memory the engine holds */
+uint64_t shs_engine_device_bytes(const shs_engine* engine);
+
+/* thread-local message of the last failing call */
+const char* shs_last_error(void);
+/* library build string (arch, flags) */
+const char* shs_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,31 @@
+"""shorsim_b200: B200-native iterative-Shor simulator (arXiv 2308.05047 hot path).
+
+The stage loop of the reference's ``IterativeShorEngine``
+(/root/reference/proj/src/statevector.cpp:323-412) on hand-written sm_100a
+kernels behind the C ABI of ``include/shorsim_b200.h``.
+"""
+from .engine import (  # noqa: F401
+    BitString,
+    BudgetExceededError,
+    CeilingExceededError,
+    ConfigError,
+    CudaError,
+    DegenerateBranchError,
+    Error,
+    ErrorConfig,
+    ErrorEvent,
+    ErrorKind,
+    FactoringProblem,
+    IterativeShorEngine,
+    NotInvertibleError,
+    PauliProbs,
+    RunResult,
+    SimulatorOptions,
+    StageTrace,
+    bit_length,
+    build_info,
+    parse_error_config,
+    recommended_t,
+    run_iterative_shor,
+    sample_measurement,
+)
