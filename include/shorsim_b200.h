@@ -59,6 +59,13 @@ extern "C" {
 #define SHS_COMBINE_KAHAN 1
 #define SHS_COMBINE_EXACT 2
 
+/* Permutation kernel selection. AUTO tiles every non-identity stage whose
+ * multiplier admits balanced rows once N >= 2^20; FORCE tiles whenever a plan
+ * exists (tests use it at small N); OFF always uses the direct gather. */
+#define SHS_TILING_AUTO 0
+#define SHS_TILING_FORCE 1
+#define SHS_TILING_OFF 2
+
 /* FactoringProblem, proj/include/shorsim/problems.hpp:15-25 (p, q ride along
  * for verification only and are not needed by the engine) */
 typedef struct {
@@ -87,6 +94,7 @@ typedef struct {
     int32_t check_norms;    /* reference default true */
     int32_t device;         /* CUDA device ordinal */
     int32_t combine;        /* SHS_COMBINE_* */
+    int32_t tiling;         /* SHS_TILING_*: sorted-residue tiles for the permutation */
 } shs_options;
 
 /* StageTrace, proj/include/shorsim/statevector.hpp:135-141 */
@@ -101,7 +109,7 @@ typedef struct {
 
 typedef struct shs_engine shs_engine;
 
-/* Library defaults (SimulatorOptions{4, 1, 26, true} on device 0, AUTO). */
+/* Library defaults (SimulatorOptions{4, 1, 26, true} on device 0, AUTO, AUTO). */
 void shs_default_options(shs_options* out);
 
 /* IterativeShorEngine::IterativeShorEngine, statevector.cpp:285-321. */
@@ -161,6 +169,10 @@ int shs_sample_measurement(double p1, uint64_t seed, uint32_t idx, uint32_t stag
  * 2 collapse. Returns accumulated milliseconds and launch counts since enable. */
 int shs_engine_set_timing(shs_engine* engine, int32_t enable);
 int shs_engine_kernel_times(const shs_engine* engine, double ms[3], uint64_t launches[3]);
+/* Tile plan of stage s: out = {tiled, H, u, v, du, dv}; tiled = 0 means the
+ * stage runs the direct-gather kernels (identity, first stage, small N, or a
+ * multiplier without balanced rows). */
+int shs_stage_tile_plan(const shs_engine* engine, uint32_t s, uint64_t out[6]);
 /* cudaStream_t the engine launches on (as void*) */
 void* shs_engine_stream(const shs_engine* engine);
 /* total kernels launched by this engine since creation */

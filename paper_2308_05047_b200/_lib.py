@@ -28,6 +28,7 @@ SHS_INVALID_ARGUMENT = 7
 SHS_CUDA_ERROR = 8
 
 COMBINE = {"auto": 0, "kahan": 1, "exact": 2}
+TILING = {"auto": 0, "force": 1, "off": 2}
 
 
 class shs_problem(C.Structure):
@@ -41,7 +42,7 @@ class shs_error(C.Structure):
 
 class shs_options(C.Structure):
     _fields_ = [("shard_count", u32), ("workers", u32), ("qubit_ceiling", u32),
-                ("check_norms", i32), ("device", i32), ("combine", i32)]
+                ("check_norms", i32), ("device", i32), ("combine", i32), ("tiling", i32)]
 
 
 class shs_stage_trace(C.Structure):
@@ -72,6 +73,7 @@ SIGNATURES = [
                                          C.POINTER(i32)]),
     ("shs_engine_set_timing", C.c_int, [vp, i32]),
     ("shs_engine_kernel_times", C.c_int, [vp, C.POINTER(dbl), C.POINTER(u64)]),
+    ("shs_stage_tile_plan", C.c_int, [vp, u32, C.POINTER(u64)]),
     ("shs_engine_stream", vp, [vp]),
     ("shs_engine_launch_count", u64, [vp]),
     ("shs_engine_device_bytes", u64, [vp]),

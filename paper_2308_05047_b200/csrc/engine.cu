@@ -16,6 +16,9 @@
 //   k_stage_collapse read sel[z], sel[src z]; write sel'[z] = h_bit  48 B/amp
 // with src z = a_inv * z mod N computed by Shoup multiplication once per thread
 // and add/conditional-subtract afterwards (no index tables: 0 B/amp).
+// Non-identity stages of large states run the same two passes as sorted-residue
+// tiles (tiled.cuh, k_tiled<true|false> + k_tile_fixup) so both the direct and
+// the gathered side of the permutation are coalesced.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,6 +31,7 @@
 #include "../../include/shorsim_b200.h"
 #include "device_math.cuh"
 #include "host_model.hpp"
+#include "tiled.cuh"
 
 using namespace shs;
 
@@ -51,6 +55,58 @@ int set_error(int code, const std::string& msg) {
 constexpr double kNormTolerance = 1e-9;     // statevector.cpp:18
 constexpr double kDegenerateMass = 1e-300;  // statevector.cpp:19
 constexpr uint64_t kKahanMaxBlocks = 1024;  // AUTO: sequential Kahan up to 2^18 amplitudes
+constexpr uint64_t kTileAutoMinN = 1ull << 20;  // AUTO tiling from 16 MB of state
+constexpr uint64_t kTileMinRow = 512;           // every 256-block touches <= 2 rows
+constexpr uint64_t kTileMaxRows = 1ull << 18;   // head scratch <= 1 GB
+
+// Host side of a stage's sorted-residue tiling (see tiled.cuh).
+struct TilePlanHost {
+    bool tiled = false;
+    uint64_t H = 0, u = 0, v = 0, du = 0, dv = 0;
+    uint64_t A = 0, A_sh = 0, m = 0, m_sh = 0, ntiles = 0;
+};
+
+// Pick the largest row count H (powers of two and 3 * 2^k up to N/1024) whose
+// three gap lengths are all >= kTileMinRow: one O(H) scan of j*A mod N with
+// running argmin / argmax gives u(H), v(H) for every candidate.
+TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling) {
+    TilePlanHost pl;
+    if (tiling == SHS_TILING_OFF || A == 1) return pl;
+    if (tiling == SHS_TILING_AUTO && N < kTileAutoMinN) return pl;
+    const uint64_t hmax = std::min<uint64_t>(N / 1024, kTileMaxRows);
+    std::vector<uint64_t> cands;
+    for (uint64_t h = 2; h <= hmax; h *= 2) {
+        cands.push_back(h);
+        if (h >= 4 && h / 2 * 3 <= hmax) cands.push_back(h / 2 * 3);
+    }
+    std::sort(cands.begin(), cands.end());
+    uint64_t j = 1, r = 0, umin = N, uj = 0, vmax = 0, vj = 0;
+    for (uint64_t H : cands) {
+        for (; j < H; ++j) {
+            r += A;
+            if (r >= N) r -= N;
+            if (r < umin) { umin = r; uj = j; }
+            if (r > vmax) { vmax = r; vj = j; }
+        }
+        const uint64_t du = umin, dv = N - vmax;
+        if (du >= kTileMinRow && dv >= kTileMinRow) {
+            pl.tiled = true;
+            pl.H = H;
+            pl.u = uj;
+            pl.v = vj;
+            pl.du = du;
+            pl.dv = dv;
+        }
+    }
+    if (pl.tiled) {
+        pl.A = A;
+        pl.A_sh = shoup(A, N);
+        pl.m = m;
+        pl.m_sh = shoup(m, N);
+        pl.ntiles = (pl.H + kRows - 1) / kRows;
+    }
+    return pl;
+}
 
 struct StageParams {
     const double2* X;
@@ -279,6 +335,12 @@ struct shs_engine {
     double* h_out = nullptr;
     uint64_t nb = 0, nchunks = 0;
     int grid_cap = 0;        // CTAs of the persistent stage kernels
+    int tiled_cap = 0;       // CTAs of the persistent tiled kernels
+    int fixup_cap = 0;       // CTAs of k_tile_fixup
+    std::vector<TilePlanHost> plans;  // per stage
+    uint64_t max_rows = 0;   // largest H over the stages' plans
+    double* head = nullptr;  // [max_rows][2][256]
+    double* tail = nullptr;  // [max_rows][2]
     bool kahan = false;      // resolved combine mode
     // state
     bool e1 = true;
@@ -373,6 +435,31 @@ StageParams params_for(const shs_engine* e, uint32_t s) {
     return p;
 }
 
+TileParams tile_params_for(const shs_engine* e, uint32_t s) {
+    const TilePlanHost& pl = e->plans[s];
+    TileParams p{};
+    p.X = e->X;
+    p.Y = e->Y;
+    p.N = e->N;
+    p.A = pl.A;
+    p.A_sh = pl.A_sh;
+    p.m = pl.m;
+    p.m_sh = pl.m_sh;
+    p.H = pl.H;
+    p.u = pl.u;
+    p.v = pl.v;
+    p.du = pl.du;
+    p.dv = pl.dv;
+    p.ntiles = pl.ntiles;
+    p.sc = e->sc;
+    p.S = e->S;
+    p.nb = e->nb;
+    p.partials = e->partials;
+    p.head = e->head;
+    p.tail = e->tail;
+    return p;
+}
+
 int grid_for(const shs_engine* e) {
     return static_cast<int>(std::min<uint64_t>(e->nchunks, static_cast<uint64_t>(e->grid_cap)));
 }
@@ -410,6 +497,8 @@ int engine_validate(const shs_problem& pr, const shs_error& er, const shs_option
     if (pr.t < 1 || pr.t > 127) return set_error(SHS_INVALID_ARGUMENT, "t must be in [1, 127]");
     if (o.combine < SHS_COMBINE_AUTO || o.combine > SHS_COMBINE_EXACT)
         return set_error(SHS_INVALID_ARGUMENT, "unknown combine mode");
+    if (o.tiling < SHS_TILING_AUTO || o.tiling > SHS_TILING_OFF)
+        return set_error(SHS_INVALID_ARGUMENT, "unknown tiling mode");
     return SHS_OK;
 }
 
@@ -426,6 +515,8 @@ void release(shs_engine* e) {
     cudaFree(e->Y);
     cudaFree(e->S);
     cudaFree(e->partials);
+    cudaFree(e->head);
+    cudaFree(e->tail);
     cudaFree(e->d_out);
     if (e->h_out) cudaFreeHost(e->h_out);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -442,6 +533,11 @@ int ensure_buffers(shs_engine* e) {
     SHS_CUDA(cudaMalloc(&e->Y, amp_bytes));
     SHS_CUDA(cudaMalloc(&e->S, sizeof(double) * 2 * e->nb));
     e->device_bytes += 2 * amp_bytes + sizeof(double) * 2 * e->nb;
+    if (e->max_rows) {
+        SHS_CUDA(cudaMalloc(&e->head, sizeof(double) * 2 * 256 * e->max_rows));
+        SHS_CUDA(cudaMalloc(&e->tail, sizeof(double) * 2 * e->max_rows));
+        e->device_bytes += sizeof(double) * 2 * 257 * e->max_rows;
+    }
     return SHS_OK;
 }
 
@@ -467,18 +563,30 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
     e->sc.inv = e->inv;
     e->sc.phase_mul = (gather || phi != 0.0) ? 1 : 0;
     e->ps = s;
-    StageParams p = params_for(e, s);
-    rc = launch(e, 0, [&] {
-        if (gather) {
-            if (e->e1) launch_probs<true, true>(e, p);
-            else launch_probs<true, false>(e, p);
-        } else {
-            if (e->e1) launch_probs<false, true>(e, p);
-            else launch_probs<false, false>(e, p);
-        }
-    });
+    int nparts = grid_for(e);
+    if (e->plans[s].tiled && !e->e1) {
+        TileParams tp = tile_params_for(e, s);
+        const int g1 = static_cast<int>(std::min<uint64_t>(tp.ntiles, e->tiled_cap));
+        const int g2 = static_cast<int>(
+            std::min<uint64_t>((2 * tp.H + 255) / 256, static_cast<uint64_t>(e->fixup_cap)));
+        rc = launch(e, 0, [&] {
+            k_tiled<true><<<g1, kTileThreads, 0, e->stream>>>(tp);
+            k_tile_fixup<<<g2, 256, 0, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
+        });
+        nparts = g1 + g2;
+    } else {
+        StageParams p = params_for(e, s);
+        rc = launch(e, 0, [&] {
+            if (gather) {
+                if (e->e1) launch_probs<true, true>(e, p);
+                else launch_probs<true, false>(e, p);
+            } else {
+                if (e->e1) launch_probs<false, true>(e, p);
+                else launch_probs<false, false>(e, p);
+            }
+        });
+    }
     if (rc) return rc;
-    const int nparts = grid_for(e);
     rc = launch(e, 1, [&] {
         k_finalize<<<1, 128, 0, e->stream>>>(e->partials, nparts, e->S, e->nb, e->kahan ? 1 : 0,
                                              e->d_out);
@@ -507,17 +615,25 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
         return set_error(SHS_DEGENERATE_BRANCH,
                          "impossible measurement branch at stage " + std::to_string(e->ps));
     const bool gather = e->a_pows[e->ps] != 1;
-    StageParams p = params_for(e, e->ps);
-    p.sel = src_group;
-    int rc = launch(e, 2, [&] {
-        if (gather) {
-            if (e->e1) launch_collapse<true, true>(e, p);
-            else launch_collapse<true, false>(e, p);
-        } else {
-            if (e->e1) launch_collapse<false, true>(e, p);
-            else launch_collapse<false, false>(e, p);
-        }
-    });
+    int rc;
+    if (e->plans[e->ps].tiled && !e->e1) {
+        TileParams tp = tile_params_for(e, e->ps);
+        tp.sel = src_group;
+        const int g1 = static_cast<int>(std::min<uint64_t>(tp.ntiles, e->tiled_cap));
+        rc = launch(e, 2, [&] { k_tiled<false><<<g1, kTileThreads, 0, e->stream>>>(tp); });
+    } else {
+        StageParams p = params_for(e, e->ps);
+        p.sel = src_group;
+        rc = launch(e, 2, [&] {
+            if (gather) {
+                if (e->e1) launch_collapse<true, true>(e, p);
+                else launch_collapse<true, false>(e, p);
+            } else {
+                if (e->e1) launch_collapse<false, true>(e, p);
+                else launch_collapse<false, false>(e, p);
+            }
+        });
+    }
     if (rc) return rc;
     std::swap(e->X, e->Y);
     e->e1 = false;
@@ -581,6 +697,7 @@ void shs_default_options(shs_options* o) {
     o->check_norms = 1;
     o->device = 0;
     o->combine = SHS_COMBINE_AUTO;
+    o->tiling = SHS_TILING_AUTO;
 }
 
 const char* shs_last_error(void) { return g_last_error.c_str(); }
@@ -621,6 +738,22 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
             return set_error(SHS_NOT_INVERTIBLE, msg);
         }
     }
+    {
+        std::vector<std::pair<uint64_t, TilePlanHost>> cache;  // per distinct multiplier
+        e->plans.assign(e->t, TilePlanHost{});
+        for (uint32_t s = 1; s < e->t; ++s) {  // stage 0 always starts from |1> (direct kernels)
+            if (e->a_pows[s] == 1) continue;
+            auto it = std::find_if(cache.begin(), cache.end(),
+                                   [&](const auto& kv) { return kv.first == e->a_pows[s]; });
+            if (it == cache.end()) {
+                cache.emplace_back(e->a_pows[s],
+                                   make_tile_plan(e->a_pows[s], e->a_invs[s], e->N, o.tiling));
+                it = cache.end() - 1;
+            }
+            e->plans[s] = it->second;
+            if (it->second.tiled) e->max_rows = std::max(e->max_rows, it->second.H);
+        }
+    }
     e->nb = (e->N + kBlock - 1) / kBlock;
     e->nchunks = (e->N + kChunk - 1) / kChunk;
     e->kahan = o.combine == SHS_COMBINE_KAHAN ||
@@ -645,9 +778,14 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<true, false>, kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     e->grid_cap = std::max(1, occ) * e->num_sms;
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<true>, kTileThreads, 0);
+    if (ce != cudaSuccess) return fail(ce, "occupancy");
+    e->tiled_cap = std::max(1, occ) * e->num_sms;
+    e->fixup_cap = 2 * e->num_sms;
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");
-    const size_t part_bytes = sizeof(unsigned long long) * 2 * kDigits * e->grid_cap;
+    const size_t part_bytes = sizeof(unsigned long long) * 2 * kDigits *
+                              std::max(e->grid_cap, e->tiled_cap + e->fixup_cap);
     if ((ce = cudaMalloc(&e->partials, part_bytes)) != cudaSuccess)
         return fail(ce, "cudaMalloc(partials)");
     if ((ce = cudaMalloc(&e->d_out, 4 * sizeof(double))) != cudaSuccess)
@@ -762,6 +900,19 @@ int shs_state_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
 }
 
 uint64_t shs_num_blocks(const shs_engine* e) { return e ? e->nb : 0; }
+
+int shs_stage_tile_plan(const shs_engine* e, uint32_t s, uint64_t out[6]) {
+    if (!e || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    if (s >= e->t) return set_error(SHS_INVALID_ARGUMENT, "stage index out of range");
+    const TilePlanHost& pl = e->plans[s];
+    out[0] = pl.tiled ? 1 : 0;
+    out[1] = pl.H;
+    out[2] = pl.u;
+    out[3] = pl.v;
+    out[4] = pl.du;
+    out[5] = pl.dv;
+    return SHS_OK;
+}
 
 int shs_stage_block_sums(shs_engine* e, double* out) {
     return guarded(e, [&]() -> int {

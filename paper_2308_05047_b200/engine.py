@@ -212,10 +212,12 @@ class SimulatorOptions:
     check_norms: bool = True
     device: int = 0
     combine: str = "auto"  # "auto" | "kahan" | "exact" (see include/shorsim_b200.h)
+    tiling: str = "auto"   # "auto" | "force" | "off"
 
     def to_c(self) -> L.shs_options:
         return L.shs_options(self.shard_count, self.workers, self.qubit_ceiling,
-                             1 if self.check_norms else 0, self.device, L.COMBINE[self.combine])
+                             1 if self.check_norms else 0, self.device, L.COMBINE[self.combine],
+                             L.TILING[self.tiling])
 
 
 @dataclass
@@ -340,6 +342,11 @@ class IterativeShorEngine:
         out = (L.u64 * count)()
         _raise(self._lib.shs_index_map(self._h, s, first, count, out))
         return out
+
+    def tile_plan(self, s: int):
+        out = (L.u64 * 6)()
+        _raise(self._lib.shs_stage_tile_plan(self._h, s, out))
+        return dict(zip(("tiled", "H", "u", "v", "du", "dv"), list(out)))
 
     # -- instrumentation
     def set_timing(self, enable: bool) -> None:
