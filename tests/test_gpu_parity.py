@@ -163,16 +163,23 @@ def test_forced_sequences_amplitudes_bit_exact(cuda_ok, golden):
             prefix |= st["bit"] << st["s"]
 
 
+@pytest.mark.parametrize("tiling", ["off", "force"])
 @pytest.mark.parametrize("N,a,t,err", [
     (1048351, 12345, 6, E()),
     (1048351, 777, 5, E("phase_init", 0.1)),
     (262139, 31337, 6, E("amplitude_init", 0.1)),
     (4194301, 5, 4, E("quantum_measure", 0.01, 0.005, 0.005, 0.0)),
+    (4194301, 1234567, 5, E("classical_measure", 0.05)),
 ])
-def test_forced_sequence_vs_oracle_full_state(cuda_ok, oracle, N, a, t, err):
+def test_forced_sequence_vs_oracle_full_state(cuda_ok, oracle, N, a, t, err, tiling):
     """Whole-state comparison (every amplitude) after every step at sizes the
-    oracle finishes in seconds; alternating forced branches."""
-    eng = engine(N, a, t, err, combine="kahan")
+    oracle finishes in seconds; random forced branches; direct-gather and
+    sorted-residue-tile kernels."""
+    eng = engine(N, a, t, err, combine="kahan", tiling=tiling)
+    tiled = [eng.tile_plan(s)["tiled"] for s in range(t)]
+    assert not tiled[0]
+    if tiling == "off":
+        assert not any(tiled)
     orc = oracle.engine(N, a, N.bit_length(), t, oracle_err(err))
     eng.state_init()
     orc.state_init()
@@ -303,3 +310,32 @@ def test_c4_size_stages(cuda_ok):
     inv = o.mod_inverse(a_pows[5], N)
     got = list(eng.index_map(5, N - 2048, 2048))
     assert got == [(inv * z) % N for z in range(N - 2048, N)]
+
+
+def test_tile_plans_partition_and_auto_selection(cuda_ok):
+    """AUTO tiles every non-identity stage of the bench problems; rows of every
+    plan satisfy the three-gap partition (checked exhaustively at small N)."""
+    for N, a in [(4294967213, 5), (268435247, 3), (16777207, 2)]:
+        eng = engine(N, a)
+        for s in range(1, eng.t):
+            pl = eng.tile_plan(s)
+            assert pl["tiled"], (N, s, pl)
+            assert pl["du"] >= 512 and pl["dv"] >= 512 and pl["H"] <= N // 1024
+    N, a = 1048351, 12345
+    eng = engine(N, a, 8, tiling="force")
+    pows = eng.stage_multipliers()
+    ntiled = 0
+    for s in range(1, 8):
+        pl = eng.tile_plan(s)
+        if not pl["tiled"]:
+            continue
+        ntiled += 1
+        H, u, v, du, dv, A = pl["H"], pl["u"], pl["v"], pl["du"], pl["dv"], pows[s]
+        cover = np.zeros(N, dtype=np.int8)
+        for j in range(H):
+            L = du if j + u < H else (dv if j >= v else du + dv)
+            z = j * A % N
+            assert z + L <= N
+            cover[z:z + L] += 1
+        assert cover.min() == 1 and cover.max() == 1
+    assert ntiled >= 5
