@@ -58,6 +58,7 @@ constexpr uint64_t kKahanMaxBlocks = 1024;  // AUTO: sequential Kahan up to 2^18
 constexpr uint64_t kTileAutoMinN = 1ull << 20;  // AUTO tiling from 16 MB of state
 constexpr uint64_t kTileMinRow = 512;           // every 256-block touches <= 2 rows
 constexpr uint64_t kTileMaxRows = 1ull << 18;   // head scratch <= 1 GB
+constexpr uint64_t kTileMinRowsPlan = 256;      // >= 16 tiles of kRows rows
 
 // Host side of a stage's sorted-residue tiling (see tiled.cuh).
 struct TilePlanHost {
@@ -67,8 +68,11 @@ struct TilePlanHost {
 };
 
 // Pick the largest row count H (powers of two and 3 * 2^k up to N/1024) whose
-// three gap lengths are all >= kTileMinRow: one O(H) scan of j*A mod N with
-// running argmin / argmax gives u(H), v(H) for every candidate.
+// three gap lengths are all >= kTileMinRow and at most 3x the mean row: one
+// O(H) scan of j*A mod N with running argmin / argmax gives u(H), v(H) for
+// every candidate. Multipliers without such an H (tiny A, or A/N with a huge
+// partial quotient) keep the direct gather, whose warps then read a few long
+// runs anyway.
 TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling) {
     TilePlanHost pl;
     if (tiling == SHS_TILING_OFF || A == 1) return pl;
@@ -89,7 +93,10 @@ TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling) {
             if (r > vmax) { vmax = r; vj = j; }
         }
         const uint64_t du = umin, dv = N - vmax;
-        if (du >= kTileMinRow && dv >= kTileMinRow) {
+        // rows must be long enough (each 256-block touches <= 2 rows) and balanced
+        // (the longest row, du + dv, within 3x the mean N / H), else a tile idles SMs
+        if (H >= kTileMinRowsPlan && du >= kTileMinRow && dv >= kTileMinRow &&
+            du + dv <= 3 * (N / H + 1)) {
             pl.tiled = true;
             pl.H = H;
             pl.u = uj;
@@ -570,7 +577,7 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
         const int g2 = static_cast<int>(
             std::min<uint64_t>((2 * tp.H + 255) / 256, static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
-            k_tiled<true><<<g1, kTileThreads, 0, e->stream>>>(tp);
+            k_tiled<true><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
             k_tile_fixup<<<g2, 256, 0, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
         nparts = g1 + g2;
@@ -620,7 +627,9 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
         TileParams tp = tile_params_for(e, e->ps);
         tp.sel = src_group;
         const int g1 = static_cast<int>(std::min<uint64_t>(tp.ntiles, e->tiled_cap));
-        rc = launch(e, 2, [&] { k_tiled<false><<<g1, kTileThreads, 0, e->stream>>>(tp); });
+        rc = launch(e, 2, [&] {
+            k_tiled<false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+        });
     } else {
         StageParams p = params_for(e, e->ps);
         p.sel = src_group;
@@ -778,9 +787,14 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<true, false>, kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     e->grid_cap = std::max(1, occ) * e->num_sms;
-    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<true>, kTileThreads, 0);
-    if (ce != cudaSuccess) return fail(ce, "occupancy");
-    e->tiled_cap = std::max(1, occ) * e->num_sms;
+    // one persistent TMA-pipelined CTA per SM for the tiled passes
+    ce = cudaFuncSetAttribute(k_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(tile_smem_bytes<true>()));
+    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<probs>)");
+    ce = cudaFuncSetAttribute(k_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(tile_smem_bytes<false>()));
+    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<collapse>)");
+    e->tiled_cap = e->num_sms;
     e->fixup_cap = 2 * e->num_sms;
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");

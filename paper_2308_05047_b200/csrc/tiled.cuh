@@ -1,30 +1,53 @@
-// Sorted-residue tiles for the modular-multiplication permutation.
+// Sorted-residue tiles for the modular-multiplication permutation,
+// fed by asynchronous global->shared copies through an mbarrier ring.
 //
 // For the stage multiplier A (m = A^-1 mod N) and a row count H, the residues
 // z_j = j*A mod N (j < H) split Z_N into H rows [z_j, z_j + g_j) and
 //                      src(z_j + i) = (j + i*m) mod N.
-// So a tile of kRows consecutive rows j and kCols consecutive columns i reads
-// the gathered side as kCols runs of kRows consecutive amplitudes (256 B) and
-// the direct side / output as kRows runs of kCols consecutive amplitudes (1 KB):
-// both HBM sides are coalesced; the transpose happens in shared memory. By the
-// three-distance theorem a row's length and its successor in z order need no
-// sort: with u = argmin_{0<j<H} (jA mod N), v = argmax_{0<j<H} (jA mod N),
+// A chunk of kRows consecutive rows j and kCols consecutive columns i therefore
+// reads the gathered side as kCols runs of kRows amplitudes (256 B each) and
+// the direct side / output as kRows runs of kCols amplitudes (1 KB each): both
+// HBM sides are whole-line and coalesced; the transpose happens in shared
+// memory. By the three-distance theorem a row's length and its successor in z
+// order need no sort: with u = argmin_{0<j<H} (jA mod N), v = argmax (jA mod N),
 //   j + u < H : length du = uA mod N,       successor j + u
 //   j >= v    : length dv = N - (vA mod N),  successor j - v
 //   otherwise : length du + dv,              successor j + u - v.
-// Block partial sums (fixed 256-amplitude blocks in z order, bit-identical to
-// proj/src/statevector.cpp:353-371) run as one sequential chain per (row,
-// group); the block that straddles two rows is finished by k_tile_fixup from
-// the predecessor's tail partial and the row's stored head norms.
+//
+// CTA roles (one persistent CTA per SM):
+//   producer warps     — 16-byte cp.async (LDGSTS) copies of the chunk's 64
+//                        source-column runs and 16 row runs into a kStages-deep
+//                        ring; each producer thread's copies complete on
+//                        full[stage] via cp.async.mbarrier.arrive.noinc. (1D TMA
+//                        bulk copies were measured slower here: ~80 requests of
+//                        256 B - 1 KB per 32 KB chunk are TMA-issue bound.)
+//   warps 0..7         — consumers: h0/h1 of 4 amplitudes per thread from shared
+//                        memory; the probs pass writes |h|^2 to a double-buffered
+//                        norm tile, the collapse pass stores sel'[z] (coalesced)
+//   warp kChainWarp    — probs pass only: one lane per (row, group) folds the
+//                        norms in z order into the fixed 256-block partials,
+//                        bit-identical to proj/src/statevector.cpp:353-371, and
+//                        into the CTA's exact accumulator; the block straddling
+//                        two rows is finished by k_tile_fixup from the
+//                        predecessor's tail partial and the row's stored head.
 #pragma once
 
 #include "device_math.cuh"
 
 namespace shs {
 
-constexpr int kRows = 16;   // rows per tile
-constexpr int kCols = 64;   // columns per chunk
-constexpr int kTileThreads = 256;
+constexpr int kRows = 16;     // rows per tile
+constexpr int kCols = 64;     // columns per chunk
+constexpr int kStages = 4;    // copy ring depth
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = 32 * kConsumerWarps;
+constexpr int kProducerWarps = 4;
+constexpr int kProducers = 32 * kProducerWarps;
+constexpr int kProducerWarp = kConsumerWarps;                   // warps 8..11
+constexpr int kChainWarp = kConsumerWarps + kProducerWarps;     // warp 12 (probs only)
+constexpr int kCopiesPerProducer = kRows * kCols / kProducers;  // 8 per side
+constexpr int kNormFull0 = 1, kNormEmpty0 = 3;     // named barrier ids (2 buffers each)
+constexpr int kNrmStride = kCols + 2;              // 16 B-aligned rows, conflict-free LDS.128
 
 struct TileParams {
     const double2* X;
@@ -44,6 +67,7 @@ struct TileParams {
 };
 
 __device__ __forceinline__ uint64_t tile_row_len(uint64_t j, const TileParams& p) {
+    if (j >= p.H) return 0;
     if (j + p.u < p.H) return p.du;
     if (j >= p.v) return p.dv;
     return p.du + p.dv;
@@ -53,6 +77,47 @@ __device__ __forceinline__ uint64_t tile_row_succ(uint64_t j, const TileParams& 
     if (j + p.u < p.H) return j + p.u;
     if (j >= p.v) return j - p.v;
     return j + p.u - p.v;
+}
+
+// ---------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 16-byte asynchronous copy global -> shared (LDGSTS), L1 bypassed
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
+                 : "memory");
+}
+// arrive on bar once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void write_partials(unsigned long long (*digits)[kDigits],
@@ -68,131 +133,251 @@ __device__ __forceinline__ void write_partials(unsigned long long (*digits)[kDig
     }
 }
 
-// kProbs: the probability pass (norms, block partials, exact accumulation).
-// !kProbs: the collapse pass (writes Y[z] = h_sel).
+// One ring slot: the chunk's gathered columns (transposed, +1 padding against
+// bank conflicts), its direct rows, and the row table the consumers need.
+struct __align__(16) TileStage {
+    double2 src[kCols][kRows + 1];
+    double2 dst[kRows][kCols];
+    uint64_t row_z[kRows];
+    uint64_t row_l[kRows];
+    uint64_t i0;
+    uint64_t last;  // 1 on the last chunk of the CTA's sequence
+};
+
 template <bool kProbs>
-__global__ void __launch_bounds__(kTileThreads) k_tiled(TileParams p) {
-    __shared__ double2 src_s[kCols][kRows + 1];               // gathered side, transposed
-    __shared__ double nrm[kProbs ? 2 : 1][kRows][kCols + 1];  // norms for the chains
-    __shared__ uint64_t row_z[kRows], row_l[kRows];
-    __shared__ unsigned long long digits[2][kDigits];
+struct TileSmem {
+    TileStage stage[kStages];
+    double nrm[kProbs ? 2 : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
+    uint64_t full[kStages], empty[kStages];
+    unsigned long long digits[2][kDigits];
+};
+
+template <bool kProbs>
+constexpr int tile_threads() {
+    return 32 * (kConsumerWarps + kProducerWarps + (kProbs ? 1 : 0));
+}
+
+template <bool kProbs>
+constexpr size_t tile_smem_bytes() {
+    return sizeof(TileSmem<kProbs>);
+}
+
+// Tile length (longest of its kRows rows) and, for lane & (kRows-1), its row.
+__device__ __forceinline__ uint64_t tile_rows(const TileParams& p, uint64_t j0, int lane,
+                                              uint64_t& z, uint64_t& len) {
+    const uint64_t j = j0 + (lane & (kRows - 1));
+    len = tile_row_len(j, p);
+    z = len ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
+    uint64_t mx = len;
+#pragma unroll
+    for (int o = kRows / 2; o > 0; o >>= 1) {
+        const uint64_t other = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = other > mx ? other : mx;
+    }
+    return mx;
+}
+
+template <bool kProbs>
+__global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TileSmem<kProbs>& sm = *reinterpret_cast<TileSmem<kProbs>*>(smem_raw);
     const int tid = threadIdx.x;
-    if (kProbs) {
-        for (int i = tid; i < 2 * kDigits; i += kTileThreads) (&digits[0][0])[i] = 0ull;
+    const int warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sm.full[s], kProducers + 1);  // copies of every producer + header
+            mbar_init(&sm.empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    DigitWindow win;
-    window_reset(win);
-    // chain lanes: warp 0, lane = g * kRows + r
-    const int cr = tid & (kRows - 1), cg = (tid >> 4) & 1;
-    const bool chain = kProbs && tid < 2 * kRows;
+    if (kProbs)
+        for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&sm.digits[0][0])[i] = 0ull;
+    __syncthreads();
 
-    for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-        const uint64_t j0 = tile * kRows;
-        __syncthreads();  // previous tile fully consumed (row_z / row_l reuse)
-        if (tid < kRows) {
-            const uint64_t j = j0 + tid;
-            if (j < p.H) {
-                row_z[tid] = mulmod_shoup(j, p.A, p.A_sh, p.N);
-                row_l[tid] = tile_row_len(j, p);
-            } else {
-                row_z[tid] = 0;
-                row_l[tid] = 0;
+    if (warp >= kProducerWarp && warp < kProducerWarp + kProducerWarps) {
+        // ------------------------------------------------------------ producers
+        // gathered side: element e = pt + kProducers * k is (column e / kRows,
+        // row e % kRows = pt % kRows): 16 consecutive threads copy one column's
+        // 256 B run. Direct side: element e is (row e / kCols = pt / kCols + 2k,
+        // column e % kCols = pt % kCols): 64 threads per 1 KB row run. The row
+        // table lives in lanes 0..15 of every producer warp (tile_rows) and is
+        // fetched by shuffles.
+        const int pt = tid - 32 * kProducerWarp;
+        const int src_c0 = pt / kRows;
+        const int dst_r0 = pt / kCols, dst_c = pt % kCols;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            const uint64_t j0 = tile * kRows;
+            uint64_t rz, rl;  // row (lane % kRows) of the tile: also this thread's source row
+            const uint64_t tlen = tile_rows(p, j0, lane, rz, rl);
+            const bool last_tile = tile + gridDim.x >= p.ntiles;
+            uint64_t dz[kCopiesPerProducer], dl[kCopiesPerProducer];
+#pragma unroll
+            for (int k = 0; k < kCopiesPerProducer; ++k) {
+                dz[k] = __shfl_sync(0xffffffffu, rz, dst_r0 + 2 * k);
+                dl[k] = __shfl_sync(0xffffffffu, rl, dst_r0 + 2 * k);
             }
-        }
-        __syncthreads();
-        uint64_t tile_len = 0;
+            for (uint64_t i0 = 0; i0 < tlen; i0 += kCols) {
+                mbar_wait(&sm.empty[stage], phase ^ 1);
+                TileStage& st = sm.stage[stage];
 #pragma unroll
-        for (int r = 0; r < kRows; ++r) tile_len = row_l[r] > tile_len ? row_l[r] : tile_len;
-        // chain state of this lane's (row, group)
-        uint64_t c_z = 0, c_len = 0, c_head = 0;
-        double c_s = 0.0;
-        if (chain) {
-            c_z = row_z[cr];
-            c_len = row_l[cr];
-            c_head = (256 - (c_z & 255)) & 255;
-        }
-
-        for (uint64_t i0 = 0; i0 < tile_len; i0 += kCols) {
-            // gathered side: column c is a run of kRows amplitudes at (j0 + (i0+c) m) mod N
-            {
-                const int r = tid & (kRows - 1);
-                const int cc = tid >> 4;
-#pragma unroll
-                for (int k = 0; k < kCols / 16; ++k) {
-                    const int c = cc + 16 * k;
+                for (int k = 0; k < kCopiesPerProducer; ++k) {
+                    const int c = src_c0 + (kProducers / kRows) * k;
                     const uint64_t pos = i0 + c;
-                    double2 v = make_double2(0.0, 0.0);
-                    if (pos < row_l[r]) {
-                        const uint64_t src = addmod(j0 + r, mulmod_shoup(pos, p.m, p.m_sh, p.N), p.N);
-                        v = __ldg(p.X + src);
+                    if (pos < rl) {
+                        const uint64_t src =
+                            addmod(j0 + (pt & (kRows - 1)), mulmod_shoup(pos, p.m, p.m_sh, p.N), p.N);
+                        cp_async16(&st.src[c][pt & (kRows - 1)], p.X + src);
                     }
-                    src_s[c][r] = v;
+                }
+#pragma unroll
+                for (int k = 0; k < kCopiesPerProducer; ++k) {
+                    const uint64_t pos = i0 + dst_c;
+                    if (pos < dl[k]) cp_async16(&st.dst[dst_r0 + 2 * k][dst_c], p.X + dz[k] + pos);
+                }
+                cp_async_arrive(&sm.full[stage]);
+                if (warp == kProducerWarp) {
+                    if (lane < kRows) {
+                        st.row_z[lane] = rz;
+                        st.row_l[lane] = rl;
+                    }
+                    __syncwarp();  // row table stores ordered before lane 0's release
+                    if (lane == 0) {
+                        st.i0 = i0;
+                        st.last = (last_tile && i0 + kCols >= tlen) ? 1 : 0;
+                        mbar_arrive(&sm.full[stage]);
+                    }
+                }
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
-            // direct side: row r is a run of kCols amplitudes at z_j + i0
-            const int c = tid & (kCols - 1);
-            const int rg = tid >> 6;
-            const uint64_t pos = i0 + c;
-            double2 xz[kRows / 4];
+        }
+    } else if (warp < kConsumerWarps) {
+        // ------------------------------------------------------------ consumers
+        int stage = 0;
+        uint32_t phase = 0;
+        uint64_t k = 0;  // chunk counter (norm buffer parity)
+        const int c = tid & (kCols - 1);
+        const int rg = tid >> 6;  // 4 row groups of 4 rows
+        bool more = blockIdx.x < p.ntiles;
+        while (more) {
+            mbar_wait(&sm.full[stage], phase);
+            TileStage& st = sm.stage[stage];
+            const uint64_t pos = st.i0 + c;
+            more = st.last == 0;
+            const int b = static_cast<int>(k & 1);
+            if (kProbs && k >= 2) named_sync(kNormEmpty0 + b, kConsumers + 32);
 #pragma unroll
-            for (int k = 0; k < kRows / 4; ++k) {
-                const int r = rg * (kRows / 4) + k;
-                xz[k] = pos < row_l[r] ? __ldg(p.X + row_z[r] + pos) : make_double2(0.0, 0.0);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < kRows / 4; ++k) {
-                const int r = rg * (kRows / 4) + k;
-                const bool live = pos < row_l[r];
+            for (int q = 0; q < kRows / 4; ++q) {
+                const int r = rg * (kRows / 4) + q;
+                const bool live = pos < st.row_l[r];
                 double h0r, h0i, h1r, h1i;
-                stage_pair(p.sc, xz[k], src_s[c][r], h0r, h0i, h1r, h1i);
+                stage_pair(p.sc, st.dst[r][c], st.src[c][r], h0r, h0i, h1r, h1i);
                 if (kProbs) {
-                    nrm[0][r][c] = live ? cnorm(h0r, h0i) : 0.0;
-                    nrm[kProbs ? 1 : 0][r][c] = live ? cnorm(h1r, h1i) : 0.0;
+                    sm.nrm[b][0][r][c] = live ? cnorm(h0r, h0i) : 0.0;
+                    sm.nrm[b][1][r][c] = live ? cnorm(h1r, h1i) : 0.0;
                 } else if (live) {
-                    p.Y[row_z[r] + pos] = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+                    p.Y[st.row_z[r] + pos] =
+                        p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
                 }
             }
-            __syncthreads();  // src_s / nrm complete; src_s free for the next chunk
-            if (kProbs) {
-                if (chain) {
-                    const uint64_t jrow = j0 + cr;
-                    double* head = p.head + (jrow * 2 + cg) * 256;
-                    for (int cc = 0; cc < kCols; ++cc) {
-                        const uint64_t q = i0 + cc;
-                        if (q >= c_len) break;
-                        const double n = nrm[cg][cr][cc];
-                        if (q < c_head) {
-                            head[q] = n;
-                        } else {
-                            c_s = __dadd_rn(c_s, n);
-                            const uint64_t z = c_z + q;
-                            if (((z + 1) & 255) == 0) {
-                                p.S[cg * p.nb + (z >> 8)] = c_s;
-                                window_add(win, c_s, digits[cg]);
-                                c_s = 0.0;
-                            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[stage]);
+            if (kProbs) named_arrive(kNormFull0 + b, kConsumers + 32);
+            ++k;
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        if (kProbs) {  // match the chain's releases of the last two norm buffers
+            if (k >= 2) named_sync(kNormEmpty0 + static_cast<int>(k & 1), kConsumers + 32);
+            if (k >= 1) named_sync(kNormEmpty0 + static_cast<int>((k + 1) & 1), kConsumers + 32);
+        }
+    } else if (kProbs && warp == kChainWarp) {
+        // ------------------------------------------------------------ chains
+        const int cr = lane & (kRows - 1), cg = lane >> 4;
+        DigitWindow win;
+        window_reset(win);
+        uint64_t k = 0;
+        for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            const uint64_t j0 = tile * kRows;
+            uint64_t c_z, c_len;
+            const uint64_t tlen = tile_rows(p, j0, lane, c_z, c_len);
+            const uint64_t c_head = (256 - (c_z & 255)) & 255;
+            double c_s = 0.0;
+            for (uint64_t i0 = 0; i0 < tlen; i0 += kCols, ++k) {
+                const int b = static_cast<int>(k & 1);
+                named_sync(kNormFull0 + b, kConsumers + 32);
+                const double* row = &sm.nrm[b][cg][cr][0];
+                if (i0 >= c_head && i0 + kCols <= c_len) {
+                    // interior chunk (the common case): 64 in-order adds, branch-free.
+                    // At most one block ends inside the chunk (kCols <= 256), at
+                    // column qb: the block's fold continues in `a`, the next block
+                    // starts in `nb` (0 + x == x exactly, as the reference's fold).
+                    const int qb = static_cast<int>(255 - ((c_z + i0) & 255));
+                    double a = c_s, nb = 0.0;
+#pragma unroll
+                    for (int cc = 0; cc < kCols; cc += 2) {
+                        const double2 x = *reinterpret_cast<const double2*>(row + cc);
+                        if (cc <= qb) a = __dadd_rn(a, x.x);
+                        else nb = __dadd_rn(nb, x.x);
+                        if (cc + 1 <= qb) a = __dadd_rn(a, x.y);
+                        else nb = __dadd_rn(nb, x.y);
+                    }
+                    if (qb < kCols) {
+                        p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = a;
+                        window_add(win, a, sm.digits[cg]);
+                        c_s = nb;
+                    } else {
+                        c_s = a;
+                    }
+                } else if (i0 < c_len) {
+                    // row start (head positions belong to the block shared with the
+                    // predecessor row, finished by k_tile_fixup) or row end
+                    const int q1 = static_cast<int>(min(c_len - i0, uint64_t(kCols)));
+                    int qa = 0;
+                    if (i0 < c_head) {
+                        qa = static_cast<int>(min(c_head - i0, uint64_t(q1)));
+                        double* head = p.head + ((j0 + cr) * 2 + cg) * 256 + i0;
+                        for (int cc = 0; cc < qa; ++cc) head[cc] = row[cc];
+                    }
+                    if (qa < q1) {
+                        const int qb = qa + static_cast<int>(255 - ((c_z + i0 + qa) & 255));
+                        if (qb < q1) {
+                            for (int cc = qa; cc <= qb; ++cc) c_s = __dadd_rn(c_s, row[cc]);
+                            p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = c_s;
+                            window_add(win, c_s, sm.digits[cg]);
+                            c_s = 0.0;
+                            qa = qb + 1;
                         }
+                        for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, row[cc]);
+                    }
+                }
+                __syncwarp();
+                named_arrive(kNormEmpty0 + b, kConsumers + 32);
+            }
+            if (c_len > 0) {
+                const uint64_t end = c_z + c_len;
+                if ((end & 255) != 0) {
+                    if (end == p.N) {  // the final (partial) block of Z_N
+                        p.S[cg * p.nb + ((p.N - 1) >> 8)] = c_s;
+                        window_add(win, c_s, sm.digits[cg]);
+                    } else {
+                        p.tail[tile_row_succ(j0 + cr, p) * 2 + cg] = c_s;
                     }
                 }
             }
         }
-        if (chain && c_len > 0) {
-            const uint64_t end = c_z + c_len;
-            if ((end & 255) != 0) {
-                if (end == p.N) {  // the final (partial) block of Z_N
-                    p.S[cg * p.nb + ((p.N - 1) >> 8)] = c_s;
-                    window_add(win, c_s, digits[cg]);
-                } else {
-                    p.tail[tile_row_succ(j0 + cr, p) * 2 + cg] = c_s;
-                }
-            }
-        }
+        window_flush(win, sm.digits[cg]);
     }
     if (kProbs) {
-        if (chain) window_flush(win, digits[cg]);
         __syncthreads();
-        write_partials(digits, p.partials + uint64_t(blockIdx.x) * 2 * kDigits, tid);
+        write_partials(sm.digits, p.partials + uint64_t(blockIdx.x) * 2 * kDigits, tid);
     }
 }
 

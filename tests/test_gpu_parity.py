@@ -317,10 +317,15 @@ def test_tile_plans_partition_and_auto_selection(cuda_ok):
     plan satisfy the three-gap partition (checked exhaustively at small N)."""
     for N, a in [(4294967213, 5), (268435247, 3), (16777207, 2)]:
         eng = engine(N, a)
+        pows = eng.stage_multipliers()
         for s in range(1, eng.t):
             pl = eng.tile_plan(s)
-            assert pl["tiled"], (N, s, pl)
-            assert pl["du"] >= 512 and pl["dv"] >= 512 and pl["H"] <= N // 1024
+            if pows[s] > 1 << 20:  # "random" multipliers; the last few (a^2^k small) may not tile
+                assert pl["tiled"], (N, s, pl)
+            if pl["tiled"]:
+                H = pl["H"]
+                assert pl["du"] >= 512 and pl["dv"] >= 512 and H <= N // 1024
+                assert pl["du"] + pl["dv"] <= 3 * (N // H + 1) and H >= 256
     N, a = 1048351, 12345
     eng = engine(N, a, 8, tiling="force")
     pows = eng.stage_multipliers()
