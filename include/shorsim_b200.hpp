@@ -1,0 +1,153 @@
+// shorsim_b200.hpp — C++ drop-in for the reference's engine API, over the C ABI.
+//
+// Include AFTER the reference's "shorsim/statevector.hpp" (it supplies
+// FactoringProblem, ErrorConfig, SimulatorOptions, RunResult and the exception
+// types of proj/include/shorsim/errors.hpp). Provides, in namespace
+// shorsim::b200, the reference's entry points with the same signatures and
+// exception behaviour:
+//   class IterativeShorEngine   — proj/include/shorsim/statevector.hpp:169-191
+//   run_iterative_shor          — statevector.hpp:164-165
+//   StepEngine (per-gate path)  — statevector.hpp:68-133 on the compressed state
+// A caller switches with one alias:
+//   namespace shorsim { using IterativeShorEngine = b200::IterativeShorEngine; }
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "shorsim_b200.h"
+
+namespace shorsim::b200 {
+
+// Map a status code to the reference's exception types (errors.hpp:8-43).
+inline void throw_status(int rc) {
+    if (rc == SHS_OK) return;
+    std::string msg = shs_last_error();
+    switch (rc) {
+        case SHS_CONFIG_ERROR: throw ConfigError(msg);
+        case SHS_CEILING_EXCEEDED: throw CeilingExceededError(msg);
+        case SHS_DEGENERATE_BRANCH: throw DegenerateBranchError(msg);
+        case SHS_BUDGET_EXCEEDED: throw BudgetExceededError(msg);
+        case SHS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case SHS_NOT_INVERTIBLE: {
+            // "not invertible: gcd(a, n) = g"
+            std::uint64_t a = 0, n = 0, g = 0;
+            auto p = msg.find("gcd(");
+            if (p != std::string::npos) {
+                a = std::stoull(msg.substr(p + 4));
+                n = std::stoull(msg.substr(msg.find(", ", p) + 2));
+                g = std::stoull(msg.substr(msg.rfind("= ") + 2));
+            }
+            throw NotInvertibleError(a, n, g);
+        }
+        default: throw Error(msg);  // SHS_ERROR (norm drift) and CUDA failures
+    }
+}
+
+inline shs_error to_c(const ErrorConfig& e) {
+    shs_error c{};
+    c.kind = static_cast<int32_t>(e.kind);
+    c.delta = e.delta;
+    if (e.pauli) {
+        c.px = e.pauli->px;
+        c.py = e.pauli->py;
+        c.pz = e.pauli->pz;
+        c.has_pauli = 1;
+    }
+    return c;
+}
+
+inline shs_options to_c(const SimulatorOptions& o, int device) {
+    shs_options c;
+    shs_default_options(&c);
+    c.shard_count = o.shard_count;
+    c.workers = o.workers;
+    c.qubit_ceiling = o.qubit_ceiling;
+    c.check_norms = o.check_norms ? 1 : 0;
+    c.device = device;
+    return c;
+}
+
+class IterativeShorEngine {
+public:
+    IterativeShorEngine(const FactoringProblem& problem, const ErrorConfig& error,
+                        const SimulatorOptions& options, int device = 0)
+        : t_(problem.t) {
+        shs_problem p{problem.N, problem.a, problem.L, problem.t, problem.seed};
+        shs_error e = to_c(error);
+        shs_options o = to_c(options, device);
+        throw_status(shs_engine_create(&p, &e, &o, &h_));
+        a_pows_.resize(t_);
+        throw_status(shs_engine_stage_multipliers(h_, a_pows_.data()));
+        trace_.resize(t_);
+    }
+    ~IterativeShorEngine() {
+        if (h_) shs_engine_destroy(h_);
+    }
+    IterativeShorEngine(const IterativeShorEngine&) = delete;
+    IterativeShorEngine& operator=(const IterativeShorEngine&) = delete;
+    IterativeShorEngine(IterativeShorEngine&& o) noexcept
+        : h_(std::exchange(o.h_, nullptr)), t_(o.t_), a_pows_(std::move(o.a_pows_)),
+          trace_(std::move(o.trace_)) {}
+
+    // IterativeShorEngine::run, statevector.cpp:323-412
+    RunResult run(u64 seed, u64 bitstring_index) {
+        std::uint64_t j[2], js[2];
+        throw_status(shs_engine_run(h_, seed, bitstring_index, j, js, trace_.data()));
+        RunResult r;
+        r.bits = BitString{t_, (u128{j[1]} << 64) | j[0]};
+        r.j_sampled = (u128{js[1]} << 64) | js[0];
+        r.trace.reserve(t_);
+        for (const auto& s : trace_)
+            r.trace.push_back(StageTrace{s.cbit, s.p1, s.sampled_bit, s.observed_bit,
+                                         ErrorEvent{s.classical_flip != 0,
+                                                    s.quantum_error_branch != 0}});
+        return r;
+    }
+
+    const std::vector<u64>& stage_multipliers() const { return a_pows_; }
+    shs_engine* handle() const { return h_; }
+
+private:
+    shs_engine* h_ = nullptr;
+    unsigned t_;
+    std::vector<u64> a_pows_;
+    std::vector<shs_stage_trace> trace_;
+};
+
+inline RunResult run_iterative_shor(const FactoringProblem& problem, const ErrorConfig& error,
+                                    u64 seed, u64 bitstring_index,
+                                    const SimulatorOptions& options) {
+    IterativeShorEngine engine(problem, error, options);
+    return engine.run(seed, bitstring_index);
+}
+
+// The per-gate ("step/measure") path for forced measurement sequences:
+// stage_probs = apply_oracle + apply_phase + apply_hadamard_top + the two group
+// norms; collapse = reset_top(src_group, reinit, p_source).
+class StepEngine {
+public:
+    explicit StepEngine(IterativeShorEngine& e) : h_(e.handle()) { throw_status(shs_state_init(h_)); }
+    std::pair<double, double> stage_probs(unsigned s, u128 prefix) {
+        double p0 = 0, p1 = 0;
+        throw_status(shs_stage_probs(h_, s, static_cast<std::uint64_t>(prefix),
+                                     static_cast<std::uint64_t>(prefix >> 64), &p0, &p1));
+        return {p0, p1};
+    }
+    void collapse(int src_group, double p_source) {
+        throw_status(shs_stage_collapse(h_, src_group, p_source));
+    }
+    std::vector<double> state(int x, u64 first, u64 count) {
+        std::vector<double> out(2 * count);
+        throw_status(shs_state_read(h_, x, first, count, out.data()));
+        return out;
+    }
+
+private:
+    shs_engine* h_;
+};
+
+}  // namespace shorsim::b200

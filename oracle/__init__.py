@@ -24,6 +24,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libshor_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libshorsim_ref.so")
 REFERENCE_SRC = "/root/reference/proj/src"
+SIMULATE_REF = os.path.join(HERE, "_ref", "simulate_ref")
+SIMULATE_B200 = os.path.join(HERE, "_ref", "simulate_b200")
+ACCEPTANCE_REF = os.path.join(HERE, "_ref", "acceptance_ref")
+ACCEPTANCE_B200 = os.path.join(HERE, "_ref", "acceptance_b200")
 
 u64 = C.c_uint64
 u32 = C.c_uint32
@@ -42,6 +46,9 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir(REFERENCE_SRC)
     if ref:
         targets.append("ref")
+        # the reference's own callers linked against the B200 engine (needs the lib built)
+        if os.path.exists(os.path.join(HERE, "..", "paper_2308_05047_b200", "libshorsim_b200.so")):
+            targets.append("link")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
