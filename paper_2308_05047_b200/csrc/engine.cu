@@ -452,6 +452,7 @@ TileParams tile_params_for(const shs_engine* e, uint32_t s) {
     p.A_sh = pl.A_sh;
     p.m = pl.m;
     p.m_sh = pl.m_sh;
+    p.m_chunk = mulmod(pl.m, kCols, e->N);
     p.H = pl.H;
     p.u = pl.u;
     p.v = pl.v;

@@ -46,7 +46,8 @@ constexpr int kProducers = 32 * kProducerWarps;
 constexpr int kProducerWarp = kConsumerWarps;                   // warps 8..11
 constexpr int kChainWarp = kConsumerWarps + kProducerWarps;     // warp 12 (probs only)
 constexpr int kCopiesPerProducer = kRows * kCols / kProducers;  // 8 per side
-constexpr int kNormFull0 = 1, kNormEmpty0 = 3;     // named barrier ids (2 buffers each)
+constexpr int kNormBufs = 4;                       // norm tiles in flight (chain slack)
+constexpr int kNormFull0 = 1, kNormEmpty0 = 1 + kNormBufs;  // named barrier ids
 constexpr int kNrmStride = kCols + 2;              // 16 B-aligned rows, conflict-free LDS.128
 
 struct TileParams {
@@ -55,6 +56,7 @@ struct TileParams {
     uint64_t N;
     uint64_t A, A_sh;   // z_j = j * A mod N
     uint64_t m, m_sh;   // src = j + i * m mod N
+    uint64_t m_chunk;   // kCols * m mod N: source advance per chunk
     uint64_t H, u, v, du, dv;
     uint64_t ntiles;
     StageScalars sc;
@@ -98,7 +100,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
@@ -147,7 +149,7 @@ struct __align__(16) TileStage {
 template <bool kProbs>
 struct TileSmem {
     TileStage stage[kStages];
-    double nrm[kProbs ? 2 : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
+    double nrm[kProbs ? kNormBufs : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
     uint64_t full[kStages], empty[kStages];
     unsigned long long digits[2][kDigits];
 };
@@ -204,20 +206,27 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         // table lives in lanes 0..15 of every producer warp (tile_rows) and is
         // fetched by shuffles.
         const int pt = tid - 32 * kProducerWarp;
+        const int r_src = pt & (kRows - 1);
         const int src_c0 = pt / kRows;
         const int dst_r0 = pt / kCols, dst_c = pt % kCols;
         int stage = 0;
         uint32_t phase = 0;
         for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const uint64_t j0 = tile * kRows;
-            uint64_t rz, rl;  // row (lane % kRows) of the tile: also this thread's source row
+            uint64_t rz, rl;  // row (lane % kRows) of the tile == this thread's source row
             const uint64_t tlen = tile_rows(p, j0, lane, rz, rl);
             const bool last_tile = tile + gridDim.x >= p.ntiles;
-            uint64_t dz[kCopiesPerProducer], dl[kCopiesPerProducer];
+            // source index of this thread's copies, advanced by kCols*m per chunk
+            uint64_t sidx[kCopiesPerProducer];
+            const double2* dptr[kCopiesPerProducer];
+            uint64_t dlen[kCopiesPerProducer];
 #pragma unroll
             for (int k = 0; k < kCopiesPerProducer; ++k) {
-                dz[k] = __shfl_sync(0xffffffffu, rz, dst_r0 + 2 * k);
-                dl[k] = __shfl_sync(0xffffffffu, rl, dst_r0 + 2 * k);
+                const uint64_t c = src_c0 + (kProducers / kRows) * k;
+                sidx[k] = addmod(j0 + r_src, mulmod_shoup(c, p.m, p.m_sh, p.N), p.N);
+                const uint64_t dz = __shfl_sync(0xffffffffu, rz, dst_r0 + 2 * k);
+                dlen[k] = __shfl_sync(0xffffffffu, rl, dst_r0 + 2 * k);
+                dptr[k] = p.X + dz + dst_c;
             }
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols) {
                 mbar_wait(&sm.empty[stage], phase ^ 1);
@@ -225,17 +234,13 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
 #pragma unroll
                 for (int k = 0; k < kCopiesPerProducer; ++k) {
                     const int c = src_c0 + (kProducers / kRows) * k;
-                    const uint64_t pos = i0 + c;
-                    if (pos < rl) {
-                        const uint64_t src =
-                            addmod(j0 + (pt & (kRows - 1)), mulmod_shoup(pos, p.m, p.m_sh, p.N), p.N);
-                        cp_async16(&st.src[c][pt & (kRows - 1)], p.X + src);
-                    }
+                    if (i0 + c < rl) cp_async16(&st.src[c][r_src], p.X + sidx[k]);
+                    sidx[k] = addmod(sidx[k], p.m_chunk, p.N);
                 }
 #pragma unroll
                 for (int k = 0; k < kCopiesPerProducer; ++k) {
-                    const uint64_t pos = i0 + dst_c;
-                    if (pos < dl[k]) cp_async16(&st.dst[dst_r0 + 2 * k][dst_c], p.X + dz[k] + pos);
+                    if (i0 + dst_c < dlen[k]) cp_async16(&st.dst[dst_r0 + 2 * k][dst_c], dptr[k]);
+                    dptr[k] += kCols;
                 }
                 cp_async_arrive(&sm.full[stage]);
                 if (warp == kProducerWarp) {
@@ -269,8 +274,8 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             TileStage& st = sm.stage[stage];
             const uint64_t pos = st.i0 + c;
             more = st.last == 0;
-            const int b = static_cast<int>(k & 1);
-            if (kProbs && k >= 2) named_sync(kNormEmpty0 + b, kConsumers + 32);
+            const int b = static_cast<int>(k % kNormBufs);
+            if (kProbs && k >= kNormBufs) named_sync(kNormEmpty0 + b, kConsumers + 32);
 #pragma unroll
             for (int q = 0; q < kRows / 4; ++q) {
                 const int r = rg * (kRows / 4) + q;
@@ -294,9 +299,9 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                 phase ^= 1;
             }
         }
-        if (kProbs) {  // match the chain's releases of the last two norm buffers
-            if (k >= 2) named_sync(kNormEmpty0 + static_cast<int>(k & 1), kConsumers + 32);
-            if (k >= 1) named_sync(kNormEmpty0 + static_cast<int>((k + 1) & 1), kConsumers + 32);
+        if (kProbs) {  // match the chain's releases of the last kNormBufs norm tiles
+            for (uint64_t q = (k > kNormBufs ? k - kNormBufs : 0); q < k; ++q)
+                named_sync(kNormEmpty0 + static_cast<int>(q % kNormBufs), kConsumers + 32);
         }
     } else if (kProbs && warp == kChainWarp) {
         // ------------------------------------------------------------ chains
@@ -311,23 +316,26 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             const uint64_t c_head = (256 - (c_z & 255)) & 255;
             double c_s = 0.0;
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols, ++k) {
-                const int b = static_cast<int>(k & 1);
+                const int b = static_cast<int>(k % kNormBufs);
                 named_sync(kNormFull0 + b, kConsumers + 32);
                 const double* row = &sm.nrm[b][cg][cr][0];
                 if (i0 >= c_head && i0 + kCols <= c_len) {
                     // interior chunk (the common case): 64 in-order adds, branch-free.
                     // At most one block ends inside the chunk (kCols <= 256), at
                     // column qb: the block's fold continues in `a`, the next block
-                    // starts in `nb` (0 + x == x exactly, as the reference's fold).
+                    // starts in `nb`. Each chain adds the value or +0.0, which leaves
+                    // a non-negative sum unchanged, so both folds are exactly the
+                    // reference's (s = 0; s += x ...); the masking is off the chains.
                     const int qb = static_cast<int>(255 - ((c_z + i0) & 255));
                     double a = c_s, nb = 0.0;
 #pragma unroll
                     for (int cc = 0; cc < kCols; cc += 2) {
                         const double2 x = *reinterpret_cast<const double2*>(row + cc);
-                        if (cc <= qb) a = __dadd_rn(a, x.x);
-                        else nb = __dadd_rn(nb, x.x);
-                        if (cc + 1 <= qb) a = __dadd_rn(a, x.y);
-                        else nb = __dadd_rn(nb, x.y);
+                        const bool lo0 = cc <= qb, lo1 = cc + 1 <= qb;
+                        a = __dadd_rn(a, lo0 ? x.x : 0.0);
+                        nb = __dadd_rn(nb, lo0 ? 0.0 : x.x);
+                        a = __dadd_rn(a, lo1 ? x.y : 0.0);
+                        nb = __dadd_rn(nb, lo1 ? 0.0 : x.y);
                     }
                     if (qb < kCols) {
                         p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = a;
