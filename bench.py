@@ -267,9 +267,21 @@ def run_ours(args):
     stage_dev_ms = sum(v["avg_ms"] for v in kernels.values())
     dom = max(("probs", "collapse"), key=lambda k: kernels[k]["avg_ms"])
     achieved = kernels[dom]["achieved_gbs"]
-    roofline = {"kernel": f"k_stage_{dom}", "bound": "hbm", "achieved": achieved,
+    tiled = eng.tile_plan(timed_stages[-1])["tiled"]
+    kname = {"probs": "k_tiled<1>" if tiled else "k_stage_probs<1,0>",
+             "collapse": "k_tiled<0>" if tiled else "k_stage_collapse<1,0>"}[dom]
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per amplitude from the committed ncu capture, scaled to this N
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")) as f:
+            ks = json.load(f)["kernels"][kname]
+        traffic = ks["dram_bytes_per_amp"] * N
+        traffic_src = f"profiles/r01/ncu_summary.json {kname} ({ks['version']}): " \
+                      f"{ks['dram_bytes_per_amp']} DRAM B/amp at n29 x N"
+    except (OSError, KeyError, ValueError):
+        pass
+    roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
                 "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": traffic, "traffic_source": traffic_src,
                 "share_of_step": kernels[dom]["avg_ms"] / ms_per_step,
                 "bytes_per_amp": per_amp[dom]}
 
