@@ -164,6 +164,11 @@ int shs_index_map(shs_engine* engine, uint32_t s, uint64_t first, uint64_t count
 int shs_sample_measurement(double p1, uint64_t seed, uint32_t idx, uint32_t stage,
                            const shs_error* error, int32_t out[4]);
 
+/* bitflip_bitstring with RngStream(seed, idx, 0, bitflip), statevector.cpp:404-409
+ * (host-side; used by drivers that assemble runs themselves, e.g. the sharded one):
+ * j = {lo, hi} updated in place */
+int shs_bitflip(uint64_t j[2], uint32_t t, double delta, uint64_t seed, uint32_t idx);
+
 /* ---- instrumentation (bench / profiling) ---- */
 /* Per-kernel CUDA-event timing on the engine's stream. kind: 0 probs, 1 combine,
  * 2 collapse. Returns accumulated milliseconds and launch counts since enable. */
@@ -179,6 +184,56 @@ void* shs_engine_stream(const shs_engine* engine);
 uint64_t shs_engine_launch_count(const shs_engine* engine);
 /* bytes of device memory the engine holds */
 uint64_t shs_engine_device_bytes(const shs_engine* engine);
+
+/* ---- sharded engine (one shard of the state per GPU; §8e) ----------------
+ * Shard q of G owns global amplitude indices [q*S, min(N, (q+1)*S)), S a
+ * multiple of 256. Each shard holds two buffers (sel and the exchange buffer P,
+ * swapping roles every stage) and needs every other shard's buffers: attach
+ * them as device pointers valid in this process (same process) or as CUDA IPC
+ * handles (one process per GPU). Per stage the driver runs, on every shard:
+ *   if shs_shard_needs_exchange(s): shs_shard_exchange(s); sync; barrier
+ *   shs_shard_probs(s, prefix, digits); allreduce-sum digits over shards;
+ *   shs_digits_to_probs(total) -> p0, p1; norm check; sample (same on all)
+ *   if s + 1 < t: shs_shard_collapse(bit, p_src); sync; barrier
+ * (paper_2308_05047_b200/sharded.py implements this driver for virtual shards
+ * in one process and for torch.distributed ranks). Results are bit-identical
+ * to the single engine with SHS_COMBINE_EXACT for every shard count. */
+typedef struct shs_shard shs_shard;
+#define SHS_MAX_SHARDS 16
+#define SHS_DIGITS 80 /* 2 groups x 40 x 32-bit digits (in uint64 words) */
+
+int shs_shard_create(const shs_problem* problem, const shs_error* error,
+                     const shs_options* options, uint32_t rank, uint32_t nshards,
+                     shs_shard** out);
+void shs_shard_destroy(shs_shard* shard);
+/* out = {lo, hi, S} */
+int shs_shard_range(const shs_shard* shard, uint64_t out[3]);
+/* this shard's two device buffers (allocated at create) */
+int shs_shard_buffers(const shs_shard* shard, void* out[2]);
+/* CUDA IPC handles of the two buffers: out receives 2 x 64 bytes */
+int shs_shard_ipc_handles(const shs_shard* shard, void* out);
+int shs_shard_attach(shs_shard* shard, uint32_t peer, void* const bufs[2]);
+int shs_shard_attach_ipc(shs_shard* shard, uint32_t peer, const void* handles);
+int shs_shard_init(shs_shard* shard);
+int shs_shard_needs_exchange(const shs_shard* shard, uint32_t s);
+int shs_shard_exchange(shs_shard* shard, uint32_t s);
+int shs_shard_probs(shs_shard* shard, uint32_t s, uint64_t prefix_lo, uint64_t prefix_hi,
+                    uint64_t digits[SHS_DIGITS]);
+int shs_shard_collapse(shs_shard* shard, int32_t src_group, double p_source);
+int shs_shard_sync(shs_shard* shard);
+/* amplitudes (global indices; zero outside this shard), as shs_state_read / shs_stage_read */
+int shs_shard_state_read(shs_shard* shard, int32_t x, uint64_t first, uint64_t count,
+                         double* interleaved);
+int shs_shard_stage_read(shs_shard* shard, int32_t x, uint64_t first, uint64_t count,
+                         double* interleaved);
+/* correctly rounded p0, p1 from summed exact digits (host-side, no device) */
+int shs_digits_to_probs(const uint64_t digits[SHS_DIGITS], double* p0, double* p1);
+/* per-kernel CUDA-event times like shs_engine_kernel_times: kind 0 probs,
+ * 1 exchange, 2 collapse */
+int shs_shard_set_timing(shs_shard* shard, int32_t enable);
+int shs_shard_kernel_times(const shs_shard* shard, double ms[3], uint64_t launches[3]);
+uint64_t shs_shard_launch_count(const shs_shard* shard);
+void* shs_shard_stream(const shs_shard* shard);
 
 /* thread-local message of the last failing call */
 const char* shs_last_error(void);

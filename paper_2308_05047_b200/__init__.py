@@ -29,3 +29,4 @@ from .engine import (  # noqa: F401
     run_iterative_shor,
     sample_measurement,
 )
+from .sharded import DistGroup, LocalGroup, Shard, ShardedShorEngine, digits_to_probs  # noqa: F401

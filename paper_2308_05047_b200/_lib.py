@@ -28,6 +28,8 @@ SHS_INVALID_ARGUMENT = 7
 SHS_CUDA_ERROR = 8
 
 COMBINE = {"auto": 0, "kahan": 1, "exact": 2}
+SHS_DIGITS = 80
+MAX_SHARDS = 16
 TILING = {"auto": 0, "force": 1, "off": 2}
 
 
@@ -71,12 +73,34 @@ SIGNATURES = [
     ("shs_index_map", C.c_int, [vp, u32, u64, u64, C.POINTER(u64)]),
     ("shs_sample_measurement", C.c_int, [dbl, u64, u32, u32, C.POINTER(shs_error),
                                          C.POINTER(i32)]),
+    ("shs_bitflip", C.c_int, [C.POINTER(u64), u32, dbl, u64, u32]),
     ("shs_engine_set_timing", C.c_int, [vp, i32]),
     ("shs_engine_kernel_times", C.c_int, [vp, C.POINTER(dbl), C.POINTER(u64)]),
     ("shs_stage_tile_plan", C.c_int, [vp, u32, C.POINTER(u64)]),
     ("shs_engine_stream", vp, [vp]),
     ("shs_engine_launch_count", u64, [vp]),
     ("shs_engine_device_bytes", u64, [vp]),
+    ("shs_shard_create", C.c_int, [C.POINTER(shs_problem), C.POINTER(shs_error),
+                                   C.POINTER(shs_options), u32, u32, C.POINTER(vp)]),
+    ("shs_shard_destroy", None, [vp]),
+    ("shs_shard_range", C.c_int, [vp, C.POINTER(u64)]),
+    ("shs_shard_buffers", C.c_int, [vp, C.POINTER(vp)]),
+    ("shs_shard_ipc_handles", C.c_int, [vp, C.c_void_p]),
+    ("shs_shard_attach", C.c_int, [vp, u32, C.POINTER(vp)]),
+    ("shs_shard_attach_ipc", C.c_int, [vp, u32, C.c_void_p]),
+    ("shs_shard_init", C.c_int, [vp]),
+    ("shs_shard_needs_exchange", C.c_int, [vp, u32]),
+    ("shs_shard_exchange", C.c_int, [vp, u32]),
+    ("shs_shard_probs", C.c_int, [vp, u32, u64, u64, C.POINTER(u64)]),
+    ("shs_shard_collapse", C.c_int, [vp, i32, dbl]),
+    ("shs_shard_sync", C.c_int, [vp]),
+    ("shs_shard_state_read", C.c_int, [vp, i32, u64, u64, C.POINTER(dbl)]),
+    ("shs_shard_stage_read", C.c_int, [vp, i32, u64, u64, C.POINTER(dbl)]),
+    ("shs_digits_to_probs", C.c_int, [C.POINTER(u64), C.POINTER(dbl), C.POINTER(dbl)]),
+    ("shs_shard_set_timing", C.c_int, [vp, i32]),
+    ("shs_shard_kernel_times", C.c_int, [vp, C.POINTER(dbl), C.POINTER(u64)]),
+    ("shs_shard_launch_count", u64, [vp]),
+    ("shs_shard_stream", vp, [vp]),
     ("shs_last_error", C.c_char_p, []),
     ("shs_build_info", C.c_char_p, []),
 ]

@@ -31,18 +31,14 @@
 #include "../../include/shorsim_b200.h"
 #include "device_math.cuh"
 #include "host_model.hpp"
+#include "stage_kernels.cuh"
+#include "tile_plan.hpp"
 #include "tiled.cuh"
 
 using namespace shs;
 
 namespace {
 
-thread_local std::string g_last_error;
-
-int set_error(int code, const std::string& msg) {
-    g_last_error = msg;
-    return code;
-}
 
 #define SHS_CUDA(call)                                                                  \
     do {                                                                                \
@@ -53,272 +49,6 @@ int set_error(int code, const std::string& msg) {
     } while (0)
 
 constexpr double kNormTolerance = 1e-9;     // statevector.cpp:18
-constexpr double kDegenerateMass = 1e-300;  // statevector.cpp:19
-constexpr uint64_t kKahanMaxBlocks = 1024;  // AUTO: sequential Kahan up to 2^18 amplitudes
-constexpr uint64_t kTileAutoMinN = 1ull << 20;  // AUTO tiling from 16 MB of state
-constexpr uint64_t kTileMinRow = 512;           // every 256-block touches <= 2 rows
-constexpr uint64_t kTileMaxRows = 1ull << 18;   // head scratch <= 1 GB
-constexpr uint64_t kTileMinRowsPlan = 256;      // >= 16 tiles of kRows rows
-
-// Host side of a stage's sorted-residue tiling (see tiled.cuh).
-struct TilePlanHost {
-    bool tiled = false;
-    uint64_t H = 0, u = 0, v = 0, du = 0, dv = 0;
-    uint64_t A = 0, A_sh = 0, m = 0, m_sh = 0, ntiles = 0;
-};
-
-// Pick the largest row count H (powers of two and 3 * 2^k up to N/1024) whose
-// three gap lengths are all >= kTileMinRow and at most 3x the mean row: one
-// O(H) scan of j*A mod N with running argmin / argmax gives u(H), v(H) for
-// every candidate. Multipliers without such an H (tiny A, or A/N with a huge
-// partial quotient) keep the direct gather, whose warps then read a few long
-// runs anyway.
-TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling) {
-    TilePlanHost pl;
-    if (tiling == SHS_TILING_OFF || A == 1) return pl;
-    if (tiling == SHS_TILING_AUTO && N < kTileAutoMinN) return pl;
-    const uint64_t hmax = std::min<uint64_t>(N / 1024, kTileMaxRows);
-    std::vector<uint64_t> cands;
-    for (uint64_t h = 2; h <= hmax; h *= 2) {
-        cands.push_back(h);
-        if (h >= 4 && h / 2 * 3 <= hmax) cands.push_back(h / 2 * 3);
-    }
-    std::sort(cands.begin(), cands.end());
-    uint64_t j = 1, r = 0, umin = N, uj = 0, vmax = 0, vj = 0;
-    for (uint64_t H : cands) {
-        for (; j < H; ++j) {
-            r += A;
-            if (r >= N) r -= N;
-            if (r < umin) { umin = r; uj = j; }
-            if (r > vmax) { vmax = r; vj = j; }
-        }
-        const uint64_t du = umin, dv = N - vmax;
-        // rows must be long enough (each 256-block touches <= 2 rows) and balanced
-        // (the longest row, du + dv, within 3x the mean N / H), else a tile idles SMs
-        if (H >= kTileMinRowsPlan && du >= kTileMinRow && dv >= kTileMinRow &&
-            du + dv <= 3 * (N / H + 1)) {
-            pl.tiled = true;
-            pl.H = H;
-            pl.u = uj;
-            pl.v = vj;
-            pl.du = du;
-            pl.dv = dv;
-        }
-    }
-    if (pl.tiled) {
-        pl.A = A;
-        pl.A_sh = shoup(A, N);
-        pl.m = m;
-        pl.m_sh = shoup(m, N);
-        pl.ntiles = (pl.H + kRows - 1) / kRows;
-    }
-    return pl;
-}
-
-struct StageParams {
-    const double2* X;
-    double2* Y;
-    uint64_t N;
-    uint64_t m;       // a_inv of the stage
-    uint64_t m_sh;    // Shoup companion of m
-    uint64_t m_step;  // kBlock * m mod N: source advance per thread element
-    StageScalars sc;
-    double* S;        // block partials: S0 [0, nb), S1 [nb, 2 nb)
-    uint64_t nb;
-    unsigned long long* partials;  // [gridDim.x][2][kDigits]
-    uint64_t nchunks;
-    int sel;          // collapse: group kept
-};
-
-template <bool kE1>
-__device__ __forceinline__ double2 load_amp(const double2* __restrict__ X, uint64_t z) {
-    if (kE1) return make_double2(z == 1 ? 1.0 : 0.0, 0.0);  // run start: sel = e_1, inv = 1
-    return __ldg(X + z);
-}
-
-// Amplitude pairs (sel[z], sel[src z]) for the kPer elements z0 + e*kBlock of one thread.
-template <bool kGather, bool kE1>
-__device__ __forceinline__ void load_pairs(const StageParams& p, uint64_t z0, double2 (&xa)[kPer],
-                                           double2 (&xs)[kPer]) {
-    uint64_t src = kGather ? mulmod_shoup(z0, p.m, p.m_sh, p.N) : 0;
-#pragma unroll
-    for (int e = 0; e < kPer; ++e) {
-        const uint64_t z = z0 + uint64_t(e) * kBlock;
-        if (z < p.N) {
-            xa[e] = load_amp<kE1>(p.X, z);
-            xs[e] = kGather ? load_amp<kE1>(p.X, src) : xa[e];
-        } else {
-            xa[e] = make_double2(0.0, 0.0);
-            xs[e] = xa[e];
-        }
-        if (kGather) src = addmod(src, p.m_step, p.N);
-    }
-}
-
-template <bool kGather, bool kE1>
-__global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
-    __shared__ double nrm[2 * kPer][kBlock + 1];  // +1: conflict-free column walks
-    __shared__ unsigned long long digits[2][kDigits];
-    const int tid = threadIdx.x;
-    for (int i = tid; i < 2 * kDigits; i += kThreads) (&digits[0][0])[i] = 0ull;
-    DigitWindow win;
-    window_reset(win);
-    __syncthreads();
-
-    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
-        const uint64_t z0 = c * kChunk + tid;
-        double2 xa[kPer], xs[kPer];
-        load_pairs<kGather, kE1>(p, z0, xa, xs);
-#pragma unroll
-        for (int e = 0; e < kPer; ++e) {
-            double h0r, h0i, h1r, h1i;
-            stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
-            const bool live = z0 + uint64_t(e) * kBlock < p.N;
-            nrm[e][tid] = live ? cnorm(h0r, h0i) : 0.0;
-            nrm[kPer + e][tid] = live ? cnorm(h1r, h1i) : 0.0;
-        }
-        __syncthreads();
-        if (tid < 2 * kPer) {
-            // one lane per (block, group): the reference's in-order block sum
-            double s = 0.0;
-#pragma unroll 16
-            for (int i = 0; i < kBlock; ++i) s = __dadd_rn(s, nrm[tid][i]);
-            const uint64_t b = c * kPer + (tid & (kPer - 1));
-            const int g = tid / kPer;
-            if (b < p.nb) {
-                p.S[g * p.nb + b] = s;
-                window_add(win, s, digits[g]);
-            }
-        }
-        __syncthreads();
-    }
-    if (tid < 2 * kPer) window_flush(win, digits[tid / kPer]);
-    __syncthreads();
-    if (tid < 2) {
-        unsigned long long carry = 0;
-        unsigned long long* out = p.partials + (uint64_t(blockIdx.x) * 2 + tid) * kDigits;
-        for (int i = 0; i < kDigits; ++i) {
-            unsigned long long v = digits[tid][i] + carry;
-            out[i] = v & 0xffffffffull;
-            carry = v >> 32;
-        }
-    }
-}
-
-// p0/p1 from the stage. kahan: reference combine_blocks (statevector.cpp:32-40),
-// two interleaved sequential chains, zeros skipped; else exact sum of partials.
-__global__ void k_finalize(const unsigned long long* __restrict__ partials, int nparts,
-                           const double* __restrict__ S, uint64_t nb, int kahan,
-                           double* __restrict__ out) {
-    __shared__ unsigned long long acc[2][kDigits];
-    if (kahan) {
-        if (threadIdx.x == 0) {
-            double s0 = 0, c0 = 0, s1 = 0, c1 = 0;
-            for (uint64_t b = 0; b < nb; ++b) {
-                const double x0 = S[b], x1 = S[nb + b];
-                if (x0 != 0.0) {
-                    double y = __dsub_rn(x0, c0);
-                    double t = __dadd_rn(s0, y);
-                    c0 = __dsub_rn(__dsub_rn(t, s0), y);
-                    s0 = t;
-                }
-                if (x1 != 0.0) {
-                    double y = __dsub_rn(x1, c1);
-                    double t = __dadd_rn(s1, y);
-                    c1 = __dsub_rn(__dsub_rn(t, s1), y);
-                    s1 = t;
-                }
-            }
-            out[0] = s0;
-            out[1] = s1;
-        }
-        return;
-    }
-    for (int i = threadIdx.x; i < 2 * kDigits; i += blockDim.x) {
-        unsigned long long s = 0;
-        for (int c = 0; c < nparts; ++c) s += partials[uint64_t(c) * 2 * kDigits + i];
-        (&acc[0][0])[i] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < 2) out[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
-}
-
-template <bool kGather, bool kE1>
-__global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
-    const int tid = threadIdx.x;
-    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
-        const uint64_t z0 = c * kChunk + tid;
-        double2 xa[kPer], xs[kPer];
-        load_pairs<kGather, kE1>(p, z0, xa, xs);
-#pragma unroll
-        for (int e = 0; e < kPer; ++e) {
-            const uint64_t z = z0 + uint64_t(e) * kBlock;
-            double h0r, h0i, h1r, h1i;
-            stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
-            if (z < p.N) p.Y[z] = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
-        }
-    }
-}
-
-// Post-Hadamard amplitudes of group x for y in [first, first + count).
-template <bool kGather, bool kE1>
-__global__ void k_stage_read(StageParams p, int x, uint64_t first, uint64_t count,
-                             double2* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t z = first + i;
-        if (z >= p.N) {
-            out[i] = make_double2(0.0, 0.0);
-            continue;
-        }
-        const uint64_t src = kGather ? mulmod_shoup(z, p.m, p.m_sh, p.N) : z;
-        double2 xa = load_amp<kE1>(p.X, z), xs = load_amp<kE1>(p.X, src);
-        double h0r, h0i, h1r, h1i;
-        stage_pair(p.sc, xa, xs, h0r, h0i, h1r, h1i);
-        out[i] = x ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
-    }
-}
-
-// g_x[y] = w_x * (sel[y] * inv), the reference state after init / reset_top.
-template <bool kE1>
-__global__ void k_state_read(const double2* __restrict__ X, uint64_t N, double wr, double wi,
-                             double inv, uint64_t first, uint64_t count,
-                             double2* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t z = first + i;
-        if (z >= N) {
-            out[i] = make_double2(0.0, 0.0);
-            continue;
-        }
-        double2 v = load_amp<kE1>(X, z);
-        double r, im;
-        cmul(wr, wi, __dmul_rn(v.x, inv), __dmul_rn(v.y, inv), r, im);
-        out[i] = make_double2(r, im);
-    }
-}
-
-// The index map exactly as the stage kernels walk it (Shoup per thread, then
-// incremental), written out for the bit-exact index-map parity check.
-__global__ void k_index_map(StageParams p, uint64_t chunk0, uint64_t nchunk, uint64_t first,
-                            uint64_t count, uint64_t* __restrict__ out) {
-    for (uint64_t c = chunk0 + blockIdx.x; c < chunk0 + nchunk; c += gridDim.x) {
-        const uint64_t z0 = c * kChunk + threadIdx.x;
-        uint64_t src = mulmod_shoup(z0, p.m, p.m_sh, p.N);
-#pragma unroll
-        for (int e = 0; e < kPer; ++e) {
-            const uint64_t z = z0 + uint64_t(e) * kBlock;
-            if (z >= first && z < first + count && z < p.N) out[z - first] = src;
-            src = addmod(src, p.m_step, p.N);
-        }
-    }
-}
-
-__global__ void k_fill_identity(uint64_t first, uint64_t count, uint64_t* __restrict__ out) {
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
-         i += uint64_t(gridDim.x) * blockDim.x)
-        out[i] = first + i;
-}
 
 }  // namespace
 
@@ -429,8 +159,11 @@ int sync(shs_engine* e) {
 StageParams params_for(const shs_engine* e, uint32_t s) {
     StageParams p{};
     p.X = e->X;
+    p.Xs = nullptr;
     p.Y = e->Y;
     p.N = e->N;
+    p.z0 = 0;
+    p.zend = e->N;
     p.m = e->a_invs[s];
     p.m_sh = e->a_pows[s] != 1 ? shoup(p.m, e->N) : 0;
     p.m_step = e->a_pows[s] != 1 ? mulmod(p.m, kBlock, e->N) : 0;
@@ -474,40 +207,12 @@ int grid_for(const shs_engine* e) {
 
 template <bool G, bool E1>
 void launch_probs(shs_engine* e, const StageParams& p) {
-    k_stage_probs<G, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
+    k_stage_probs<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
 }
 
 template <bool G, bool E1>
 void launch_collapse(shs_engine* e, const StageParams& p) {
-    k_stage_collapse<G, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
-}
-
-int engine_validate(const shs_problem& pr, const shs_error& er, const shs_options& o) {
-    std::string why;
-    if (validate_error(er, &why)) return set_error(SHS_CONFIG_ERROR, why);  // :289
-    unsigned n = pr.L + 1;
-    if (n > o.qubit_ceiling)  // statevector.cpp:291-294
-        return set_error(SHS_CEILING_EXCEEDED, "simulator: n = " + std::to_string(n) +
-                                                   " exceeds qubit ceiling " +
-                                                   std::to_string(o.qubit_ceiling));
-    // make_shard_layout (statevector.cpp:65-72); the n <= 33 cap of the u32
-    // reference layout is lifted (indices are u64 here, N < 2^63).
-    if (n < 2) return set_error(SHS_INVALID_ARGUMENT, "shard layout: need 2 <= n");
-    if (o.shard_count < 2 || (o.shard_count & (o.shard_count - 1)) != 0)
-        return set_error(SHS_INVALID_ARGUMENT,
-                         "shard layout: shard count must be a power of two >= 2");
-    if (static_cast<unsigned>(__builtin_ctz(o.shard_count)) > n - 1)
-        return set_error(SHS_INVALID_ARGUMENT, "shard layout: more shards than group states");
-    if (pr.N < 2) return set_error(SHS_INVALID_ARGUMENT, "modulus must be >= 2");
-    if (pr.L > 62) return set_error(SHS_INVALID_ARGUMENT, "L > 62 unsupported (N < 2^63)");
-    if (pr.N > (u64{1} << pr.L))
-        return set_error(SHS_INVALID_ARGUMENT, "N exceeds 2^L: L must be at least bit_length(N)");
-    if (pr.t < 1 || pr.t > 127) return set_error(SHS_INVALID_ARGUMENT, "t must be in [1, 127]");
-    if (o.combine < SHS_COMBINE_AUTO || o.combine > SHS_COMBINE_EXACT)
-        return set_error(SHS_INVALID_ARGUMENT, "unknown combine mode");
-    if (o.tiling < SHS_TILING_AUTO || o.tiling > SHS_TILING_OFF)
-        return set_error(SHS_INVALID_ARGUMENT, "unknown tiling mode");
-    return SHS_OK;
+    k_stage_collapse<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
 }
 
 void release(shs_engine* e) {
@@ -710,7 +415,7 @@ void shs_default_options(shs_options* o) {
     o->tiling = SHS_TILING_AUTO;
 }
 
-const char* shs_last_error(void) { return g_last_error.c_str(); }
+const char* shs_last_error(void) { return last_error(); }
 
 const char* shs_build_info(void) {
     return "shorsim_b200: sm_100a, fp64 no-FMA (--fmad=false), nvcc " SHS_NVCC_VERSION;
@@ -722,7 +427,7 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     shs_options o;
     if (options) o = *options;
     else shs_default_options(&o);
-    int rc = engine_validate(*problem, *error, o);
+    int rc = validate_engine_config(*problem, *error, o);
     if (rc) return rc;
     auto* e = new shs_engine;
     e->prob = *problem;
@@ -785,7 +490,7 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     }
     e->num_sms = prop.multiProcessorCount;
     int occ = 0;
-    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<true, false>, kThreads, 0);
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcGather, false>, kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     e->grid_cap = std::max(1, occ) * e->num_sms;
     // one persistent TMA-pipelined CTA per SM for the tiled passes
@@ -878,11 +583,11 @@ int shs_stage_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
         const int grid = static_cast<int>(std::min<uint64_t>((count + 255) / 256, 4096));
         int rc = launch(e, -1, [&] {
             if (gather) {
-                if (e->e1) k_stage_read<true, true><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
-                else k_stage_read<true, false><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
+                if (e->e1) k_stage_read<kSrcGather, true><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
+                else k_stage_read<kSrcGather, false><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
             } else {
-                if (e->e1) k_stage_read<false, true><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
-                else k_stage_read<false, false><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
+                if (e->e1) k_stage_read<kSrcDirect, true><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
+                else k_stage_read<kSrcDirect, false><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
             }
         });
         if (rc) return rc;
@@ -903,8 +608,8 @@ int shs_state_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
         const int grid = static_cast<int>(std::min<uint64_t>((count + 255) / 256, 4096));
         const double wr = e->w[2 * x], wi = e->w[2 * x + 1];
         int rc = launch(e, -1, [&] {
-            if (e->e1) k_state_read<true><<<grid, 256, 0, e->stream>>>(e->X, e->N, wr, wi, e->inv, first, count, d);
-            else k_state_read<false><<<grid, 256, 0, e->stream>>>(e->X, e->N, wr, wi, e->inv, first, count, d);
+            if (e->e1) k_state_read<true><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, first, count, d);
+            else k_state_read<false><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, first, count, d);
         });
         if (rc) return rc;
         SHS_CUDA(cudaMemcpyAsync(host, d, sizeof(double2) * count, cudaMemcpyDeviceToHost,
@@ -974,6 +679,14 @@ int shs_sample_measurement(double p1, uint64_t seed, uint32_t idx, uint32_t stag
     out[1] = m.observed_bit;
     out[2] = m.error_branch ? 1 : 0;
     out[3] = m.classical_flip ? 1 : 0;
+    return SHS_OK;
+}
+
+int shs_bitflip(uint64_t j[2], uint32_t t, double delta, uint64_t seed, uint32_t idx) {
+    if (!j) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    u128 v = bitflip_bitstring((u128{j[1]} << 64) | j[0], t, delta, seed, idx);
+    j[0] = static_cast<uint64_t>(v);
+    j[1] = static_cast<uint64_t>(v >> 64);
     return SHS_OK;
 }
 

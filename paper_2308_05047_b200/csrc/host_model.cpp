@@ -136,6 +136,72 @@ Measurement sample_measurement(double p1, u64 seed, u32 idx, u32 stage, const sh
     return m;
 }
 
+namespace {
+thread_local std::string g_last_error;
+}  // namespace
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+const char* last_error() { return g_last_error.c_str(); }
+
+int validate_engine_config(const shs_problem& pr, const shs_error& er, const shs_options& o) {
+    std::string why;
+    if (validate_error(er, &why)) return set_error(SHS_CONFIG_ERROR, why);  // :289
+    unsigned n = pr.L + 1;
+    if (n > o.qubit_ceiling)  // statevector.cpp:291-294
+        return set_error(SHS_CEILING_EXCEEDED, "simulator: n = " + std::to_string(n) +
+                                                   " exceeds qubit ceiling " +
+                                                   std::to_string(o.qubit_ceiling));
+    // make_shard_layout (statevector.cpp:65-72); the n <= 33 cap of the u32
+    // reference layout is lifted (indices are u64 here, N < 2^63).
+    if (n < 2) return set_error(SHS_INVALID_ARGUMENT, "shard layout: need 2 <= n");
+    if (o.shard_count < 2 || (o.shard_count & (o.shard_count - 1)) != 0)
+        return set_error(SHS_INVALID_ARGUMENT,
+                         "shard layout: shard count must be a power of two >= 2");
+    if (static_cast<unsigned>(__builtin_ctz(o.shard_count)) > n - 1)
+        return set_error(SHS_INVALID_ARGUMENT, "shard layout: more shards than group states");
+    if (pr.N < 2) return set_error(SHS_INVALID_ARGUMENT, "modulus must be >= 2");
+    if (pr.L > 62) return set_error(SHS_INVALID_ARGUMENT, "L > 62 unsupported (N < 2^63)");
+    if (pr.N > (u64{1} << pr.L))
+        return set_error(SHS_INVALID_ARGUMENT, "N exceeds 2^L: L must be at least bit_length(N)");
+    if (pr.t < 1 || pr.t > 127) return set_error(SHS_INVALID_ARGUMENT, "t must be in [1, 127]");
+    if (o.combine < SHS_COMBINE_AUTO || o.combine > SHS_COMBINE_EXACT)
+        return set_error(SHS_INVALID_ARGUMENT, "unknown combine mode");
+    if (o.tiling < SHS_TILING_AUTO || o.tiling > SHS_TILING_OFF)
+        return set_error(SHS_INVALID_ARGUMENT, "unknown tiling mode");
+    return SHS_OK;
+}
+
+
+double digits_to_double_host(std::uint64_t* acc) {
+    constexpr int kDigitsN = 40, kAnchorBits = 1088;
+    std::uint64_t carry = 0;
+    for (int i = 0; i < kDigitsN; ++i) {
+        std::uint64_t v = acc[i] + carry;
+        acc[i] = v & 0xffffffffull;
+        carry = v >> 32;
+    }
+    int top = -1;
+    for (int i = kDigitsN - 1; i >= 0 && top < 0; --i)
+        if (acc[i]) top = i * 32 + 63 - __builtin_clzll(acc[i]);
+    if (top < 0) return 0.0;
+    auto bit = [&](int p) -> int {
+        return p >= 0 ? static_cast<int>((acc[p >> 5] >> (p & 31)) & 1ull) : 0;
+    };
+    int lsb = top - 52;
+    if (lsb < kAnchorBits - 1074) lsb = kAnchorBits - 1074;
+    std::uint64_t mant = 0;
+    for (int p = top; p >= lsb; --p) mant = (mant << 1) | static_cast<std::uint64_t>(bit(p));
+    const int round = bit(lsb - 1);
+    int sticky = 0;
+    for (int p = lsb - 2; p >= 0 && !sticky; --p) sticky = bit(p);
+    if (round && (sticky || (mant & 1ull))) ++mant;
+    return std::ldexp(static_cast<double>(mant), lsb - kAnchorBits);
+}
+
 u128 bitflip_bitstring(u128 j, unsigned t, double delta, u64 seed, u32 idx) {
     for (unsigned i = 0; i < t; ++i)
         if (rng_double(seed, idx, 0, kDomainBitflip, i) < delta) j ^= u128{1} << i;

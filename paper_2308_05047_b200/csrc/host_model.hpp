@@ -50,4 +50,16 @@ Measurement sample_measurement(double p1, u64 seed, u32 idx, u32 stage, const sh
 // bitflip_bitstring with RngStream(seed, idx, 0, bitflip), statevector.cpp:406-409
 u128 bitflip_bitstring(u128 j, unsigned t, double delta, u64 seed, u32 idx);
 
+// thread-local last error shared by every C-ABI entry point (shs_last_error)
+int set_error(int code, const std::string& msg);
+const char* last_error();
+
+// IterativeShorEngine construction checks in the reference's order
+// (statevector.cpp:289-295, :65-72), plus this engine's own limits
+int validate_engine_config(const shs_problem& pr, const shs_error& er, const shs_options& o);
+
+// correctly rounded (nearest-even) value of an exact 40-digit accumulator
+// (value = F * 2^-1088, 32-bit digits in uint64 words); normalises in place
+double digits_to_double_host(std::uint64_t* digits);
+
 }  // namespace shs

@@ -1,0 +1,262 @@
+// Direct (untiled) stage kernels, shared by the single-GPU engine (engine.cu)
+// and the sharded engine (shard.cu).
+//
+// Each kernel walks amplitude indices z in [z0, zend) — the whole of Z_N for the
+// single engine, one shard for the sharded engine — in chunks of kChunk (8
+// reduction blocks), with local buffer offsets z - z0 (z0 is a multiple of 256,
+// so the reference's fixed 256-blocks never straddle a shard). The gathered
+// side of the permutation comes from one of three sources:
+//   kSrcGather  sel[src z], src z = a_inv * z mod N (Shoup once per thread, then
+//               add / conditional subtract) — single engine only (z0 = 0)
+//   kSrcDirect  sel[z] itself (identity stage: a_pow = 1)
+//   kSrcBuffer  P[z - z0], the value a separate exchange already gathered
+// and kE1 replaces sel by the implicit run start e_1 (no memory traffic).
+#pragma once
+
+#include "device_math.cuh"
+
+namespace shs {
+
+enum SrcMode : int { kSrcGather = 0, kSrcDirect = 1, kSrcBuffer = 2 };
+
+struct StageParams {
+    const double2* X;   // sel over [z0, zend), local index z - z0
+    const double2* Xs;  // kSrcBuffer: gathered values, local index z - z0
+    double2* Y;         // collapse output, local index z - z0 (may alias Xs)
+    uint64_t N, z0, zend;
+    uint64_t m;       // a_inv of the stage
+    uint64_t m_sh;    // Shoup companion of m
+    uint64_t m_step;  // kBlock * m mod N: source advance per thread element
+    StageScalars sc;
+    double* S;        // local block partials: S0 [0, nb), S1 [nb, 2 nb)
+    uint64_t nb;
+    unsigned long long* partials;  // [gridDim.x][2][kDigits]
+    uint64_t nchunks;
+    int sel;          // collapse: group kept
+};
+
+// amplitude at GLOBAL index z; under kE1 the run-start state e_1 (inv = 1)
+template <bool kE1>
+__device__ __forceinline__ double2 load_amp(const double2* __restrict__ X, uint64_t z,
+                                            uint64_t z0) {
+    if (kE1) return make_double2(z == 1 ? 1.0 : 0.0, 0.0);
+    return __ldg(X + (z - z0));
+}
+
+// (sel[z], gathered[z]) for the kPer elements zg + e*kBlock of one thread
+template <int kMode, bool kE1>
+__device__ __forceinline__ void load_pairs(const StageParams& p, uint64_t zg, double2 (&xa)[kPer],
+                                           double2 (&xs)[kPer]) {
+    uint64_t src = kMode == kSrcGather ? mulmod_shoup(zg, p.m, p.m_sh, p.N) : 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        const uint64_t z = zg + uint64_t(e) * kBlock;
+        if (z < p.zend) {
+            xa[e] = load_amp<kE1>(p.X, z, p.z0);
+            if (kMode == kSrcGather) xs[e] = load_amp<kE1>(p.X, src, p.z0);
+            else if (kMode == kSrcBuffer) xs[e] = p.Xs[z - p.z0];
+            else xs[e] = xa[e];
+        } else {
+            xa[e] = make_double2(0.0, 0.0);
+            xs[e] = xa[e];
+        }
+        if (kMode == kSrcGather) src = addmod(src, p.m_step, p.N);
+    }
+}
+
+__device__ __forceinline__ void write_cta_digits(unsigned long long (*digits)[kDigits],
+                                                 unsigned long long* out_slot, int tid) {
+    if (tid < 2) {
+        unsigned long long carry = 0;
+        unsigned long long* out = out_slot + tid * kDigits;
+        for (int i = 0; i < kDigits; ++i) {
+            unsigned long long v = digits[tid][i] + carry;
+            out[i] = v & 0xffffffffull;
+            carry = v >> 32;
+        }
+    }
+}
+
+template <int kMode, bool kE1>
+__global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
+    __shared__ double nrm[2 * kPer][kBlock + 1];  // +1: conflict-free column walks
+    __shared__ unsigned long long digits[2][kDigits];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 2 * kDigits; i += kThreads) (&digits[0][0])[i] = 0ull;
+    DigitWindow win;
+    window_reset(win);
+    __syncthreads();
+
+    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
+        const uint64_t zg = p.z0 + c * kChunk + tid;
+        double2 xa[kPer], xs[kPer];
+        load_pairs<kMode, kE1>(p, zg, xa, xs);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            double h0r, h0i, h1r, h1i;
+            stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            const bool live = zg + uint64_t(e) * kBlock < p.zend;
+            nrm[e][tid] = live ? cnorm(h0r, h0i) : 0.0;
+            nrm[kPer + e][tid] = live ? cnorm(h1r, h1i) : 0.0;
+        }
+        __syncthreads();
+        if (tid < 2 * kPer) {
+            // one lane per (block, group): the reference's in-order block sum
+            double s = 0.0;
+#pragma unroll 16
+            for (int i = 0; i < kBlock; ++i) s = __dadd_rn(s, nrm[tid][i]);
+            const uint64_t b = c * kPer + (tid & (kPer - 1));
+            const int g = tid / kPer;
+            if (b < p.nb) {
+                p.S[g * p.nb + b] = s;
+                window_add(win, s, digits[g]);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < 2 * kPer) window_flush(win, digits[tid / kPer]);
+    __syncthreads();
+    write_cta_digits(digits, p.partials + uint64_t(blockIdx.x) * 2 * kDigits, tid);
+}
+
+// p0/p1 from the stage. kahan: reference combine_blocks (statevector.cpp:32-40),
+// two interleaved sequential chains, zeros skipped; else exact sum of partials.
+static __global__ void k_finalize(const unsigned long long* __restrict__ partials, int nparts,
+                           const double* __restrict__ S, uint64_t nb, int kahan,
+                           double* __restrict__ out) {
+    __shared__ unsigned long long acc[2][kDigits];
+    if (kahan) {
+        if (threadIdx.x == 0) {
+            double s0 = 0, c0 = 0, s1 = 0, c1 = 0;
+            for (uint64_t b = 0; b < nb; ++b) {
+                const double x0 = S[b], x1 = S[nb + b];
+                if (x0 != 0.0) {
+                    double y = __dsub_rn(x0, c0);
+                    double t = __dadd_rn(s0, y);
+                    c0 = __dsub_rn(__dsub_rn(t, s0), y);
+                    s0 = t;
+                }
+                if (x1 != 0.0) {
+                    double y = __dsub_rn(x1, c1);
+                    double t = __dadd_rn(s1, y);
+                    c1 = __dsub_rn(__dsub_rn(t, s1), y);
+                    s1 = t;
+                }
+            }
+            out[0] = s0;
+            out[1] = s1;
+        }
+        return;
+    }
+    for (int i = threadIdx.x; i < 2 * kDigits; i += blockDim.x) {
+        unsigned long long s = 0;
+        for (int c = 0; c < nparts; ++c) s += partials[uint64_t(c) * 2 * kDigits + i];
+        (&acc[0][0])[i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) out[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
+}
+
+// The exact digits of this engine's (or shard's) partial masses: sum of the
+// per-CTA digit slots, carry-normalised to 32-bit digits (for an allreduce).
+static __global__ void k_sum_partials(const unsigned long long* __restrict__ partials, int nparts,
+                               unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long acc[2][kDigits];
+    for (int i = threadIdx.x; i < 2 * kDigits; i += blockDim.x) {
+        unsigned long long s = 0;
+        for (int c = 0; c < nparts; ++c) s += partials[uint64_t(c) * 2 * kDigits + i];
+        (&acc[0][0])[i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        unsigned long long carry = 0;
+        for (int i = 0; i < kDigits; ++i) {
+            unsigned long long v = acc[threadIdx.x][i] + carry;
+            out[threadIdx.x * kDigits + i] = v & 0xffffffffull;
+            carry = v >> 32;
+        }
+    }
+}
+
+template <int kMode, bool kE1>
+__global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
+    const int tid = threadIdx.x;
+    for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
+        const uint64_t zg = p.z0 + c * kChunk + tid;
+        double2 xa[kPer], xs[kPer];
+        load_pairs<kMode, kE1>(p, zg, xa, xs);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const uint64_t z = zg + uint64_t(e) * kBlock;
+            double h0r, h0i, h1r, h1i;
+            stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            if (z < p.zend)
+                p.Y[z - p.z0] = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+        }
+    }
+}
+
+// Post-Hadamard amplitudes of group x for global y in [first, first + count).
+template <int kMode, bool kE1>
+__global__ void k_stage_read(StageParams p, int x, uint64_t first, uint64_t count,
+                             double2* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t z = first + i;
+        if (z >= p.zend || z < p.z0) {
+            out[i] = make_double2(0.0, 0.0);
+            continue;
+        }
+        double2 xa = load_amp<kE1>(p.X, z, p.z0), xs;
+        if (kMode == kSrcGather) xs = load_amp<kE1>(p.X, mulmod_shoup(z, p.m, p.m_sh, p.N), p.z0);
+        else if (kMode == kSrcBuffer) xs = p.Xs[z - p.z0];
+        else xs = xa;
+        double h0r, h0i, h1r, h1i;
+        stage_pair(p.sc, xa, xs, h0r, h0i, h1r, h1i);
+        out[i] = x ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+    }
+}
+
+// g_x[y] = w_x * (sel[y] * inv), the reference state after init / reset_top,
+// for global y in [first, first + count) (zero outside [z0, zend)).
+template <bool kE1>
+__global__ void k_state_read(const double2* __restrict__ X, uint64_t z0, uint64_t zend, double wr,
+                             double wi, double inv, uint64_t first, uint64_t count,
+                             double2* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t z = first + i;
+        if (z >= zend || z < z0) {
+            out[i] = make_double2(0.0, 0.0);
+            continue;
+        }
+        double2 v = load_amp<kE1>(X, z, z0);
+        double r, im;
+        cmul(wr, wi, __dmul_rn(v.x, inv), __dmul_rn(v.y, inv), r, im);
+        out[i] = make_double2(r, im);
+    }
+}
+
+// The index map exactly as the gather kernels walk it (Shoup per thread, then
+// incremental), written out for the bit-exact index-map parity check.
+static __global__ void k_index_map(StageParams p, uint64_t chunk0, uint64_t nchunk, uint64_t first,
+                            uint64_t count, uint64_t* __restrict__ out) {
+    for (uint64_t c = chunk0 + blockIdx.x; c < chunk0 + nchunk; c += gridDim.x) {
+        const uint64_t z0 = c * kChunk + threadIdx.x;
+        uint64_t src = mulmod_shoup(z0, p.m, p.m_sh, p.N);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const uint64_t z = z0 + uint64_t(e) * kBlock;
+            if (z >= first && z < first + count && z < p.N) out[z - first] = src;
+            src = addmod(src, p.m_step, p.N);
+        }
+    }
+}
+
+static __global__ void k_fill_identity(uint64_t first, uint64_t count, uint64_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = first + i;
+}
+
+}  // namespace shs

@@ -33,6 +33,7 @@
 #pragma once
 
 #include "device_math.cuh"
+#include "stage_kernels.cuh"
 
 namespace shs {
 
@@ -124,15 +125,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
 
 __device__ __forceinline__ void write_partials(unsigned long long (*digits)[kDigits],
                                                unsigned long long* out_slot, int tid) {
-    if (tid < 2) {
-        unsigned long long carry = 0;
-        unsigned long long* out = out_slot + tid * kDigits;
-        for (int i = 0; i < kDigits; ++i) {
-            unsigned long long v = digits[tid][i] + carry;
-            out[i] = v & 0xffffffffull;
-            carry = v >> 32;
-        }
-    }
+    write_cta_digits(digits, out_slot, tid);
 }
 
 // One ring slot: the chunk's gathered columns (transposed, +1 padding against
@@ -391,7 +384,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
 
 // The block straddling the boundary between a row and its z-order predecessor:
 // S_b = fold(predecessor's tail partial, this row's head norms).
-__global__ void __launch_bounds__(256) k_tile_fixup(TileParams p, unsigned long long* slots) {
+static __global__ void __launch_bounds__(256) k_tile_fixup(TileParams p, unsigned long long* slots) {
     __shared__ unsigned long long digits[2][kDigits];
     const int tid = threadIdx.x;
     for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&digits[0][0])[i] = 0ull;

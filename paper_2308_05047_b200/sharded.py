@@ -1,0 +1,266 @@
+"""Sharded iterative-Shor engine: one shard of the state per GPU.
+
+The state `sel` is block-sharded over G shards (shard q owns global amplitude
+indices [q*S, min(N, (q+1)*S)), S a multiple of 256). Per stage every shard runs
+(include/shorsim_b200.h, "sharded engine"):
+
+    exchange   P = sel o src (only stages with a real permutation): each rank
+               pulls 256 B source runs from, and pushes 1 KB destination runs to,
+               the owners' buffers (NVLink peer memory across GPUs)
+    probs      shard-local h0/h1 and the reference's 256-block partials, folded
+               into 80 exact integer digits -> allreduce (sum) over shards ->
+               correctly rounded p0, p1 (identical for every G)
+    measure    host sampling, identical on every rank (same Philox stream)
+    collapse   shard-local, in place over P, which becomes the next sel
+
+Two process layouts share this driver:
+  * ``LocalGroup`` — every shard in this process (virtual shards on one GPU,
+    or one shard per visible GPU); barrier = stream syncs, allreduce = host sum
+  * ``DistGroup`` — one shard per ``torch.distributed`` rank (NCCL or gloo);
+    shards see each other's buffers through CUDA IPC handles.
+The driver only sequences C-ABI calls; all amplitude arithmetic is on device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+from . import _lib as L
+from .engine import (BitString, Error, ErrorConfig, ErrorEvent, FactoringProblem, RunResult,
+                     SimulatorOptions, StageTrace, _raise, sample_measurement)
+
+NORM_TOLERANCE = 1e-9  # statevector.cpp:18
+
+
+def digits_to_probs(digits: Sequence[int]):
+    """Correctly rounded (p0, p1) from summed exact digits (host, no device)."""
+    arr = (L.u64 * L.SHS_DIGITS)(*[int(d) for d in digits])
+    p0, p1 = L.dbl(), L.dbl()
+    _raise(L.load().shs_digits_to_probs(arr, C.byref(p0), C.byref(p1)))
+    return p0.value, p1.value
+
+
+class Shard:
+    """One shard of the state on one device (ctypes over shs_shard_*)."""
+
+    def __init__(self, problem: FactoringProblem, error: ErrorConfig,
+                 options: SimulatorOptions, rank: int, nshards: int):
+        self._lib = L.load()
+        self.rank, self.nshards, self.t = rank, nshards, problem.t
+        self._h = L.vp()
+        pr = L.shs_problem(problem.N, problem.a, problem.L, problem.t, problem.seed)
+        er = error.to_c()
+        op = options.to_c()
+        _raise(self._lib.shs_shard_create(C.byref(pr), C.byref(er), C.byref(op), rank, nshards,
+                                          C.byref(self._h)))
+        rng = (L.u64 * 3)()
+        _raise(self._lib.shs_shard_range(self._h, rng))
+        self.lo, self.hi, self.S = rng[0], rng[1], rng[2]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.shs_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def buffers(self):
+        out = (L.vp * 2)()
+        _raise(self._lib.shs_shard_buffers(self._h, out))
+        return [out[0], out[1]]
+
+    def ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        _raise(self._lib.shs_shard_ipc_handles(self._h, buf))
+        return buf.raw
+
+    def attach(self, peer: int, bufs):
+        arr = (L.vp * 2)(*bufs)
+        _raise(self._lib.shs_shard_attach(self._h, peer, arr))
+
+    def attach_ipc(self, peer: int, handles: bytes):
+        buf = C.create_string_buffer(handles, 128)
+        _raise(self._lib.shs_shard_attach_ipc(self._h, peer, buf))
+
+    def init(self):
+        _raise(self._lib.shs_shard_init(self._h))
+
+    def needs_exchange(self, s: int) -> bool:
+        return bool(self._lib.shs_shard_needs_exchange(self._h, s))
+
+    def exchange(self, s: int):
+        _raise(self._lib.shs_shard_exchange(self._h, s))
+
+    def probs(self, s: int, prefix: int) -> List[int]:
+        out = (L.u64 * L.SHS_DIGITS)()
+        _raise(self._lib.shs_shard_probs(self._h, s, prefix & (2**64 - 1), prefix >> 64, out))
+        return list(out)
+
+    def collapse(self, src_group: int, p_source: float):
+        _raise(self._lib.shs_shard_collapse(self._h, src_group, p_source))
+
+    def sync(self):
+        _raise(self._lib.shs_shard_sync(self._h))
+
+    def state_read(self, x: int, first: int, count: int):
+        out = (L.dbl * (2 * count))()
+        _raise(self._lib.shs_shard_state_read(self._h, x, first, count, out))
+        return out
+
+    def stage_read(self, x: int, first: int, count: int):
+        out = (L.dbl * (2 * count))()
+        _raise(self._lib.shs_shard_stage_read(self._h, x, first, count, out))
+        return out
+
+    def set_timing(self, enable: bool):
+        _raise(self._lib.shs_shard_set_timing(self._h, 1 if enable else 0))
+
+    def kernel_times(self):
+        ms = (L.dbl * 3)()
+        n = (L.u64 * 3)()
+        _raise(self._lib.shs_shard_kernel_times(self._h, ms, n))
+        return {"probs": (ms[0], n[0]), "exchange": (ms[1], n[1]), "collapse": (ms[2], n[2])}
+
+    def launch_count(self) -> int:
+        return self._lib.shs_shard_launch_count(self._h)
+
+    def stream_handle(self) -> int:
+        return self._lib.shs_shard_stream(self._h) or 0
+
+
+class LocalGroup:
+    """All shards live in this process: barrier = device syncs, allreduce = sum."""
+
+    def __init__(self, shards: Sequence):
+        self.shards = list(shards)
+        for a in self.shards:
+            for b in self.shards:
+                if a is not b:
+                    a.attach(b.rank, b.buffers())
+
+    def barrier(self):
+        for sh in self.shards:
+            sh.sync()
+
+    def allreduce(self, digits: List[int]) -> List[int]:
+        return digits
+
+
+class DistGroup:
+    """One shard per torch.distributed rank; peers attached through CUDA IPC."""
+
+    def __init__(self, shard, attach_ipc: bool = True, device=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.torch = dist, torch
+        self.shards = [shard]
+        self.device = device
+        if attach_ipc:
+            handles = [None] * dist.get_world_size()
+            dist.all_gather_object(handles, shard.ipc_handles())
+            for q, h in enumerate(handles):
+                if q != shard.rank:
+                    shard.attach_ipc(q, h)
+            dist.barrier()
+
+    def barrier(self):
+        for sh in self.shards:
+            sh.sync()
+        self.dist.barrier()
+
+    def allreduce(self, digits: List[int]) -> List[int]:
+        t = self.torch.tensor(digits, dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return [int(x) for x in t.tolist()]
+
+
+class ShardedShorEngine:
+    """IterativeShorEngine semantics (run(seed, bitstring_index)) over a sharded
+    state. ``shards`` are this process's shards; ``group`` sequences them with
+    the others (LocalGroup / DistGroup). With combine="exact" the results equal
+    the single-GPU engine's bit for bit."""
+
+    def __init__(self, problem: FactoringProblem, error: Optional[ErrorConfig],
+                 options: Optional[SimulatorOptions], shards: Sequence, group):
+        self.problem = problem
+        self.error = error if error is not None else ErrorConfig()
+        self.options = options if options is not None else SimulatorOptions()
+        self.shards = list(shards)
+        self.group = group
+        self.t = problem.t
+
+    @staticmethod
+    def virtual(problem: FactoringProblem, error: Optional[ErrorConfig] = None,
+                options: Optional[SimulatorOptions] = None, nshards: int = 2,
+                devices: Optional[Sequence[int]] = None) -> "ShardedShorEngine":
+        """G shards in this process (on one GPU, or spread over `devices`)."""
+        import dataclasses
+        error = error if error is not None else ErrorConfig()
+        options = options if options is not None else SimulatorOptions()
+        shards = []
+        for r in range(nshards):
+            o = dataclasses.replace(options, device=(devices[r % len(devices)] if devices
+                                                     else options.device))
+            shards.append(Shard(problem, error, o, r, nshards))
+        return ShardedShorEngine(problem, error, options, shards, LocalGroup(shards))
+
+    def close(self):
+        for sh in self.shards:
+            sh.close()
+
+    # -- step API (what run() is made of)
+    def state_init(self):
+        for sh in self.shards:
+            sh.init()
+
+    def stage_probs(self, s: int, prefix: int = 0):
+        if any(sh.needs_exchange(s) for sh in self.shards):
+            for sh in self.shards:
+                sh.exchange(s)
+            self.group.barrier()  # every P complete before anyone reads it
+        digits = [0] * L.SHS_DIGITS
+        for sh in self.shards:
+            d = sh.probs(s, prefix)
+            digits = [a + b for a, b in zip(digits, d)]
+        digits = self.group.allreduce(digits)
+        p0, p1 = digits_to_probs(digits)
+        if self.options.check_norms and abs(p0 + p1 - 1.0) > NORM_TOLERANCE:
+            raise Error(f"statevector norm drifted beyond 1e-9 at stage {s}")
+        return p0, p1
+
+    def stage_collapse(self, src_group: int, p_source: float):
+        for sh in self.shards:
+            sh.collapse(src_group, p_source)
+        self.group.barrier()  # the next exchange reads every shard's new sel
+
+    def run(self, seed: int, bitstring_index: int) -> RunResult:
+        """IterativeShorEngine::run, statevector.cpp:323-412, sharded."""
+        self.state_init()
+        observed = sampled = 0
+        trace = []
+        idx32 = bitstring_index & 0xFFFFFFFF
+        for s in range(self.t):
+            p0, p1 = self.stage_probs(s, observed)
+            m = sample_measurement(p1, seed, idx32, s, self.error)
+            trace.append(StageTrace(s, p1, m["sampled_bit"], m["observed_bit"],
+                                    ErrorEvent(m["classical_flip"], m["error_branch"])))
+            observed |= m["observed_bit"] << s
+            sampled |= m["sampled_bit"] << s
+            if s + 1 < self.t:
+                src_group = 1 - m["sampled_bit"] if m["error_branch"] else m["sampled_bit"]
+                self.stage_collapse(src_group, p1 if src_group == 1 else p0)
+        j = observed
+        if int(self.error.kind) == 5:  # ErrorKind::bitflip
+            j = _bitflip(j, self.t, self.error.delta, seed, idx32)
+        return RunResult(BitString(self.t, j), sampled, trace)
+
+
+def _bitflip(j: int, t: int, delta: float, seed: int, idx: int) -> int:
+    """bitflip_bitstring (statevector.cpp:404-409) through the library's host model."""
+    arr = (L.u64 * 2)(j & (2**64 - 1), j >> 64)
+    _raise(L.load().shs_bitflip(arr, t, delta, seed, idx))
+    return arr[0] | (arr[1] << 64)
