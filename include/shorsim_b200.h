@@ -122,9 +122,18 @@ void shs_engine_destroy(shs_engine* engine);
 int shs_engine_run(shs_engine* engine, uint64_t seed, uint64_t bitstring_index, uint64_t j[2],
                    uint64_t j_sampled[2], shs_stage_trace* trace);
 
-/* count consecutive runs idx0 .. idx0+count-1; j receives 2*count words. */
+/* count consecutive runs idx0 .. idx0+count-1; j receives 2*count words. Small
+ * problems (N <= 4096, t <= 20: configs 1-2) run whole runs on the device, one
+ * CTA per run (batch.cuh); larger ones run stage by stage. Identical results. */
 int shs_engine_run_batch(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
                          uint64_t* j);
+/* as run_batch, with optional per-run outputs (NULL to skip): j_sampled [2*count],
+ * p1 [count*t], bits [count*t*4] = sampled, observed, classical_flip, error_branch */
+int shs_engine_run_many(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
+                        uint64_t* j, uint64_t* j_sampled, double* p1, int32_t* bits);
+/* the same runs forced through the per-stage path (for comparisons) */
+int shs_engine_run_sequential(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
+                              uint64_t* j);
 
 /* IterativeShorEngine::stage_multipliers: a^(2^(t-1-s)) mod N, t entries. */
 int shs_engine_stage_multipliers(const shs_engine* engine, uint64_t* out);

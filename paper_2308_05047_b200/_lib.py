@@ -61,6 +61,9 @@ SIGNATURES = [
     ("shs_engine_run", C.c_int, [vp, u64, u64, C.POINTER(u64), C.POINTER(u64),
                                  C.POINTER(shs_stage_trace)]),
     ("shs_engine_run_batch", C.c_int, [vp, u64, u64, u32, C.POINTER(u64)]),
+    ("shs_engine_run_many", C.c_int, [vp, u64, u64, u32, C.POINTER(u64), C.POINTER(u64),
+                                      C.POINTER(dbl), C.POINTER(i32)]),
+    ("shs_engine_run_sequential", C.c_int, [vp, u64, u64, u32, C.POINTER(u64)]),
     ("shs_engine_stage_multipliers", C.c_int, [vp, C.POINTER(u64)]),
     ("shs_engine_stages", u32, [vp]),
     ("shs_state_init", C.c_int, [vp]),

@@ -34,6 +34,7 @@
 #include "stage_kernels.cuh"
 #include "tile_plan.hpp"
 #include "tiled.cuh"
+#include "batch.cuh"
 
 using namespace shs;
 
@@ -98,6 +99,14 @@ struct shs_engine {
     uint64_t klaunch[3] = {0, 0, 0};
     uint64_t launches = 0;
     uint64_t device_bytes = 0;
+    // batched small-N runs (batch.cuh), allocated on first use
+    uint64_t* d_apows = nullptr;
+    uint64_t* d_ainvs = nullptr;
+    uint64_t* d_ainvsh = nullptr;
+    double2* d_phase = nullptr;
+    void* d_batch_out = nullptr;
+    size_t batch_out_bytes = 0;
+    int batch_grid = 0;
 };
 
 namespace {
@@ -230,6 +239,11 @@ void release(shs_engine* e) {
     cudaFree(e->partials);
     cudaFree(e->head);
     cudaFree(e->tail);
+    cudaFree(e->d_apows);
+    cudaFree(e->d_ainvs);
+    cudaFree(e->d_ainvsh);
+    cudaFree(e->d_phase);
+    cudaFree(e->d_batch_out);
     cudaFree(e->d_out);
     if (e->h_out) cudaFreeHost(e->h_out);
     if (e->stream) cudaStreamDestroy(e->stream);
@@ -392,6 +406,106 @@ int engine_run(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
     return SHS_OK;
 }
 
+bool batchable(const shs_engine* e) { return e->N <= kBatchMaxN && e->t <= kBatchMaxT; }
+
+// Device tables for whole-run batches: multipliers, inverses (+ Shoup) and the
+// phase table std::polar(1, stage_phase(s, p)) for every (s, prefix) computed
+// here with glibc, exactly as the per-stage driver computes each phase.
+int ensure_batch_tables(shs_engine* e) {
+    if (e->d_phase) return SHS_OK;
+    std::vector<uint64_t> invsh(e->t, 0);
+    for (uint32_t s = 0; s < e->t; ++s)
+        if (e->a_pows[s] != 1) invsh[s] = shoup(e->a_invs[s], e->N);
+    const uint64_t entries = (uint64_t(1) << e->t) - 1;
+    std::vector<double2> phase(std::max<uint64_t>(entries, 1));
+    for (uint32_t s = 0; s < e->t; ++s)
+        for (uint64_t pfx = 0; pfx < (uint64_t(1) << s); ++pfx) {
+            const double phi = stage_phase(s, pfx);
+            phase[((uint64_t(1) << s) - 1) + pfx] = make_double2(1.0 * std::cos(phi), 1.0 * std::sin(phi));
+        }
+    SHS_CUDA(cudaMalloc(&e->d_apows, sizeof(uint64_t) * e->t));
+    SHS_CUDA(cudaMalloc(&e->d_ainvs, sizeof(uint64_t) * e->t));
+    SHS_CUDA(cudaMalloc(&e->d_ainvsh, sizeof(uint64_t) * e->t));
+    SHS_CUDA(cudaMalloc(&e->d_phase, sizeof(double2) * phase.size()));
+    SHS_CUDA(cudaMemcpy(e->d_apows, e->a_pows.data(), sizeof(uint64_t) * e->t, cudaMemcpyHostToDevice));
+    SHS_CUDA(cudaMemcpy(e->d_ainvs, e->a_invs.data(), sizeof(uint64_t) * e->t, cudaMemcpyHostToDevice));
+    SHS_CUDA(cudaMemcpy(e->d_ainvsh, invsh.data(), sizeof(uint64_t) * e->t, cudaMemcpyHostToDevice));
+    SHS_CUDA(cudaMemcpy(e->d_phase, phase.data(), sizeof(double2) * phase.size(), cudaMemcpyHostToDevice));
+    const size_t smem = batch_smem_bytes(e->N);
+    SHS_CUDA(cudaFuncSetAttribute(k_batch_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int occ = 0;
+    SHS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch_runs, kBatchThreads, smem));
+    e->batch_grid = std::max(1, occ) * e->num_sms;
+    e->device_bytes += sizeof(uint64_t) * 3 * e->t + sizeof(double2) * phase.size();
+    return SHS_OK;
+}
+
+// `count` whole runs idx0 .. idx0+count-1 in one launch (one CTA per run).
+int run_many_batched(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_t* j,
+                     uint64_t* js, double* p1, int32_t* bits) {
+    int rc = ensure_batch_tables(e);
+    if (rc) return rc;
+    const size_t jb = sizeof(uint64_t) * 2 * count;
+    const size_t pb = p1 ? sizeof(double) * count * e->t : 0;
+    const size_t bb = bits ? sizeof(int32_t) * 4 * count * e->t : 0;
+    const size_t sb = sizeof(int32_t) * count;
+    const size_t need = 2 * jb + pb + bb + sb + 64;
+    if (need > e->batch_out_bytes) {
+        cudaFree(e->d_batch_out);
+        e->d_batch_out = nullptr;
+        SHS_CUDA(cudaMalloc(&e->d_batch_out, need));
+        e->batch_out_bytes = need;
+    }
+    char* base = static_cast<char*>(e->d_batch_out);
+    BatchParams bp{};
+    bp.N = e->N;
+    bp.t = e->t;
+    bp.seed = seed;
+    bp.idx0 = idx0;
+    bp.count = count;
+    bp.a_pows = e->d_apows;
+    bp.a_invs = e->d_ainvs;
+    bp.a_invsh = e->d_ainvsh;
+    bp.phase = e->d_phase;
+    bp.w0r = e->w[0];
+    bp.w0i = e->w[1];
+    bp.w1r = e->w[2];
+    bp.w1i = e->w[3];
+    bp.kind = e->err.kind;
+    bp.delta = e->err.delta;
+    bp.px = e->err.px;
+    bp.py = e->err.py;
+    bp.check_norms = e->opt.check_norms;
+    bp.j_out = reinterpret_cast<uint64_t*>(base);
+    bp.js_out = reinterpret_cast<uint64_t*>(base + jb);
+    bp.p1_out = p1 ? reinterpret_cast<double*>(base + 2 * jb) : nullptr;
+    bp.bits_out = bits ? reinterpret_cast<int32_t*>(base + 2 * jb + pb) : nullptr;
+    bp.status = reinterpret_cast<int32_t*>(base + 2 * jb + pb + bb);
+    const int g = static_cast<int>(std::min<uint64_t>(count, static_cast<uint64_t>(e->batch_grid)));
+    rc = launch(e, -1, [&] {
+        k_batch_runs<<<g, kBatchThreads, batch_smem_bytes(e->N), e->stream>>>(bp);
+    });
+    if (rc) return rc;
+    std::vector<int32_t> status(count);
+    SHS_CUDA(cudaMemcpyAsync(status.data(), bp.status, sb, cudaMemcpyDeviceToHost, e->stream));
+    SHS_CUDA(cudaMemcpyAsync(j, bp.j_out, jb, cudaMemcpyDeviceToHost, e->stream));
+    if (js) SHS_CUDA(cudaMemcpyAsync(js, bp.js_out, jb, cudaMemcpyDeviceToHost, e->stream));
+    if (p1) SHS_CUDA(cudaMemcpyAsync(p1, bp.p1_out, pb, cudaMemcpyDeviceToHost, e->stream));
+    if (bits) SHS_CUDA(cudaMemcpyAsync(bits, bp.bits_out, bb, cudaMemcpyDeviceToHost, e->stream));
+    rc = sync(e);
+    if (rc) return rc;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (status[i] == SHS_ERROR)
+            return set_error(SHS_ERROR, "statevector norm drifted beyond 1e-9 (run " +
+                                            std::to_string(idx0 + i) + ")");
+        if (status[i] == SHS_DEGENERATE_BRANCH)
+            return set_error(SHS_DEGENERATE_BRANCH,
+                             "impossible measurement branch (run " + std::to_string(idx0 + i) + ")");
+    }
+    return SHS_OK;
+}
+
 template <typename F>
 int guarded(shs_engine* e, F&& f) {
     if (!e) return set_error(SHS_INVALID_ARGUMENT, "null engine");
@@ -546,8 +660,45 @@ int shs_engine_run(shs_engine* e, uint64_t seed, uint64_t idx, uint64_t j[2],
     });
 }
 
+int shs_engine_run_many(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t count,
+                        uint64_t* j, uint64_t* j_sampled, double* p1, int32_t* bits) {
+    return guarded(e, [&]() -> int {
+        if (!j) return set_error(SHS_INVALID_ARGUMENT, "null output");
+        if (count == 0) return SHS_OK;
+        if (batchable(e)) return run_many_batched(e, seed, idx0, count, j, j_sampled, p1, bits);
+        std::vector<shs_stage_trace> tr(e->t);
+        for (uint32_t i = 0; i < count; ++i) {
+            u128 jj = 0, js = 0;
+            int rc = engine_run(e, seed, idx0 + i, &jj, &js, tr.data());
+            if (rc) return rc;
+            j[2 * i] = static_cast<uint64_t>(jj);
+            j[2 * i + 1] = static_cast<uint64_t>(jj >> 64);
+            if (j_sampled) {
+                j_sampled[2 * i] = static_cast<uint64_t>(js);
+                j_sampled[2 * i + 1] = static_cast<uint64_t>(js >> 64);
+            }
+            for (uint32_t s = 0; s < e->t; ++s) {
+                if (p1) p1[uint64_t(i) * e->t + s] = tr[s].p1;
+                if (bits) {
+                    int32_t* o = bits + (uint64_t(i) * e->t + s) * 4;
+                    o[0] = tr[s].sampled_bit;
+                    o[1] = tr[s].observed_bit;
+                    o[2] = tr[s].classical_flip;
+                    o[3] = tr[s].quantum_error_branch;
+                }
+            }
+        }
+        return SHS_OK;
+    });
+}
+
 int shs_engine_run_batch(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t count,
                          uint64_t* j) {
+    return shs_engine_run_many(e, seed, idx0, count, j, nullptr, nullptr, nullptr);
+}
+
+int shs_engine_run_sequential(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t count,
+                              uint64_t* j) {
     return guarded(e, [&] {
         for (uint32_t i = 0; i < count; ++i) {
             u128 jj = 0;

@@ -300,8 +300,34 @@ class IterativeShorEngine:
         return RunResult(BitString(self.t, j[0] | (j[1] << 64)), js[0] | (js[1] << 64), trace)
 
     def run_batch(self, seed: int, idx0: int, count: int) -> List[int]:
+        """Bit strings of runs idx0 .. idx0+count-1 (whole runs on the device for
+        small problems; see shs_engine_run_batch)."""
         out = (L.u64 * (2 * count))()
         _raise(self._lib.shs_engine_run_batch(self._h, seed, idx0, count, out))
+        return [out[2 * i] | (out[2 * i + 1] << 64) for i in range(count)]
+
+    def run_many(self, seed: int, idx0: int, count: int) -> List[RunResult]:
+        """RunResult (with traces) for runs idx0 .. idx0+count-1 in one call."""
+        t = self.t
+        j = (L.u64 * (2 * count))()
+        js = (L.u64 * (2 * count))()
+        p1 = (L.dbl * (count * t))()
+        bits = (L.i32 * (4 * count * t))()
+        _raise(self._lib.shs_engine_run_many(self._h, seed, idx0, count, j, js, p1, bits))
+        out = []
+        for i in range(count):
+            trace = []
+            for s in range(t):
+                b = bits[4 * (i * t + s):4 * (i * t + s) + 4]
+                trace.append(StageTrace(s, p1[i * t + s], b[0], b[1],
+                                        ErrorEvent(bool(b[2]), bool(b[3]))))
+            out.append(RunResult(BitString(t, j[2 * i] | (j[2 * i + 1] << 64)),
+                                 js[2 * i] | (js[2 * i + 1] << 64), trace))
+        return out
+
+    def run_sequential(self, seed: int, idx0: int, count: int) -> List[int]:
+        out = (L.u64 * (2 * count))()
+        _raise(self._lib.shs_engine_run_sequential(self._h, seed, idx0, count, out))
         return [out[2 * i] | (out[2 * i + 1] << 64) for i in range(count)]
 
     def stage_multipliers(self) -> List[int]:
