@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libshorsim_b200.so")
+# SHS_LIB overrides the library path (build variants for A/B measurements)
+LIB_PATH = os.environ.get("SHS_LIB") or os.path.join(HERE, "libshorsim_b200.so")
 
 u64 = C.c_uint64
 u32 = C.c_uint32

@@ -146,15 +146,15 @@ static __global__ void __launch_bounds__(kExchangeThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         const int c = tid & (kCols - 1);
-        const int rg = tid >> 6;
+        const int rg = tid / kCols;
         bool more = first < p.ntiles;
         while (more) {
             mbar_wait(&sm.full[stage], phase);
             const uint64_t pos = sm.i0[stage] + c;
             more = sm.last[stage] == 0;
 #pragma unroll
-            for (int q = 0; q < kRows / 4; ++q) {
-                const int r = rg * (kRows / 4) + q;
+            for (int q = 0; q < kRowsPerConsumer; ++q) {
+                const int r = rg * kRowsPerConsumer + q;
                 if (pos < sm.row_l[stage][r]) {
                     const uint64_t z = sm.row_z[stage][r] + pos;
                     const int d = shard_owner(z, shmap);

@@ -5,10 +5,11 @@
 // z_j = j*A mod N (j < H) split Z_N into H rows [z_j, z_j + g_j) and
 //                      src(z_j + i) = (j + i*m) mod N.
 // A chunk of kRows consecutive rows j and kCols consecutive columns i therefore
-// reads the gathered side as kCols runs of kRows amplitudes (256 B each) and
-// the direct side / output as kRows runs of kCols amplitudes (1 KB each): both
-// HBM sides are whole-line and coalesced; the transpose happens in shared
-// memory. By the three-distance theorem a row's length and its successor in z
+// reads the gathered side as kCols runs of kRows amplitudes and the direct side
+// / output as kRows runs of kCols amplitudes: both HBM sides are whole-line and
+// coalesced; the transpose happens in shared memory. 32 x 32 chunks (512 B
+// runs on both sides) measured best on B200 (profiles/r01/README.md: 16 x 64,
+// i.e. 256 B gathered runs, was 10% slower). By the three-distance theorem a row's length and its successor in z
 // order need no sort: with u = argmin_{0<j<H} (jA mod N), v = argmax (jA mod N),
 //   j + u < H : length du = uA mod N,       successor j + u
 //   j >= v    : length dv = N - (vA mod N),  successor j - v
@@ -37,17 +38,35 @@
 
 namespace shs {
 
-constexpr int kRows = 16;     // rows per tile
-constexpr int kCols = 64;     // columns per chunk
-constexpr int kStages = 4;    // copy ring depth
+#ifndef SHS_TILE_ROWS
+#define SHS_TILE_ROWS 32
+#endif
+#ifndef SHS_TILE_COLS
+#define SHS_TILE_COLS 32
+#endif
+#ifndef SHS_RING_STAGES
+#define SHS_RING_STAGES 4
+#endif
+constexpr int kRows = SHS_TILE_ROWS;    // rows per tile (gathered-side run length)
+constexpr int kCols = SHS_TILE_COLS;    // columns per chunk (direct-side run length)
+constexpr int kStages = SHS_RING_STAGES;  // copy ring depth
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kProducerWarps = 4;
 constexpr int kProducers = 32 * kProducerWarps;
 constexpr int kProducerWarp = kConsumerWarps;                   // warps 8..11
-constexpr int kChainWarp = kConsumerWarps + kProducerWarps;     // warp 12 (probs only)
-constexpr int kCopiesPerProducer = kRows * kCols / kProducers;  // 8 per side
-constexpr int kNormBufs = 4;                       // norm tiles in flight (chain slack)
+constexpr int kChainWarp = kConsumerWarps + kProducerWarps;     // first chain warp (probs only)
+constexpr int kChainWarps = (2 * kRows + 31) / 32;              // one lane per (row, group)
+constexpr int kCopiesPerProducer = kRows * kCols / kProducers;  // copies per side per chunk
+constexpr int kDstRowStep = kProducers / kCols;                 // rows between a thread's copies
+constexpr int kRowsPerConsumer = kRows * kCols / kConsumers;    // rows a consumer thread owns
+constexpr int kNormSync = kConsumers + 32 * kChainWarps;        // named-barrier thread count
+static_assert(kRows <= 32 && (kRows & (kRows - 1)) == 0, "kRows: power of two <= 32");
+static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0, "kCols");
+#ifndef SHS_NORM_BUFS
+#define SHS_NORM_BUFS 4
+#endif
+constexpr int kNormBufs = SHS_NORM_BUFS;           // norm tiles in flight (chain slack)
 constexpr int kNormFull0 = 1, kNormEmpty0 = 1 + kNormBufs;  // named barrier ids
 constexpr int kNrmStride = kCols + 2;              // 16 B-aligned rows, conflict-free LDS.128
 
@@ -149,7 +168,7 @@ struct TileSmem {
 
 template <bool kProbs>
 constexpr int tile_threads() {
-    return 32 * (kConsumerWarps + kProducerWarps + (kProbs ? 1 : 0));
+    return 32 * (kConsumerWarps + kProducerWarps + (kProbs ? kChainWarps : 0));
 }
 
 template <bool kProbs>
@@ -193,9 +212,9 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
     if (warp >= kProducerWarp && warp < kProducerWarp + kProducerWarps) {
         // ------------------------------------------------------------ producers
         // gathered side: element e = pt + kProducers * k is (column e / kRows,
-        // row e % kRows = pt % kRows): 16 consecutive threads copy one column's
-        // 256 B run. Direct side: element e is (row e / kCols = pt / kCols + 2k,
-        // column e % kCols = pt % kCols): 64 threads per 1 KB row run. The row
+        // row e % kRows = pt % kRows): kRows consecutive threads copy one
+        // column's run. Direct side: element e is (row e / kCols = pt / kCols +
+        // kDstRowStep k, column e % kCols = pt % kCols): kCols threads per row run. The row
         // table lives in lanes 0..15 of every producer warp (tile_rows) and is
         // fetched by shuffles.
         const int pt = tid - 32 * kProducerWarp;
@@ -217,8 +236,8 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             for (int k = 0; k < kCopiesPerProducer; ++k) {
                 const uint64_t c = src_c0 + (kProducers / kRows) * k;
                 sidx[k] = addmod(j0 + r_src, mulmod_shoup(c, p.m, p.m_sh, p.N), p.N);
-                const uint64_t dz = __shfl_sync(0xffffffffu, rz, dst_r0 + 2 * k);
-                dlen[k] = __shfl_sync(0xffffffffu, rl, dst_r0 + 2 * k);
+                const uint64_t dz = __shfl_sync(0xffffffffu, rz, dst_r0 + kDstRowStep * k);
+                dlen[k] = __shfl_sync(0xffffffffu, rl, dst_r0 + kDstRowStep * k);
                 dptr[k] = p.X + dz + dst_c;
             }
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols) {
@@ -232,7 +251,8 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                 }
 #pragma unroll
                 for (int k = 0; k < kCopiesPerProducer; ++k) {
-                    if (i0 + dst_c < dlen[k]) cp_async16(&st.dst[dst_r0 + 2 * k][dst_c], dptr[k]);
+                    if (i0 + dst_c < dlen[k])
+                        cp_async16(&st.dst[dst_r0 + kDstRowStep * k][dst_c], dptr[k]);
                     dptr[k] += kCols;
                 }
                 cp_async_arrive(&sm.full[stage]);
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         uint32_t phase = 0;
         uint64_t k = 0;  // chunk counter (norm buffer parity)
         const int c = tid & (kCols - 1);
-        const int rg = tid >> 6;  // 4 row groups of 4 rows
+        const int rg = tid / kCols;  // row group: rows rg * kRowsPerConsumer + q
         bool more = blockIdx.x < p.ntiles;
         while (more) {
             mbar_wait(&sm.full[stage], phase);
@@ -268,10 +288,10 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             const uint64_t pos = st.i0 + c;
             more = st.last == 0;
             const int b = static_cast<int>(k % kNormBufs);
-            if (kProbs && k >= kNormBufs) named_sync(kNormEmpty0 + b, kConsumers + 32);
+            if (kProbs && k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
 #pragma unroll
-            for (int q = 0; q < kRows / 4; ++q) {
-                const int r = rg * (kRows / 4) + q;
+            for (int q = 0; q < kRowsPerConsumer; ++q) {
+                const int r = rg * kRowsPerConsumer + q;
                 const bool live = pos < st.row_l[r];
                 double h0r, h0i, h1r, h1i;
                 stage_pair(p.sc, st.dst[r][c], st.src[c][r], h0r, h0i, h1r, h1i);
@@ -285,7 +305,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[stage]);
-            if (kProbs) named_arrive(kNormFull0 + b, kConsumers + 32);
+            if (kProbs) named_arrive(kNormFull0 + b, kNormSync);
             ++k;
             if (++stage == kStages) {
                 stage = 0;
@@ -294,11 +314,12 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         }
         if (kProbs) {  // match the chain's releases of the last kNormBufs norm tiles
             for (uint64_t q = (k > kNormBufs ? k - kNormBufs : 0); q < k; ++q)
-                named_sync(kNormEmpty0 + static_cast<int>(q % kNormBufs), kConsumers + 32);
+                named_sync(kNormEmpty0 + static_cast<int>(q % kNormBufs), kNormSync);
         }
-    } else if (kProbs && warp == kChainWarp) {
+    } else if (kProbs && warp >= kChainWarp && warp < kChainWarp + kChainWarps) {
         // ------------------------------------------------------------ chains
-        const int cr = lane & (kRows - 1), cg = lane >> 4;
+        const int ct = tid - 32 * kChainWarp;  // one lane per (row, group)
+        const int cr = ct % kRows, cg = ct / kRows;
         DigitWindow win;
         window_reset(win);
         uint64_t k = 0;
@@ -310,7 +331,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             double c_s = 0.0;
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols, ++k) {
                 const int b = static_cast<int>(k % kNormBufs);
-                named_sync(kNormFull0 + b, kConsumers + 32);
+                named_sync(kNormFull0 + b, kNormSync);
                 const double* row = &sm.nrm[b][cg][cr][0];
                 if (i0 >= c_head && i0 + kCols <= c_len) {
                     // interior chunk (the common case): 64 in-order adds, branch-free.
@@ -360,7 +381,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                     }
                 }
                 __syncwarp();
-                named_arrive(kNormEmpty0 + b, kConsumers + 32);
+                named_arrive(kNormEmpty0 + b, kNormSync);
             }
             if (c_len > 0) {
                 const uint64_t end = c_z + c_len;
