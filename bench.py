@@ -321,6 +321,8 @@ def run_ours(args):
                 "last_j": str(res.bits.j)},
         "gpu_launches": launches, "clocks": clock_info,
     }
+    if rank == 0 and ws == 1 and not args.no_small:
+        line["batched_small_n"] = small_n_throughput(shs)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             r = reference_sample(1, 0, os.cpu_count() or 1)
@@ -339,6 +341,49 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def small_n_throughput(shs):
+    """Configs 1-2 (BASELINE.json configs[0..1]): whole runs per second through
+    the batched engine (shs_engine_run_batch), beside the unmodified reference's
+    per-run time on one host core (its engine runs small problems single-threaded;
+    the reference's campaign parallelism is one problem per worker thread)."""
+    out = {}
+    cases = {"config1_N15": [(15, 7)],
+             "config2_N21_N35": [(21, a) for a in (2, 4, 5, 8, 10, 11, 13, 16, 17, 19, 20)] +
+                                [(35, a) for a in range(2, 35) if math.gcd(a, 35) == 1]}
+    shots = {"config1_N15": 100000, "config2_N21_N35": 1024}
+    try:
+        from oracle import Reference
+        ref = Reference()
+    except Exception:
+        ref = None
+    for name, problems in cases.items():
+        engines = [shs.IterativeShorEngine(shs.FactoringProblem.make(N, a), shs.ErrorConfig(),
+                                           shs.SimulatorOptions(qubit_ceiling=64))
+                   for N, a in problems]
+        for e in engines:
+            e.run_batch(2, 0, 64)  # tables + warm
+        t0 = time.perf_counter()
+        runs = 0
+        for e in engines:
+            e.run_batch(2, 0, shots[name])
+            runs += shots[name]
+        dt = time.perf_counter() - t0
+        entry = {"runs": runs, "seconds": dt, "runs_per_s": runs / dt,
+                 "problems": len(problems), "shots_per_problem": shots[name]}
+        if ref is not None:
+            N, a = problems[0]
+            t = 2 * N.bit_length()
+            re = ref.engine(N, a, N.bit_length(), t, qubit_ceiling=33)
+            k = 20000
+            sec = re.time_runs(2, 0, k)
+            entry["reference_cpu_runs_per_s_1core"] = k / sec
+            entry["reference_sample"] = f"{k} IterativeShorEngine::run calls of N={N}, a={a}, 1 thread"
+        out[name] = entry
+        for e in engines:
+            e.close()
+    return out
 
 
 def run_sharded(args):
@@ -468,6 +513,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--e2e-runs", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="skip the configs 1-2 batched line")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -101,9 +101,10 @@ static __global__ void __launch_bounds__(kExchangeThreads, 1)
         uint32_t phase = 0;
         for (uint64_t tile = first; tile < p.ntiles; tile += step) {
             const uint64_t j0 = tile * kRows;
-            uint64_t rz, rl;
-            const uint64_t tlen = tile_rows(p, j0, lane, rz, rl);
+            LaneRows lr;
+            const uint64_t tlen = tile_rows(p, j0, lane, lr);
             const bool last_tile = tile + step >= p.ntiles;
+            const uint64_t rl = lr.len[kRowsPerLane > 1 ? (r_src >> 5) : 0];
             uint64_t sidx[kCopiesPerProducer];
 #pragma unroll
             for (int k = 0; k < kCopiesPerProducer; ++k) {
@@ -125,10 +126,7 @@ static __global__ void __launch_bounds__(kExchangeThreads, 1)
                 }
                 cp_async_arrive(&sm.full[stage]);
                 if (warp == kProducerWarp) {
-                    if (lane < kRows) {
-                        sm.row_z[stage][lane] = rz;
-                        sm.row_l[stage][lane] = rl;
-                    }
+                    store_rows(lr, lane, sm.row_z[stage], sm.row_l[stage]);
                     __syncwarp();
                     if (lane == 0) {
                         sm.i0[stage] = i0;

@@ -61,7 +61,8 @@ constexpr int kCopiesPerProducer = kRows * kCols / kProducers;  // copies per si
 constexpr int kDstRowStep = kProducers / kCols;                 // rows between a thread's copies
 constexpr int kRowsPerConsumer = kRows * kCols / kConsumers;    // rows a consumer thread owns
 constexpr int kNormSync = kConsumers + 32 * kChainWarps;        // named-barrier thread count
-static_assert(kRows <= 32 && (kRows & (kRows - 1)) == 0, "kRows: power of two <= 32");
+static_assert(kRows <= 64 && (kRows & (kRows - 1)) == 0, "kRows: power of two <= 64");
+constexpr int kRowsPerLane = kRows > 32 ? kRows / 32 : 1;       // row bookkeeping per lane
 static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0, "kCols");
 #ifndef SHS_NORM_BUFS
 #define SHS_NORM_BUFS 4
@@ -176,19 +177,61 @@ constexpr size_t tile_smem_bytes() {
     return sizeof(TileSmem<kProbs>);
 }
 
-// Tile length (longest of its kRows rows) and, for lane & (kRows-1), its row.
+// The tile's row table, spread over a warp: lane l holds rows l + 32 h
+// (h < kRowsPerLane), or row l & (kRows - 1) when kRows < 32. Returns the tile
+// length (longest row).
+struct LaneRows {
+    uint64_t z[kRowsPerLane], len[kRowsPerLane];
+};
+
 __device__ __forceinline__ uint64_t tile_rows(const TileParams& p, uint64_t j0, int lane,
-                                              uint64_t& z, uint64_t& len) {
-    const uint64_t j = j0 + (lane & (kRows - 1));
-    len = tile_row_len(j, p);
-    z = len ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
-    uint64_t mx = len;
+                                              LaneRows& lr) {
+    uint64_t mx = 0;
 #pragma unroll
-    for (int o = kRows / 2; o > 0; o >>= 1) {
+    for (int h = 0; h < kRowsPerLane; ++h) {
+        const int r = kRows >= 32 ? lane + 32 * h : (lane & (kRows - 1));
+        const uint64_t j = j0 + r;
+        lr.len[h] = tile_row_len(j, p);
+        lr.z[h] = lr.len[h] ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
+        mx = lr.len[h] > mx ? lr.len[h] : mx;
+    }
+#pragma unroll
+    for (int o = (kRows >= 32 ? 16 : kRows / 2); o > 0; o >>= 1) {
         const uint64_t other = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = other > mx ? other : mx;
     }
     return mx;
+}
+
+// (z, len) of tile row r from the warp's LaneRows (all lanes must call)
+__device__ __forceinline__ void row_from_lanes(const LaneRows& lr, int r, uint64_t& z,
+                                               uint64_t& len) {
+    const int src_lane = r & 31;
+    const int h = kRowsPerLane > 1 ? (r >> 5) : 0;
+    z = 0;
+    len = 0;
+#pragma unroll
+    for (int hh = 0; hh < kRowsPerLane; ++hh) {
+        const uint64_t zz = __shfl_sync(0xffffffffu, lr.z[hh], src_lane);
+        const uint64_t ll = __shfl_sync(0xffffffffu, lr.len[hh], src_lane);
+        if (hh == h) {
+            z = zz;
+            len = ll;
+        }
+    }
+}
+
+// write the tile's row table into a ring slot (lanes of one warp)
+__device__ __forceinline__ void store_rows(const LaneRows& lr, int lane, uint64_t* row_z,
+                                           uint64_t* row_l) {
+#pragma unroll
+    for (int h = 0; h < kRowsPerLane; ++h) {
+        const int r = lane + 32 * h;
+        if (kRows >= 32 || lane < kRows) {
+            row_z[r] = lr.z[h];
+            row_l[r] = lr.len[h];
+        }
+    }
 }
 
 template <bool kProbs>
@@ -225,9 +268,11 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         uint32_t phase = 0;
         for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const uint64_t j0 = tile * kRows;
-            uint64_t rz, rl;  // row (lane % kRows) of the tile == this thread's source row
-            const uint64_t tlen = tile_rows(p, j0, lane, rz, rl);
+            LaneRows lr;
+            const uint64_t tlen = tile_rows(p, j0, lane, lr);
             const bool last_tile = tile + gridDim.x >= p.ntiles;
+            // this thread's source row r_src = lane + 32 * (warp-uniform h)
+            const uint64_t rl = lr.len[kRowsPerLane > 1 ? (r_src >> 5) : 0];
             // source index of this thread's copies, advanced by kCols*m per chunk
             uint64_t sidx[kCopiesPerProducer];
             const double2* dptr[kCopiesPerProducer];
@@ -236,8 +281,8 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
             for (int k = 0; k < kCopiesPerProducer; ++k) {
                 const uint64_t c = src_c0 + (kProducers / kRows) * k;
                 sidx[k] = addmod(j0 + r_src, mulmod_shoup(c, p.m, p.m_sh, p.N), p.N);
-                const uint64_t dz = __shfl_sync(0xffffffffu, rz, dst_r0 + kDstRowStep * k);
-                dlen[k] = __shfl_sync(0xffffffffu, rl, dst_r0 + kDstRowStep * k);
+                uint64_t dz;
+                row_from_lanes(lr, dst_r0 + kDstRowStep * k, dz, dlen[k]);
                 dptr[k] = p.X + dz + dst_c;
             }
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols) {
@@ -257,10 +302,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                 }
                 cp_async_arrive(&sm.full[stage]);
                 if (warp == kProducerWarp) {
-                    if (lane < kRows) {
-                        st.row_z[lane] = rz;
-                        st.row_l[lane] = rl;
-                    }
+                    store_rows(lr, lane, st.row_z, st.row_l);
                     __syncwarp();  // row table stores ordered before lane 0's release
                     if (lane == 0) {
                         st.i0 = i0;
@@ -325,8 +367,10 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         uint64_t k = 0;
         for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
             const uint64_t j0 = tile * kRows;
-            uint64_t c_z, c_len;
-            const uint64_t tlen = tile_rows(p, j0, lane, c_z, c_len);
+            LaneRows lr;
+            const uint64_t tlen = tile_rows(p, j0, lane, lr);
+            const int hsel = kRowsPerLane > 1 ? ((ct >> 5) % kRowsPerLane) : 0;  // row cr = lane + 32 hsel
+            const uint64_t c_z = lr.z[hsel], c_len = lr.len[hsel];
             const uint64_t c_head = (256 - (c_z & 255)) & 255;
             double c_s = 0.0;
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols, ++k) {
