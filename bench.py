@@ -362,12 +362,14 @@ def small_n_throughput(shs):
         engines = [shs.IterativeShorEngine(shs.FactoringProblem.make(N, a), shs.ErrorConfig(),
                                            shs.SimulatorOptions(qubit_ceiling=64))
                    for N, a in problems]
-        for e in engines:
-            e.run_batch(2, 0, 64)  # tables + warm
-        t0 = time.perf_counter()
+        import numpy as np
+        bufs = [np.empty((shots[name], 2), dtype=np.uint64) for _ in engines]
+        for e, b in zip(engines, bufs):
+            e.run_batch_array(2, 0, shots[name], b)  # tables, buffers, warm
+        t0 = time.perf_counter()  # the C-ABI call with host output buffers
         runs = 0
-        for e in engines:
-            e.run_batch(2, 0, shots[name])
+        for e, b in zip(engines, bufs):
+            e.run_batch_array(2, 0, shots[name], b)
             runs += shots[name]
         dt = time.perf_counter() - t0
         entry = {"runs": runs, "seconds": dt, "runs_per_s": runs / dt,

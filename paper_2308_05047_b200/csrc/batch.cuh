@@ -23,7 +23,7 @@ namespace shs {
 
 constexpr uint32_t kBatchMaxT = 20;      // phase table of 2^t entries (16 MB at t = 20)
 constexpr uint64_t kBatchMaxN = 4096;    // 64 KB of shared state per CTA
-constexpr int kBatchThreads = 128;
+constexpr int kBatchThreads = 128;  // CTA size cap; small N use one warp per run
 
 struct BatchParams {
     uint64_t N;
@@ -88,6 +88,7 @@ __device__ __forceinline__ double kahan_blocks(const double* x, int n) {
 }
 
 static __global__ void __launch_bounds__(kBatchThreads) k_batch_runs(BatchParams bp) {
+    // blockDim.x = batch_threads(N): 32..128
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint64_t N = bp.N;
     const int nb = static_cast<int>((N + kBlock - 1) / kBlock);
@@ -136,12 +137,13 @@ static __global__ void __launch_bounds__(kBatchThreads) k_batch_runs(BatchParams
                 nrm[nb * kBlock + z] = cnorm(h1r, h1i);
             }
             __syncthreads();
-            // in-order 256-block folds (statevector.cpp:354-370)
+            // in-order 256-block folds over the live amplitudes (statevector.cpp:354-370)
             if (tid < 2 * nb) {
                 const int g = tid / nb, b = tid % nb;
                 const double* row = nrm + g * nb * kBlock + b * kBlock;
+                const int live = static_cast<int>(min(uint64_t(kBlock), N - uint64_t(b) * kBlock));
                 double acc = 0.0;
-                for (int i = 0; i < kBlock; ++i) acc = __dadd_rn(acc, row[i]);
+                for (int i = 0; i < live; ++i) acc = __dadd_rn(acc, row[i]);
                 bsum[g * nb + b] = acc;
             }
             __syncthreads();
@@ -252,6 +254,10 @@ static __global__ void __launch_bounds__(kBatchThreads) k_batch_runs(BatchParams
         Y = X + N;
         __syncthreads();
     }
+}
+
+inline int batch_threads(uint64_t N) {
+    return N <= 64 ? 32 : (N <= 256 ? 64 : kBatchThreads);
 }
 
 inline size_t batch_smem_bytes(uint64_t N) {

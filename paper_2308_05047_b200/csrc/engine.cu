@@ -435,7 +435,7 @@ int ensure_batch_tables(shs_engine* e) {
     SHS_CUDA(cudaFuncSetAttribute(k_batch_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int occ = 0;
-    SHS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch_runs, kBatchThreads, smem));
+    SHS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch_runs, batch_threads(e->N), smem));
     e->batch_grid = std::max(1, occ) * e->num_sms;
     e->device_bytes += sizeof(uint64_t) * 3 * e->t + sizeof(double2) * phase.size();
     return SHS_OK;
@@ -484,7 +484,7 @@ int run_many_batched(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_t
     bp.status = reinterpret_cast<int32_t*>(base + 2 * jb + pb + bb);
     const int g = static_cast<int>(std::min<uint64_t>(count, static_cast<uint64_t>(e->batch_grid)));
     rc = launch(e, -1, [&] {
-        k_batch_runs<<<g, kBatchThreads, batch_smem_bytes(e->N), e->stream>>>(bp);
+        k_batch_runs<<<g, batch_threads(e->N), batch_smem_bytes(e->N), e->stream>>>(bp);
     });
     if (rc) return rc;
     std::vector<int32_t> status(count);

@@ -306,6 +306,16 @@ class IterativeShorEngine:
         _raise(self._lib.shs_engine_run_batch(self._h, seed, idx0, count, out))
         return [out[2 * i] | (out[2 * i + 1] << 64) for i in range(count)]
 
+    def run_batch_array(self, seed: int, idx0: int, count: int, out=None):
+        """As run_batch, into a numpy uint64 array of shape (count, 2) = (lo, hi)
+        words of each bit string (no per-run Python objects)."""
+        import numpy as np
+        if out is None:
+            out = np.empty((count, 2), dtype=np.uint64)
+        ptr = out.ctypes.data_as(C.POINTER(L.u64))
+        _raise(self._lib.shs_engine_run_batch(self._h, seed, idx0, count, ptr))
+        return out
+
     def run_many(self, seed: int, idx0: int, count: int) -> List[RunResult]:
         """RunResult (with traces) for runs idx0 .. idx0+count-1 in one call."""
         t = self.t
