@@ -131,6 +131,8 @@ int shs_engine_run_batch(shs_engine* engine, uint64_t seed, uint64_t idx0, uint3
  * p1 [count*t], bits [count*t*4] = sampled, observed, classical_flip, error_branch */
 int shs_engine_run_many(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
                         uint64_t* j, uint64_t* j_sampled, double* p1, int32_t* bits);
+/* 1 when run_batch / run_many use the whole-run device kernel for this problem */
+int shs_engine_batched(const shs_engine* engine);
 /* the same runs forced through the per-stage path (for comparisons) */
 int shs_engine_run_sequential(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
                               uint64_t* j);

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("shs_engine_run_many", C.c_int, [vp, u64, u64, u32, C.POINTER(u64), C.POINTER(u64),
                                       C.POINTER(dbl), C.POINTER(i32)]),
     ("shs_engine_run_sequential", C.c_int, [vp, u64, u64, u32, C.POINTER(u64)]),
+    ("shs_engine_batched", C.c_int, [vp]),
     ("shs_engine_stage_multipliers", C.c_int, [vp, C.POINTER(u64)]),
     ("shs_engine_stages", u32, [vp]),
     ("shs_state_init", C.c_int, [vp]),

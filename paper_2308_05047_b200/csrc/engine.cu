@@ -692,6 +692,8 @@ int shs_engine_run_many(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t co
     });
 }
 
+int shs_engine_batched(const shs_engine* e) { return e && batchable(e) ? 1 : 0; }
+
 int shs_engine_run_batch(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t count,
                          uint64_t* j) {
     return shs_engine_run_many(e, seed, idx0, count, j, nullptr, nullptr, nullptr);
