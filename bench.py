@@ -323,6 +323,7 @@ def run_ours(args):
     }
     if rank == 0 and ws == 1 and not args.no_small:
         line["batched_small_n"] = small_n_throughput(shs)
+        line["config3_error_models"] = config3_runs(shs)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             r = reference_sample(1, 0, os.cpu_count() or 1)
@@ -385,6 +386,37 @@ def small_n_throughput(shs):
         out[name] = entry
         for e in engines:
             e.close()
+    return out
+
+
+def config3_runs(shs):
+    """Config 3 (BASELINE.json configs[2]): N = 16777207, t = 48, full runs
+    through the C ABI with each of the paper's error models at p_error = 0.01
+    (acceptance criterion 8's settings, proj/tests/acceptance/acceptance_main.cpp:
+    367-378), amplitude updates/s = N t / run time."""
+    w = WORKLOADS["c3"]
+    N, a = w["N"], w["a"]
+    prob = shs.FactoringProblem.make(N, a)
+    models = {"none": shs.ErrorConfig(),
+              "classical_measure": shs.ErrorConfig(shs.ErrorKind.classical_measure, 0.01),
+              "quantum_measure": shs.ErrorConfig(shs.ErrorKind.quantum_measure, 0.01,
+                                                 shs.PauliProbs(0.005, 0.005, 0.0)),
+              "amplitude_init": shs.ErrorConfig(shs.ErrorKind.amplitude_init,
+                                                2.0 * math.sqrt(0.01 * 0.99)),
+              "phase_init": shs.ErrorConfig(shs.ErrorKind.phase_init,
+                                            math.acos(1.0 - 2.0 * 0.01) / math.pi),
+              "bitflip": shs.ErrorConfig(shs.ErrorKind.bitflip, 0.01)}
+    out = {"N": N, "a": a, "t": prob.t}
+    for name, err in models.items():
+        eng = shs.IterativeShorEngine(prob, err, shs.SimulatorOptions(qubit_ceiling=64))
+        eng.run(7, 0)  # warm
+        t0 = time.perf_counter()
+        runs = 3
+        for i in range(runs):
+            eng.run(7, 1 + i)
+        dt = (time.perf_counter() - t0) / runs
+        out[name] = {"s_per_run": dt, "amp_updates_per_s": N * prob.t / dt}
+        eng.close()
     return out
 
 
