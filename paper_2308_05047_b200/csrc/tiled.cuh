@@ -323,6 +323,13 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         uint64_t k = 0;  // chunk counter (norm buffer parity)
         const int c = tid & (kCols - 1);
         const int rg = tid / kCols;  // row group: rows rg * kRowsPerConsumer + q
+        // collapse with 32-column chunks: a warp owns whole row segments; a row that
+        // starts at an odd index stores its segment shifted by one element (the last
+        // one is carried into the next chunk) so every store covers whole 32 B sectors
+        constexpr bool kSectorShift = !kProbs && kCols == 32;
+        double2 carry[kRowsPerConsumer];
+#pragma unroll
+        for (int q = 0; q < kRowsPerConsumer; ++q) carry[q] = make_double2(0.0, 0.0);
         bool more = blockIdx.x < p.ntiles;
         while (more) {
             mbar_wait(&sm.full[stage], phase);
@@ -340,6 +347,27 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                 if (kProbs) {
                     sm.nrm[b][0][r][c] = live ? cnorm(h0r, h0i) : 0.0;
                     sm.nrm[b][1][r][c] = live ? cnorm(h1r, h1i) : 0.0;
+                } else if (kSectorShift) {
+                    const double2 hv = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+                    const uint64_t rz = st.row_z[r], rl = st.row_l[r];
+                    if ((rz & 1) == 0) {
+                        if (live) p.Y[rz + pos] = hv;
+                    } else {
+                        // lane c stores column c - 1; lane 0 the previous chunk's column 31
+                        const double2 up = make_double2(__shfl_up_sync(0xffffffffu, hv.x, 1),
+                                                        __shfl_up_sync(0xffffffffu, hv.y, 1));
+                        const double2 last = make_double2(__shfl_sync(0xffffffffu, hv.x, 31),
+                                                          __shfl_sync(0xffffffffu, hv.y, 31));
+                        const uint64_t i0 = st.i0;
+                        if (c > 0) {
+                            if (pos - 1 < rl) p.Y[rz + pos - 1] = up;
+                        } else if (i0 > 0 && i0 - 1 < rl) {
+                            p.Y[rz + i0 - 1] = carry[q];
+                        }
+                        // the row's final element when it falls in column 31 of its last chunk
+                        if (c == kCols - 1 && pos + 1 == rl) p.Y[rz + pos] = hv;
+                        carry[q] = last;
+                    }
                 } else if (live) {
                     p.Y[st.row_z[r] + pos] =
                         p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
