@@ -20,6 +20,7 @@
 // tiles (tiled.cuh, k_tiled<true|false> + k_tile_fixup) so both the direct and
 // the gathered side of the permutation are coalesced.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -275,8 +276,15 @@ int state_init(shs_engine* e) {
     return SHS_OK;
 }
 
+// NVTX range for the lifetime of a scope (visible in nsys / ncu timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) {
     if (s >= e->t) return set_error(SHS_INVALID_ARGUMENT, "stage index out of range");
+    NvtxRange nvtx("shs stage probs");
     int rc = ensure_buffers(e);
     if (rc) return rc;
     const double phi = stage_phase(s, prefix);
@@ -338,6 +346,7 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
     if (!e->pending) return set_error(SHS_INVALID_ARGUMENT, "collapse without a pending stage");
     if (src_group != 0 && src_group != 1)
         return set_error(SHS_INVALID_ARGUMENT, "src_group must be 0 or 1");
+    NvtxRange nvtx("shs stage collapse");
     if (p_src < kDegenerateMass)  // statevector.cpp:388-390 / 265-266
         return set_error(SHS_DEGENERATE_BRANCH,
                          "impossible measurement branch at stage " + std::to_string(e->ps));
@@ -374,6 +383,7 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
 
 int engine_run(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
                shs_stage_trace* trace) {
+    NvtxRange nvtx("shs run");
     state_init(e);
     u128 observed = 0, sampled = 0;
     for (uint32_t s = 0; s < e->t; ++s) {

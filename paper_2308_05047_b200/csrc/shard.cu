@@ -11,6 +11,7 @@
 //   collapse  shard-local, in place over P, which becomes the next sel.
 // Identity stages and the first stage (implicit |1>) need no exchange.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -83,6 +84,11 @@ int shard_guard(shs_shard* sh, F&& f) {
 
 template <typename F>
 int shard_launch(shs_shard* sh, int kind, F&& f) {
+    static const char* kNames[3] = {"shs shard probs", "shs shard exchange", "shs shard collapse"};
+    nvtxRangePushA(kNames[kind]);
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     if (sh->timing) cudaEventRecord(sh->ev[0], sh->stream);
     f();
     cudaError_t err = cudaGetLastError();
