@@ -246,6 +246,14 @@ int shs_shard_kernel_times(const shs_shard* shard, double ms[3], uint64_t launch
 uint64_t shs_shard_launch_count(const shs_shard* shard);
 void* shs_shard_stream(const shs_shard* shard);
 
+/* ---- exhaustive_joint_distribution (statevector.hpp:193-198, statevector.cpp:533-579) ----
+ * Exact distribution over the 2^t observed bit strings by enumerating every
+ * measurement path on the device, error branches marginalised; out receives
+ * 2^t doubles. Same limits and errors as the reference (t <= 14 and n <= 12,
+ * else SHS_BUDGET_EXCEEDED; node budget, default 2^22) and bit-identical output. */
+int shs_exhaustive_distribution(const shs_problem* problem, const shs_error* error,
+                                uint64_t node_budget, int32_t device, double* out);
+
 /* thread-local message of the last failing call */
 const char* shs_last_error(void);
 /* library build string (arch, flags) */

@@ -24,6 +24,7 @@ from .engine import (  # noqa: F401
     StageTrace,
     bit_length,
     build_info,
+    exhaustive_joint_distribution,
     parse_error_config,
     recommended_t,
     run_iterative_shor,

@@ -106,6 +106,8 @@ SIGNATURES = [
     ("shs_shard_kernel_times", C.c_int, [vp, C.POINTER(dbl), C.POINTER(u64)]),
     ("shs_shard_launch_count", u64, [vp]),
     ("shs_shard_stream", vp, [vp]),
+    ("shs_exhaustive_distribution", C.c_int, [C.POINTER(shs_problem), C.POINTER(shs_error), u64,
+                                              i32, C.POINTER(dbl)]),
     ("shs_last_error", C.c_char_p, []),
     ("shs_build_info", C.c_char_p, []),
 ]

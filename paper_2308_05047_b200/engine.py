@@ -421,5 +421,18 @@ def sample_measurement(p1: float, seed: int, idx: int, stage: int, error: ErrorC
             "classical_flip": bool(out[3])}
 
 
+def exhaustive_joint_distribution(problem: FactoringProblem, error: Optional[ErrorConfig] = None,
+                                  node_budget: int = 1 << 22, device: int = 0) -> List[float]:
+    """exhaustive_joint_distribution, statevector.cpp:533-579: the exact distribution
+    over observed bit strings (2^t values), computed on the device; raises
+    BudgetExceededError past t > 14, n > 12 or the node budget, as the reference does."""
+    error = error if error is not None else ErrorConfig()
+    pr = L.shs_problem(problem.N, problem.a, problem.L, problem.t, problem.seed)
+    er = error.to_c()
+    out = (L.dbl * (1 << problem.t))()
+    _raise(L.load().shs_exhaustive_distribution(C.byref(pr), C.byref(er), node_budget, device, out))
+    return list(out)
+
+
 def build_info() -> str:
     return L.load().shs_build_info().decode()

@@ -128,6 +128,18 @@ def main():
     # 8. exhaustive distribution, test_statevector.cpp:357-364
     dist = ref.exhaustive(15, 7, 4, 8)
     out["exhaustive_15_7_8"] = hexlist(dist)
+    # error-model marginalisation, test_statevector.cpp:366-396 and test_noise.cpp:100-116
+    ex = []
+    for N, a, t, ename, ekw in [(15, 7, 5, "classical", dict(kind="classical_measure", delta=0.3)),
+                                (15, 7, 5, "quantum", dict(kind="quantum_measure", delta=0.1, px=0.05, py=0.05, pz=0.1)),
+                                (21, 2, 8, "pz_only", dict(kind="quantum_measure", delta=0.0, px=0.0, py=0.0, pz=0.3)),
+                                (55, 16, 8, "none", dict(kind="none")),
+                                (35, 4, 7, "bitflip", dict(kind="bitflip", delta=0.05)),
+                                (57, 5, 6, "phase", dict(kind="phase_init", delta=0.2)),
+                                (33, 5, 6, "amplitude", dict(kind="amplitude_init", delta=0.1))]:
+        d = ref.exhaustive(N, a, N.bit_length(), t, make_error(**ekw))
+        ex.append({"N": N, "a": a, "t": t, "name": ename, "error": ekw, "dist": hexlist(d)})
+    out["exhaustive_cases"] = ex
 
     out["_meta"] = {"generator": "tests/golden/make_golden.py",
                     "reference": "/root/reference/proj (unmodified), oracle/_ref/libshorsim_ref.so",
