@@ -58,8 +58,11 @@ def test_exhaustive_limits_and_budget(cuda_ok):
         dist(15, 7, 16)
     with pytest.raises(BudgetExceededError):  # n <= 12
         dist(4093, 3, 10)
-    with pytest.raises(BudgetExceededError):  # node budget
-        dist(15, 7, 8, node_budget=100)
+    # node budget: N=15, a=7, t=8 costs 9 path nodes + 4 leaves = 13 ticks (six identity
+    # stages have p1 = 0), so 13 suffices and 12 throws, as in the reference's recurse()
+    assert abs(sum(dist(15, 7, 8, node_budget=13)) - 1.0) < 1e-12
+    with pytest.raises(BudgetExceededError):
+        dist(15, 7, 8, node_budget=12)
     with pytest.raises(ConfigError):
         dist(15, 7, 8, E("bitflip", 2.0))
     d = dist(1021, 5, 14)  # the reference's largest: t = 14
