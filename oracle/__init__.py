@@ -49,7 +49,7 @@ def build(ref: bool | None = None) -> None:
         # the reference's own callers linked against the B200 engine (needs the lib built)
         if os.path.exists(os.path.join(HERE, "..", "paper_2308_05047_b200", "libshorsim_b200.so")):
             targets.append("link")
-    subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+    subprocess.run(["make", "-s", "-j4", "-C", HERE] + targets, check=True)
 
 
 class so_error(C.Structure):
