@@ -613,6 +613,14 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         return set_error(SHS_CUDA_ERROR, "device is not sm_100-class (B200 required)");
     }
     e->num_sms = prop.multiProcessorCount;
+    if (o.tiling == SHS_TILING_AUTO && kTileMinTilesPerSM > 0) {
+        e->max_rows = 0;
+        for (auto& pl : e->plans) {
+            if (pl.tiled && pl.ntiles < kTileMinTilesPerSM * static_cast<uint64_t>(e->num_sms))
+                pl.tiled = false;
+            if (pl.tiled) e->max_rows = std::max(e->max_rows, pl.H);
+        }
+    }
     int occ = 0;
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcGather, false>, kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");

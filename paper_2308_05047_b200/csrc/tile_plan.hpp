@@ -17,7 +17,17 @@ inline constexpr uint64_t kKahanMaxBlocks = 1024;  // AUTO: sequential Kahan up 
 inline constexpr uint64_t kTileAutoMinN = 1ull << 20;  // AUTO tiling from 16 MB of state
 inline constexpr uint64_t kTileMinRow = 512;           // every 256-block touches <= 2 rows
 inline constexpr uint64_t kTileMaxRows = 1ull << 18;   // head scratch <= 1 GB
-inline constexpr uint64_t kTileMinRowsPlan = 256;      // >= 16 tiles of kRows rows
+inline constexpr uint64_t kTileMinRowsPlan = 256;      // >= 8 tiles of kRows rows
+#ifndef SHS_TILE_AVG_ROW
+#define SHS_TILE_AVG_ROW 640
+#endif
+#ifndef SHS_TILE_MIN_TILES
+#define SHS_TILE_MIN_TILES 1
+#endif
+inline constexpr uint64_t kTileAvgRow = SHS_TILE_AVG_ROW;  // H <= N / kTileAvgRow
+// AUTO mode keeps the direct kernels when a plan has fewer tiles than this
+// multiple of the SM count (too few tiles leave SMs idle: one CTA per tile row set)
+inline constexpr uint64_t kTileMinTilesPerSM = SHS_TILE_MIN_TILES;
 
 // Host side of a stage's sorted-residue tiling (see tiled.cuh).
 struct TilePlanHost {
@@ -36,7 +46,7 @@ inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tilin
     TilePlanHost pl;
     if (tiling == SHS_TILING_OFF || A == 1) return pl;
     if (tiling == SHS_TILING_AUTO && N < kTileAutoMinN) return pl;
-    const uint64_t hmax = std::min<uint64_t>(N / 1024, kTileMaxRows);
+    const uint64_t hmax = std::min<uint64_t>(N / kTileAvgRow, kTileMaxRows);
     std::vector<uint64_t> cands;
     for (uint64_t h = 2; h <= hmax; h *= 2) {
         cands.push_back(h);
