@@ -74,8 +74,11 @@ struct ExchangeSmem {
 constexpr size_t exchange_smem_bytes() { return sizeof(ExchangeSmem); }
 
 // Tiled exchange over this rank's tiles t = tile0 + tile_step * k: producers
-// copy source runs (LDGSTS from the owners' sel), consumers store destination
-// runs (to the owners' P). Same ring / mbarrier protocol as k_tiled.
+// copy source runs from the owners' sel, consumers store destination runs to
+// the owners' P. Same ring / mbarrier protocol as k_tiled, except that the
+// producers use plain loads + shared stores + an mbarrier release instead of
+// cp.async: sources are mostly peer memory (NVLink), whose per-SM bandwidth
+// (~5 GB/s of 770 GB/s) 8 loads in flight per producer thread already cover.
 static __global__ void __launch_bounds__(kExchangeThreads, 1)
     k_exchange(TileParams p, ShardMap shmap, uint64_t tile0, uint64_t tile_step) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -90,7 +93,7 @@ static __global__ void __launch_bounds__(kExchangeThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const uint64_t first = tile0 + uint64_t(blockIdx.x) * tile_step;
+    const uint64_t first = tile0 + uint64_t(blockIdx.x) * tile_step;  // (ring slots below)
     const uint64_t step = uint64_t(gridDim.x) * tile_step;
 
     if (warp >= kProducerWarp && warp < kProducerWarp + kProducerWarps) {
@@ -113,18 +116,22 @@ static __global__ void __launch_bounds__(kExchangeThreads, 1)
             }
             for (uint64_t i0 = 0; i0 < tlen; i0 += kCols) {
                 mbar_wait(&sm.empty[stage], phase ^ 1);
+                double2 v[kCopiesPerProducer];
 #pragma unroll
-                for (int k = 0; k < kCopiesPerProducer; ++k) {
+                for (int k = 0; k < kCopiesPerProducer; ++k) {  // all loads in flight first
                     const int c = src_c0 + (kProducers / kRows) * k;
+                    v[k] = make_double2(0.0, 0.0);
                     if (i0 + c < rl) {
                         const uint64_t x = sidx[k];
                         const int q = shard_owner(x, shmap);
-                        cp_async16(&sm.src[stage][c][r_src],
-                                   shmap.src[q] + (x - uint64_t(q) * shmap.S));
+                        v[k] = shmap.src[q][x - uint64_t(q) * shmap.S];
                     }
                     sidx[k] = addmod(sidx[k], p.m_chunk, p.N);
                 }
-                cp_async_arrive(&sm.full[stage]);
+#pragma unroll
+                for (int k = 0; k < kCopiesPerProducer; ++k)
+                    sm.src[stage][src_c0 + (kProducers / kRows) * k][r_src] = v[k];
+                mbar_arrive(&sm.full[stage]);  // release of this thread's shared stores
                 if (warp == kProducerWarp) {
                     store_rows(lr, lane, sm.row_z[stage], sm.row_l[stage]);
                     __syncwarp();
