@@ -80,6 +80,7 @@ struct shs_engine {
     uint64_t max_rows = 0;   // largest H over the stages' plans
     double* head = nullptr;  // [max_rows][2][256]
     double* tail = nullptr;  // [max_rows][2]
+    uint2* split = nullptr;  // [t][tiled_cap + 1] CTA range starts of the tiled stages
     bool kahan = false;      // resolved combine mode
     // state
     bool e1 = true;
@@ -202,6 +203,8 @@ TileParams tile_params_for(const shs_engine* e, uint32_t s) {
     p.du = pl.du;
     p.dv = pl.dv;
     p.ntiles = pl.ntiles;
+    p.split = e->split + uint64_t(s) * (e->tiled_cap + 1);
+    p.bulk_rounds = pl.bulk_rounds;
     p.sc = e->sc;
     p.S = e->S;
     p.nb = e->nb;
@@ -240,6 +243,7 @@ void release(shs_engine* e) {
     cudaFree(e->partials);
     cudaFree(e->head);
     cudaFree(e->tail);
+    cudaFree(e->split);
     cudaFree(e->d_apows);
     cudaFree(e->d_ainvs);
     cudaFree(e->d_ainvsh);
@@ -265,6 +269,17 @@ int ensure_buffers(shs_engine* e) {
         SHS_CUDA(cudaMalloc(&e->head, sizeof(double) * 2 * 256 * e->max_rows));
         SHS_CUDA(cudaMalloc(&e->tail, sizeof(double) * 2 * e->max_rows));
         e->device_bytes += sizeof(double) * 2 * 257 * e->max_rows;
+        // the tiled stages' CTA range tables (tile_plan.hpp make_tile_split)
+        const size_t per = static_cast<size_t>(e->tiled_cap) + 1;
+        std::vector<uint32_t> tab(2 * per * e->t, 0);
+        for (uint32_t s = 0; s < e->t; ++s)
+            if (e->plans[s].tiled)
+                std::copy(e->plans[s].split.begin(), e->plans[s].split.end(),
+                          tab.begin() + 2 * per * s);
+        SHS_CUDA(cudaMalloc(&e->split, sizeof(uint32_t) * tab.size()));
+        SHS_CUDA(cudaMemcpy(e->split, tab.data(), sizeof(uint32_t) * tab.size(),
+                            cudaMemcpyHostToDevice));
+        e->device_bytes += sizeof(uint32_t) * tab.size();
     }
     return SHS_OK;
 }
@@ -301,11 +316,16 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
     int nparts = grid_for(e);
     if (e->plans[s].tiled && !e->e1) {
         TileParams tp = tile_params_for(e, s);
-        const int g1 = static_cast<int>(std::min<uint64_t>(tp.ntiles, e->tiled_cap));
+        const TilePlanHost& pl = e->plans[s];
+        const int g1 = pl.split_tail ? pl.grid
+                                     : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         const int g2 = static_cast<int>(
             std::min<uint64_t>((2 * tp.H + 255) / 256, static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
-            k_tiled<true><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
+            if (pl.split_tail)
+                k_tiled<true, true><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
+            else
+                k_tiled<true, false><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
             k_tile_fixup<<<g2, 256, 0, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
         nparts = g1 + g2;
@@ -355,9 +375,14 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
     if (e->plans[e->ps].tiled && !e->e1) {
         TileParams tp = tile_params_for(e, e->ps);
         tp.sel = src_group;
-        const int g1 = static_cast<int>(std::min<uint64_t>(tp.ntiles, e->tiled_cap));
+        const TilePlanHost& pl = e->plans[e->ps];
+        const int g1 = pl.split_tail ? pl.grid
+                                     : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         rc = launch(e, 2, [&] {
-            k_tiled<false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+            if (pl.split_tail)
+                k_tiled<false, true><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+            else
+                k_tiled<false, false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
         });
     } else {
         StageParams p = params_for(e, e->ps);
@@ -613,26 +638,31 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         return set_error(SHS_CUDA_ERROR, "device is not sm_100-class (B200 required)");
     }
     e->num_sms = prop.multiProcessorCount;
-    if (o.tiling == SHS_TILING_AUTO && kTileMinTilesPerSM > 0) {
-        e->max_rows = 0;
-        for (auto& pl : e->plans) {
-            if (pl.tiled && pl.ntiles < kTileMinTilesPerSM * static_cast<uint64_t>(e->num_sms))
-                pl.tiled = false;
-            if (pl.tiled) e->max_rows = std::max(e->max_rows, pl.H);
-        }
+    e->tiled_cap = e->num_sms;
+    e->max_rows = 0;
+    for (auto& pl : e->plans) {
+        if (!pl.tiled) continue;
+        make_tile_split(pl, e->tiled_cap);
+        if (o.tiling == SHS_TILING_AUTO &&
+            pl.chunks < kTileMinChunksPerCTA * static_cast<uint64_t>(e->tiled_cap))
+            pl.tiled = false;
+        if (pl.tiled) e->max_rows = std::max(e->max_rows, pl.H);
     }
     int occ = 0;
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcGather, false>, kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     e->grid_cap = std::max(1, occ) * e->num_sms;
     // one persistent TMA-pipelined CTA per SM for the tiled passes
-    ce = cudaFuncSetAttribute(k_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(tile_smem_bytes<true>()));
-    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<probs>)");
-    ce = cudaFuncSetAttribute(k_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(tile_smem_bytes<false>()));
-    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<collapse>)");
-    e->tiled_cap = e->num_sms;
+    for (auto fn : {k_tiled<true, false>, k_tiled<true, true>}) {
+        ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tile_smem_bytes<true>()));
+        if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<probs>)");
+    }
+    for (auto fn : {k_tiled<false, false>, k_tiled<false, true>}) {
+        ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tile_smem_bytes<false>()));
+        if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<collapse>)");
+    }
     e->fixup_cap = 2 * e->num_sms;
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");

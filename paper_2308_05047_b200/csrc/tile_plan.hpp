@@ -16,25 +16,76 @@ inline constexpr double kDegenerateMass = 1e-300;  // statevector.cpp:19
 inline constexpr uint64_t kKahanMaxBlocks = 1024;  // AUTO: sequential Kahan up to 2^18 amplitudes
 inline constexpr uint64_t kTileAutoMinN = 1ull << 20;  // AUTO tiling from 16 MB of state
 inline constexpr uint64_t kTileMinRow = 512;           // every 256-block touches <= 2 rows
-inline constexpr uint64_t kTileMaxRows = 1ull << 18;   // head scratch <= 1 GB
+#ifndef SHS_TILE_MAX_ROWS
+#define SHS_TILE_MAX_ROWS (1ull << 18)
+#endif
+inline constexpr uint64_t kTileMaxRows = SHS_TILE_MAX_ROWS;  // head scratch <= 1 GB
 inline constexpr uint64_t kTileMinRowsPlan = 256;      // >= 8 tiles of kRows rows
 #ifndef SHS_TILE_AVG_ROW
 #define SHS_TILE_AVG_ROW 640
 #endif
-#ifndef SHS_TILE_MIN_TILES
-#define SHS_TILE_MIN_TILES 1
+#ifndef SHS_TILE_MIN_CHUNKS
+#define SHS_TILE_MIN_CHUNKS 16
 #endif
 inline constexpr uint64_t kTileAvgRow = SHS_TILE_AVG_ROW;  // H <= N / kTileAvgRow
-// AUTO mode keeps the direct kernels when a plan has fewer tiles than this
-// multiple of the SM count (too few tiles leave SMs idle: one CTA per tile row set)
-inline constexpr uint64_t kTileMinTilesPerSM = SHS_TILE_MIN_TILES;
+// AUTO mode keeps the direct kernels when a plan has fewer chunks than this many
+// per CTA (a CTA's range cut costs up to 256 / kCols partly masked chunks)
+inline constexpr uint64_t kTileMinChunksPerCTA = SHS_TILE_MIN_CHUNKS;
+// plans with at least this many bands per CTA run whole bands round-robin only
+inline constexpr uint64_t kTileRoundRobinBands = 16;
 
 // Host side of a stage's sorted-residue tiling (see tiled.cuh).
 struct TilePlanHost {
     bool tiled = false;
     uint64_t H = 0, u = 0, v = 0, du = 0, dv = 0;
     uint64_t A = 0, A_sh = 0, m = 0, m_sh = 0, ntiles = 0;
+    uint64_t chunks = 0;          // kRows x kCols chunks over all bands
+    int grid = 0;                 // CTAs of k_tiled
+    uint64_t bulk_rounds = 0;     // whole bands per CTA, round-robin
+    bool split_tail = true;       // k_tiled<., true>: balanced remainder ranges
+    std::vector<uint32_t> split;  // [grid + 1] x (band, chunk): each CTA's remainder range
 };
+
+// Longest row of band b (its chunk count is this / kCols, rounded up): rows
+// j < H - u have length du, rows in [H - u, v) du + dv, the rest dv.
+inline uint64_t tile_band_len(const TilePlanHost& pl, uint64_t b) {
+    const uint64_t j0 = b * kRows, j1 = std::min<uint64_t>(j0 + kRows, pl.H);
+    const uint64_t hu = pl.H - pl.u, vb = std::max(pl.v, hu);
+    uint64_t mx = 0;
+    if (j0 < hu) mx = std::max(mx, pl.du);
+    if (j0 < pl.v && j1 > hu && hu < pl.v) mx = std::max(mx, pl.du + pl.dv);
+    if (j1 > vb) mx = std::max(mx, pl.dv);
+    return mx;
+}
+
+// Work split of the tiled kernels over `cap` CTAs (tiled.cuh, CtaWork): whole
+// bands round-robin for floor(ntiles / cap) rounds, then the remaining bands'
+// chunks, band-major, cut into cap contiguous ranges of equal size (within one
+// chunk). Without full rounds the grid shrinks to the chunk count if smaller.
+inline void make_tile_split(TilePlanHost& pl, int cap) {
+    uint64_t G = static_cast<uint64_t>(cap);
+    pl.split_tail = pl.ntiles < kTileRoundRobinBands * G;
+    pl.bulk_rounds = pl.ntiles / G;
+    const uint64_t b0 = std::min(pl.bulk_rounds * G, pl.ntiles);
+    std::vector<uint64_t> pre(pl.ntiles - b0 + 1, 0);
+    pl.chunks = 0;
+    for (uint64_t b = 0; b < pl.ntiles; ++b) {
+        const uint64_t nch = (tile_band_len(pl, b) + kCols - 1) / kCols;
+        pl.chunks += nch;
+        if (b >= b0) pre[b - b0 + 1] = pre[b - b0] + nch;
+    }
+    const uint64_t T = pre.back();
+    if (pl.bulk_rounds == 0) G = std::min<uint64_t>(G, T);
+    pl.grid = static_cast<int>(G);
+    pl.split.assign(2 * (G + 1), 0);
+    uint64_t b = 0;
+    for (uint64_t g = 0; g <= G; ++g) {
+        const uint64_t C = g * T / G;
+        while (b < pl.ntiles - b0 && pre[b + 1] <= C) ++b;
+        pl.split[2 * g] = static_cast<uint32_t>(b0 + b);
+        pl.split[2 * g + 1] = static_cast<uint32_t>(C - pre[b]);
+    }
+}
 
 // Pick the largest row count H (powers of two and 3 * 2^k up to N/1024) whose
 // three gap lengths are all >= kTileMinRow and at most 3x the mean row: one
@@ -65,7 +116,7 @@ inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tilin
         // rows must be long enough (each 256-block touches <= 2 rows) and balanced
         // (the longest row, du + dv, within 3x the mean N / H), else a tile idles SMs
         if (H >= kTileMinRowsPlan && du >= kTileMinRow && dv >= kTileMinRow &&
-            du + dv <= 3 * (N / H + 1)) {
+            du + dv <= 3 * (N / H + 1) && du + dv < (1ull << 31)) {  // 32-bit row spans
             pl.tiled = true;
             pl.H = H;
             pl.u = uj;

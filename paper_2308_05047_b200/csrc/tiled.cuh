@@ -15,6 +15,15 @@
 //   j >= v    : length dv = N - (vA mod N),  successor j - v
 //   otherwise : length du + dv,              successor j + u - v.
 //
+// Work split (CtaWork): whole bands round-robin, then the remaining bands' chunks
+// (kRows rows x kCols columns, band-major) cut into one contiguous range per CTA
+// (host table `split`, balanced to within a chunk). Where a cut falls inside a
+// band at column i, each row r is
+// cut at its first 256-block boundary e_r >= i (or its end): the earlier CTA
+// runs the row's columns [.., e_r), the later one [e_r, ..). So no block is
+// folded by two CTAs except at row boundaries (k_tile_fixup), and any plan,
+// even one with fewer bands than SMs, keeps every SM busy.
+//
 // CTA roles (one persistent CTA per SM):
 //   producer warps     — 16-byte cp.async (LDGSTS) copies of the chunk's 64
 //                        source-column runs and 16 row runs into a kStages-deep
@@ -79,7 +88,9 @@ struct TileParams {
     uint64_t m, m_sh;   // src = j + i * m mod N
     uint64_t m_chunk;   // kCols * m mod N: source advance per chunk
     uint64_t H, u, v, du, dv;
-    uint64_t ntiles;
+    uint64_t ntiles;    // bands of kRows rows
+    uint64_t bulk_rounds;  // whole bands per CTA, round-robin (CtaWork)
+    const uint2* split;    // [gridDim.x + 1] (band, chunk): each CTA's remainder range
     StageScalars sc;
     double* S;          // block partials, S0 [0, nb), S1 [nb, 2nb)
     uint64_t nb;
@@ -154,7 +165,8 @@ struct __align__(16) TileStage {
     double2 src[kCols][kRows + 1];
     double2 dst[kRows][kCols];
     uint64_t row_z[kRows];
-    uint64_t row_l[kRows];
+    uint32_t row_lo[kRows];  // the CTA's columns of each row: [row_lo, row_lo + row_n)
+    uint32_t row_n[kRows];   // (rows are < 2^32 long: make_tile_plan)
     uint64_t i0;
     uint64_t last;  // 1 on the last chunk of the CTA's sequence
 };
@@ -182,7 +194,15 @@ constexpr size_t tile_smem_bytes() {
 // length (longest row).
 struct LaneRows {
     uint64_t z[kRowsPerLane], len[kRowsPerLane];
+    uint64_t lo[kRowsPerLane], hi[kRowsPerLane];  // this CTA's columns of the row
 };
+
+// where a row starting at z, of length len, is cut for a band cut at column i:
+// its first 256-block boundary at or after i, or its end
+__device__ __forceinline__ uint64_t row_cut(uint64_t z, uint64_t len, uint64_t i) {
+    const uint64_t e = i + ((256 - ((z + i) & 255)) & 255);
+    return e < len ? e : len;
+}
 
 __device__ __forceinline__ uint64_t tile_rows(const TileParams& p, uint64_t j0, int lane,
                                               LaneRows& lr) {
@@ -201,6 +221,126 @@ __device__ __forceinline__ uint64_t tile_rows(const TileParams& p, uint64_t j0, 
         mx = other > mx ? other : mx;
     }
     return mx;
+}
+
+// Rows of band j0 / kRows for a CTA whose range covers the band's columns from
+// lo_col (0: the band's start) to hi_col (~0: its end). Returns the largest hi.
+__device__ __forceinline__ uint64_t tile_rows_split(const TileParams& p, uint64_t j0, int lane,
+                                                    LaneRows& lr, uint64_t lo_col,
+                                                    uint64_t hi_col) {
+    tile_rows(p, j0, lane, lr);
+    uint64_t mx = 0;
+#pragma unroll
+    for (int h = 0; h < kRowsPerLane; ++h) {
+        lr.lo[h] = lo_col ? row_cut(lr.z[h], lr.len[h], lo_col) : 0;
+        lr.hi[h] = hi_col != ~0ull ? row_cut(lr.z[h], lr.len[h], hi_col) : lr.len[h];
+        mx = lr.hi[h] > mx ? lr.hi[h] : mx;
+    }
+#pragma unroll
+    for (int o = (kRows >= 32 ? 16 : kRows / 2); o > 0; o >>= 1) {
+        const uint64_t other = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = other > mx ? other : mx;
+    }
+    return mx;
+}
+
+// A CTA's work items, each a band and a column range [lo_col, hi_col) (lo_col 0:
+// the band's start; hi_col ~0: its end), walked identically by producers and
+// chain warps: first bulk_rounds whole bands round-robin (band g + k * grid), so
+// the CTAs in flight work on neighbouring bands and their gathered runs are
+// adjacent in HBM (DRAM pages used whole: 8-14% faster than scattered ranges at
+// config 4); then one contiguous, balanced chunk range of the remaining bands
+// (host table `split`, so the leftover nbands mod grid bands, or a plan with
+// fewer bands than SMs, still keeps every SM busy). CtaWork<false>: whole bands
+// round-robin only (plans with >= kTileRoundRobinBands bands per CTA, where the
+// imbalance of one band is small): no cut columns, and no span arithmetic left
+// in the inner loops once lo = 0 / hi = len fold at compile time.
+template <bool kSplit>
+struct CtaWork;
+
+template <>
+struct CtaWork<false> {
+    uint64_t b, nt;
+    __device__ __forceinline__ explicit CtaWork(const TileParams& p) : b(blockIdx.x), nt(p.ntiles) {}
+    __device__ __forceinline__ bool valid() const { return b < nt; }
+    __device__ __forceinline__ void next() { b += gridDim.x; }
+    __device__ __forceinline__ bool last() const { return b + gridDim.x >= nt; }
+    __device__ __forceinline__ uint64_t band() const { return b; }
+    __device__ __forceinline__ uint64_t lo() const { return 0; }
+    __device__ __forceinline__ uint64_t hi() const { return ~0ull; }
+};
+
+template <>
+struct CtaWork<true> {
+    uint64_t k, K, b, b_first, b_last, lo_col, hi_col, nt;
+    bool bulk, tail_empty;
+    __device__ __forceinline__ explicit CtaWork(const TileParams& p) {
+        const uint2 s0 = p.split[blockIdx.x], s1 = p.split[blockIdx.x + 1];
+        b_first = s0.x;
+        lo_col = uint64_t(s0.y) * kCols;
+        b_last = s1.y ? s1.x : uint64_t(s1.x) - 1;
+        hi_col = uint64_t(s1.y) * kCols;
+        tail_empty = s0.x == s1.x && s0.y == s1.y;
+        K = p.bulk_rounds;
+        nt = p.ntiles;
+        k = 0;
+        bulk = K > 0 && blockIdx.x < nt;
+        b = bulk ? blockIdx.x : b_first;
+    }
+    __device__ __forceinline__ bool valid() const { return bulk || (!tail_empty && b <= b_last); }
+    __device__ __forceinline__ void next() {
+        if (bulk) {
+            if (++k < K && b + gridDim.x < nt) {
+                b += gridDim.x;
+            } else {
+                bulk = false;
+                b = b_first;
+            }
+        } else {
+            ++b;
+        }
+    }
+    __device__ __forceinline__ bool last() const {
+        return bulk ? ((k + 1 == K || b + gridDim.x >= nt) && tail_empty) : b == b_last;
+    }
+    __device__ __forceinline__ uint64_t band() const { return b; }
+    __device__ __forceinline__ uint64_t lo() const { return (!bulk && b == b_first) ? lo_col : 0; }
+    __device__ __forceinline__ uint64_t hi() const {
+        return (!bulk && b == b_last && hi_col) ? hi_col : ~0ull;
+    }
+};
+
+// (z, lo, hi) of tile row r from the warp's LaneRows (all lanes must call)
+__device__ __forceinline__ void row_span_from_lanes(const LaneRows& lr, int r, uint64_t& z,
+                                                    uint64_t& lo, uint64_t& hi) {
+    const int src_lane = r & 31;
+    const int h = kRowsPerLane > 1 ? (r >> 5) : 0;
+    z = lo = hi = 0;
+#pragma unroll
+    for (int hh = 0; hh < kRowsPerLane; ++hh) {
+        const uint64_t zz = __shfl_sync(0xffffffffu, lr.z[hh], src_lane);
+        const uint64_t ll = __shfl_sync(0xffffffffu, lr.lo[hh], src_lane);
+        const uint64_t uu = __shfl_sync(0xffffffffu, lr.hi[hh], src_lane);
+        if (hh == h) {
+            z = zz;
+            lo = ll;
+            hi = uu;
+        }
+    }
+}
+
+// write the band's row spans into a ring slot (lanes of one warp)
+__device__ __forceinline__ void store_row_spans(const LaneRows& lr, int lane, uint64_t* row_z,
+                                                uint32_t* row_lo, uint32_t* row_n) {
+#pragma unroll
+    for (int h = 0; h < kRowsPerLane; ++h) {
+        const int r = lane + 32 * h;
+        if (kRows >= 32 || lane < kRows) {
+            row_z[r] = lr.z[h];
+            row_lo[r] = static_cast<uint32_t>(lr.lo[h]);
+            row_n[r] = static_cast<uint32_t>(lr.hi[h] > lr.lo[h] ? lr.hi[h] - lr.lo[h] : 0);
+        }
+    }
 }
 
 // (z, len) of tile row r from the warp's LaneRows (all lanes must call)
@@ -234,7 +374,7 @@ __device__ __forceinline__ void store_rows(const LaneRows& lr, int lane, uint64_
     }
 }
 
-template <bool kProbs>
+template <bool kProbs, bool kSplit>
 __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmem<kProbs>& sm = *reinterpret_cast<TileSmem<kProbs>*>(smem_raw);
@@ -258,7 +398,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         // row e % kRows = pt % kRows): kRows consecutive threads copy one
         // column's run. Direct side: element e is (row e / kCols = pt / kCols +
         // kDstRowStep k, column e % kCols = pt % kCols): kCols threads per row run. The row
-        // table lives in lanes 0..15 of every producer warp (tile_rows) and is
+        // table lives in every producer warp's lanes (tile_rows_split) and is
         // fetched by shuffles.
         const int pt = tid - 32 * kProducerWarp;
         const int r_src = pt & (kRows - 1);
@@ -266,47 +406,57 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         const int dst_r0 = pt / kCols, dst_c = pt % kCols;
         int stage = 0;
         uint32_t phase = 0;
-        for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-            const uint64_t j0 = tile * kRows;
+        for (CtaWork<kSplit> wk(p); wk.valid(); wk.next()) {
+            const uint64_t j0 = wk.band() * kRows;
+            const uint64_t lo_col = wk.lo();
             LaneRows lr;
-            const uint64_t tlen = tile_rows(p, j0, lane, lr);
-            const bool last_tile = tile + gridDim.x >= p.ntiles;
+            const uint64_t tend = tile_rows_split(p, j0, lane, lr, lo_col, wk.hi());
+            const uint64_t iend = tend > lo_col ? tend : lo_col + 1;  // >= 1 chunk per item
             // this thread's source row r_src = lane + 32 * (warp-uniform h)
-            const uint64_t rl = lr.len[kRowsPerLane > 1 ? (r_src >> 5) : 0];
+            const int hs = kRowsPerLane > 1 ? (r_src >> 5) : 0;
+            // spans as (lo, n), 32-bit: pos in [lo, lo + n) <=> pos - lo < n (unsigned)
+            const uint32_t rlo = static_cast<uint32_t>(lr.lo[hs]);
+            const uint32_t rn = static_cast<uint32_t>(lr.hi[hs] > lr.lo[hs] ? lr.hi[hs] - lr.lo[hs] : 0);
             // source index of this thread's copies, advanced by kCols*m per chunk
             uint64_t sidx[kCopiesPerProducer];
             const double2* dptr[kCopiesPerProducer];
-            uint64_t dlen[kCopiesPerProducer];
+            uint32_t dlo[kCopiesPerProducer], dn[kCopiesPerProducer];
 #pragma unroll
             for (int k = 0; k < kCopiesPerProducer; ++k) {
-                const uint64_t c = src_c0 + (kProducers / kRows) * k;
+                const uint64_t c = lo_col + src_c0 + (kProducers / kRows) * k;
                 sidx[k] = addmod(j0 + r_src, mulmod_shoup(c, p.m, p.m_sh, p.N), p.N);
-                uint64_t dz;
-                row_from_lanes(lr, dst_r0 + kDstRowStep * k, dz, dlen[k]);
-                dptr[k] = p.X + dz + dst_c;
+                uint64_t dz, l, h;
+                row_span_from_lanes(lr, dst_r0 + kDstRowStep * k, dz, l, h);
+                dlo[k] = static_cast<uint32_t>(l);
+                dn[k] = static_cast<uint32_t>(h > l ? h - l : 0);
+                dptr[k] = p.X + dz + lo_col + dst_c;
             }
-            for (uint64_t i0 = 0; i0 < tlen; i0 += kCols) {
+            for (uint64_t i0 = lo_col; i0 < iend; i0 += kCols) {
                 mbar_wait(&sm.empty[stage], phase ^ 1);
                 TileStage& st = sm.stage[stage];
 #pragma unroll
                 for (int k = 0; k < kCopiesPerProducer; ++k) {
-                    const int c = src_c0 + (kProducers / kRows) * k;
-                    if (i0 + c < rl) cp_async16(&st.src[c][r_src], p.X + sidx[k]);
+                    const uint32_t pos =
+                        static_cast<uint32_t>(i0) + src_c0 + (kProducers / kRows) * k;
+                    if (pos - rlo < rn)
+                        cp_async16(&st.src[src_c0 + (kProducers / kRows) * k][r_src],
+                                   p.X + sidx[k]);
                     sidx[k] = addmod(sidx[k], p.m_chunk, p.N);
                 }
 #pragma unroll
                 for (int k = 0; k < kCopiesPerProducer; ++k) {
-                    if (i0 + dst_c < dlen[k])
+                    const uint32_t pos = static_cast<uint32_t>(i0) + dst_c;
+                    if (pos - dlo[k] < dn[k])
                         cp_async16(&st.dst[dst_r0 + kDstRowStep * k][dst_c], dptr[k]);
                     dptr[k] += kCols;
                 }
                 cp_async_arrive(&sm.full[stage]);
                 if (warp == kProducerWarp) {
-                    store_rows(lr, lane, st.row_z, st.row_l);
+                    store_row_spans(lr, lane, st.row_z, st.row_lo, st.row_n);
                     __syncwarp();  // row table stores ordered before lane 0's release
                     if (lane == 0) {
                         st.i0 = i0;
-                        st.last = (last_tile && i0 + kCols >= tlen) ? 1 : 0;
+                        st.last = (wk.last() && i0 + kCols >= iend) ? 1 : 0;
                         mbar_arrive(&sm.full[stage]);
                     }
                 }
@@ -330,18 +480,20 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         double2 carry[kRowsPerConsumer];
 #pragma unroll
         for (int q = 0; q < kRowsPerConsumer; ++q) carry[q] = make_double2(0.0, 0.0);
-        bool more = blockIdx.x < p.ntiles;
+        bool more = true;  // every CTA has >= 1 item, every item >= 1 chunk
         while (more) {
             mbar_wait(&sm.full[stage], phase);
             TileStage& st = sm.stage[stage];
-            const uint64_t pos = st.i0 + c;
+            const uint32_t i0 = static_cast<uint32_t>(st.i0);
+            const uint32_t pos = i0 + c;
             more = st.last == 0;
             const int b = static_cast<int>(k % kNormBufs);
             if (kProbs && k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
 #pragma unroll
             for (int q = 0; q < kRowsPerConsumer; ++q) {
                 const int r = rg * kRowsPerConsumer + q;
-                const bool live = pos < st.row_l[r];
+                const uint32_t rlo = kSplit ? st.row_lo[r] : 0u, rn = st.row_n[r];
+                const bool live = pos - rlo < rn;
                 double h0r, h0i, h1r, h1i;
                 stage_pair(p.sc, st.dst[r][c], st.src[c][r], h0r, h0i, h1r, h1i);
                 if (kProbs) {
@@ -349,23 +501,23 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                     sm.nrm[b][1][r][c] = live ? cnorm(h1r, h1i) : 0.0;
                 } else if (kSectorShift) {
                     const double2 hv = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
-                    const uint64_t rz = st.row_z[r], rl = st.row_l[r];
+                    const uint64_t rz = st.row_z[r];
                     if ((rz & 1) == 0) {
                         if (live) p.Y[rz + pos] = hv;
                     } else {
                         // lane c stores column c - 1; lane 0 the previous chunk's column 31
+                        // (carried: i0 - 1 >= row_lo means that chunk was this CTA's)
                         const double2 up = make_double2(__shfl_up_sync(0xffffffffu, hv.x, 1),
                                                         __shfl_up_sync(0xffffffffu, hv.y, 1));
                         const double2 last = make_double2(__shfl_sync(0xffffffffu, hv.x, 31),
                                                           __shfl_sync(0xffffffffu, hv.y, 31));
-                        const uint64_t i0 = st.i0;
                         if (c > 0) {
-                            if (pos - 1 < rl) p.Y[rz + pos - 1] = up;
-                        } else if (i0 > 0 && i0 - 1 < rl) {
+                            if (pos - 1 - rlo < rn) p.Y[rz + pos - 1] = up;
+                        } else if (i0 - 1 - rlo < rn) {  // (i0 = 0 wraps: never below 2^32 - 1 - lo)
                             p.Y[rz + i0 - 1] = carry[q];
                         }
-                        // the row's final element when it falls in column 31 of its last chunk
-                        if (c == kCols - 1 && pos + 1 == rl) p.Y[rz + pos] = hv;
+                        // the span's final element when it falls in column 31 of its last chunk
+                        if (c == kCols - 1 && live && pos + 1 == rlo + rn) p.Y[rz + pos] = hv;
                         carry[q] = last;
                     }
                 } else if (live) {
@@ -393,19 +545,25 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         DigitWindow win;
         window_reset(win);
         uint64_t k = 0;
-        for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-            const uint64_t j0 = tile * kRows;
+        for (CtaWork<kSplit> wk(p); wk.valid(); wk.next()) {
+            const uint64_t j0 = wk.band() * kRows;
+            const uint64_t lo_col = wk.lo();
             LaneRows lr;
-            const uint64_t tlen = tile_rows(p, j0, lane, lr);
+            const uint64_t tend = tile_rows_split(p, j0, lane, lr, lo_col, wk.hi());
+            const uint64_t iend = tend > lo_col ? tend : lo_col + 1;
             const int hsel = kRowsPerLane > 1 ? ((ct >> 5) % kRowsPerLane) : 0;  // row cr = lane + 32 hsel
             const uint64_t c_z = lr.z[hsel], c_len = lr.len[hsel];
+            const uint64_t c_lo = lr.lo[hsel], c_hi = lr.hi[hsel];
+            // head positions belong to the block shared with the predecessor row
+            // (k_tile_fixup); c_lo > 0 is a block boundary, hence >= c_head
             const uint64_t c_head = (256 - (c_z & 255)) & 255;
+            const uint64_t c_fast = c_lo > c_head ? c_lo : c_head;
             double c_s = 0.0;
-            for (uint64_t i0 = 0; i0 < tlen; i0 += kCols, ++k) {
+            for (uint64_t i0 = lo_col; i0 < iend; i0 += kCols, ++k) {
                 const int b = static_cast<int>(k % kNormBufs);
                 named_sync(kNormFull0 + b, kNormSync);
                 const double* row = &sm.nrm[b][cg][cr][0];
-                if (i0 >= c_head && i0 + kCols <= c_len) {
+                if (i0 >= c_fast && i0 + kCols <= c_hi) {
                     // interior chunk (the common case): 64 in-order adds, branch-free.
                     // At most one block ends inside the chunk (kCols <= 256), at
                     // column qb: the block's fold continues in `a`, the next block
@@ -430,17 +588,18 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                     } else {
                         c_s = a;
                     }
-                } else if (i0 < c_len) {
-                    // row start (head positions belong to the block shared with the
-                    // predecessor row, finished by k_tile_fixup) or row end
-                    const int q1 = static_cast<int>(min(c_len - i0, uint64_t(kCols)));
-                    int qa = 0;
-                    if (i0 < c_head) {
-                        qa = static_cast<int>(min(c_head - i0, uint64_t(q1)));
+                } else if (i0 < c_hi && i0 + kCols > c_lo) {
+                    // span start / end: the row's head (stored for k_tile_fixup), then
+                    // blocks folded in order
+                    const int q1 = static_cast<int>(min(c_hi - i0, uint64_t(kCols)));
+                    int qa = c_lo > i0 ? static_cast<int>(c_lo - i0) : 0;
+                    if (i0 + qa < c_head) {
+                        const int qh = static_cast<int>(min(c_head - i0, uint64_t(q1)));
                         double* head = p.head + ((j0 + cr) * 2 + cg) * 256 + i0;
-                        for (int cc = 0; cc < qa; ++cc) head[cc] = row[cc];
+                        for (int cc = qa; cc < qh; ++cc) head[cc] = row[cc];
+                        qa = qh;
                     }
-                    if (qa < q1) {
+                    while (qa < q1) {
                         const int qb = qa + static_cast<int>(255 - ((c_z + i0 + qa) & 255));
                         if (qb < q1) {
                             for (int cc = qa; cc <= qb; ++cc) c_s = __dadd_rn(c_s, row[cc]);
@@ -448,14 +607,16 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                             window_add(win, c_s, sm.digits[cg]);
                             c_s = 0.0;
                             qa = qb + 1;
+                        } else {
+                            for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, row[cc]);
+                            qa = q1;
                         }
-                        for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, row[cc]);
                     }
                 }
                 __syncwarp();
                 named_arrive(kNormEmpty0 + b, kNormSync);
             }
-            if (c_len > 0) {
+            if (c_len > 0 && c_hi == c_len && c_lo < c_hi) {  // this CTA ran the row's end
                 const uint64_t end = c_z + c_len;
                 if ((end & 255) != 0) {
                     if (end == p.N) {  // the final (partial) block of Z_N
