@@ -343,7 +343,7 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
     }
     if (rc) return rc;
     rc = launch(e, 1, [&] {
-        k_finalize<<<1, 128, 0, e->stream>>>(e->partials, nparts, e->S, e->nb, e->kahan ? 1 : 0,
+        k_finalize<<<1, kFinalizeThreads, 0, e->stream>>>(e->partials, nparts, e->S, e->nb, e->kahan ? 1 : 0,
                                              e->d_out);
     });
     if (rc) return rc;

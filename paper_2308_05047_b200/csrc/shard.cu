@@ -415,7 +415,7 @@ int shs_shard_probs(shs_shard* sh, uint32_t s, uint64_t lo, uint64_t hi,
             } else {
                 k_stage_probs<kSrcDirect, false><<<g, kThreads, 0, sh->stream>>>(p);
             }
-            k_sum_partials<<<1, 128, 0, sh->stream>>>(sh->partials, g, sh->d_digits);
+            k_sum_partials<<<1, kFinalizeThreads, 0, sh->stream>>>(sh->partials, g, sh->d_digits);
         });
         if (rc) return rc;
         SHD_CUDA(cudaMemcpyAsync(sh->h_digits, sh->d_digits, sizeof(unsigned long long) * 2 * kDigits,

@@ -121,7 +121,31 @@ __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
 
 // p0/p1 from the stage. kahan: reference combine_blocks (statevector.cpp:32-40),
 // two interleaved sequential chains, zeros skipped; else exact sum of partials.
-static __global__ void k_finalize(const unsigned long long* __restrict__ partials, int nparts,
+constexpr int kFinalizeSlices = 12;
+constexpr int kFinalizeThreads = 2 * kDigits * kFinalizeSlices;  // 960
+
+// acc = the sum of the nparts per-CTA digit slots (carry-save). kFinalizeSlices x
+// 80 threads: slice l sums slots l, l + kFinalizeSlices, ... (coalesced 640 B
+// rows), then one thread per digit adds the slices. Ends with __syncthreads().
+__device__ __forceinline__ void sum_slots(const unsigned long long* __restrict__ partials,
+                                          int nparts, unsigned long long (*acc)[kDigits]) {
+    __shared__ unsigned long long red[kFinalizeSlices][2 * kDigits];
+    const int i = threadIdx.x % (2 * kDigits), l = threadIdx.x / (2 * kDigits);
+    if (l < kFinalizeSlices) {
+        unsigned long long s = 0;
+        for (int c = l; c < nparts; c += kFinalizeSlices) s += partials[uint64_t(c) * 2 * kDigits + i];
+        red[l][i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * kDigits) {
+        unsigned long long s = 0;
+        for (int k = 0; k < kFinalizeSlices; ++k) s += red[k][threadIdx.x];
+        (&acc[0][0])[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+static __global__ void __launch_bounds__(kFinalizeThreads) k_finalize(const unsigned long long* __restrict__ partials, int nparts,
                            const double* __restrict__ S, uint64_t nb, int kahan,
                            double* __restrict__ out) {
     __shared__ unsigned long long acc[2][kDigits];
@@ -148,26 +172,16 @@ static __global__ void k_finalize(const unsigned long long* __restrict__ partial
         }
         return;
     }
-    for (int i = threadIdx.x; i < 2 * kDigits; i += blockDim.x) {
-        unsigned long long s = 0;
-        for (int c = 0; c < nparts; ++c) s += partials[uint64_t(c) * 2 * kDigits + i];
-        (&acc[0][0])[i] = s;
-    }
-    __syncthreads();
+    sum_slots(partials, nparts, acc);
     if (threadIdx.x < 2) out[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
 }
 
 // The exact digits of this engine's (or shard's) partial masses: sum of the
 // per-CTA digit slots, carry-normalised to 32-bit digits (for an allreduce).
-static __global__ void k_sum_partials(const unsigned long long* __restrict__ partials, int nparts,
+static __global__ void __launch_bounds__(kFinalizeThreads) k_sum_partials(const unsigned long long* __restrict__ partials, int nparts,
                                unsigned long long* __restrict__ out) {
     __shared__ unsigned long long acc[2][kDigits];
-    for (int i = threadIdx.x; i < 2 * kDigits; i += blockDim.x) {
-        unsigned long long s = 0;
-        for (int c = 0; c < nparts; ++c) s += partials[uint64_t(c) * 2 * kDigits + i];
-        (&acc[0][0])[i] = s;
-    }
-    __syncthreads();
+    sum_slots(partials, nparts, acc);
     if (threadIdx.x < 2) {
         unsigned long long carry = 0;
         for (int i = 0; i < kDigits; ++i) {

@@ -28,6 +28,10 @@ inline constexpr uint64_t kTileMinRowsPlan = 256;      // >= 8 tiles of kRows ro
 #define SHS_TILE_MIN_CHUNKS 16
 #endif
 inline constexpr uint64_t kTileAvgRow = SHS_TILE_AVG_ROW;  // H <= N / kTileAvgRow
+#ifndef SHS_TILE_TARGET_ROW
+#define SHS_TILE_TARGET_ROW 8192
+#endif
+inline constexpr uint64_t kTileTargetRow = SHS_TILE_TARGET_ROW;  // preferred mean row length
 // AUTO mode keeps the direct kernels when a plan has fewer chunks than this many
 // per CTA (a CTA's range cut costs up to 256 / kCols partly masked chunks)
 inline constexpr uint64_t kTileMinChunksPerCTA = SHS_TILE_MIN_CHUNKS;
@@ -87,8 +91,9 @@ inline void make_tile_split(TilePlanHost& pl, int cap) {
     }
 }
 
-// Pick the largest row count H (powers of two and 3 * 2^k up to N/1024) whose
-// three gap lengths are all >= kTileMinRow and at most 3x the mean row: one
+// Pick a row count H (powers of two and 3 * 2^k up to N / kTileAvgRow) whose
+// three gap lengths are all >= kTileMinRow and at most 3x the mean row, the
+// largest such H <= N / kTileTargetRow or else the smallest above it: one
 // O(H) scan of j*A mod N with running argmin / argmax gives u(H), v(H) for
 // every candidate. Multipliers without such an H (tiny A, or A/N with a huge
 // partial quotient) keep the direct gather, whose warps then read a few long
@@ -115,8 +120,11 @@ inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tilin
         const uint64_t du = umin, dv = N - vmax;
         // rows must be long enough (each 256-block touches <= 2 rows) and balanced
         // (the longest row, du + dv, within 3x the mean N / H), else a tile idles SMs
+        // prefer rows of about kTileTargetRow (fewer rows: fewer heads to fix up):
+        // the largest valid H <= N / kTileTargetRow, else the smallest valid H
         if (H >= kTileMinRowsPlan && du >= kTileMinRow && dv >= kTileMinRow &&
-            du + dv <= 3 * (N / H + 1) && du + dv < (1ull << 31)) {  // 32-bit row spans
+            du + dv <= 3 * (N / H + 1) && du + dv < (1ull << 31) &&  // 32-bit row spans
+            (!pl.tiled || H * kTileTargetRow <= N)) {
             pl.tiled = true;
             pl.H = H;
             pl.u = uj;

@@ -637,7 +637,9 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
 }
 
 // The block straddling the boundary between a row and its z-order predecessor:
-// S_b = fold(predecessor's tail partial, this row's head norms).
+// S_b = fold(predecessor's tail partial, this row's head norms). One thread per
+// (row, group); the head loads are issued 16 ahead of the (inherently serial)
+// fold, each thread's 16 from the same one or two L1 lines.
 static __global__ void __launch_bounds__(256) k_tile_fixup(TileParams p, unsigned long long* slots) {
     __shared__ unsigned long long digits[2][kDigits];
     const int tid = threadIdx.x;
@@ -651,11 +653,19 @@ static __global__ void __launch_bounds__(256) k_tile_fixup(TileParams p, unsigne
         const uint64_t j = idx >> 1;
         const int g = static_cast<int>(idx & 1);
         const uint64_t z = mulmod_shoup(j, p.A, p.A_sh, p.N);
-        const uint64_t hl = (256 - (z & 255)) & 255;
+        const uint32_t hl = static_cast<uint32_t>((256 - (z & 255)) & 255);
         if (hl == 0) continue;
         double s = p.tail[j * 2 + g];
         const double* head = p.head + (j * 2 + g) * 256;
-        for (uint64_t q = 0; q < hl; ++q) s = __dadd_rn(s, head[q]);
+        uint32_t q = 0;
+        for (; q + 16 <= hl; q += 16) {
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = head[q + u];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) s = __dadd_rn(s, v[u]);
+        }
+        for (; q < hl; ++q) s = __dadd_rn(s, head[q]);
         p.S[g * p.nb + (z >> 8)] = s;
         window_add(g ? w1 : w0, s, digits[g]);
     }
