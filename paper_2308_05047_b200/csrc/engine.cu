@@ -167,6 +167,20 @@ int sync(shs_engine* e) {
     return SHS_OK;
 }
 
+// Direct-kernel stages with a small multiplier stage their A gathered runs
+// through shared memory (stage_kernels.cuh kSrcStreams) from 16 MB of state on:
+// always in the collapse pass; in the probs pass, whose in-order block folds
+// stall the staged CTAs, only from A = kStreamsProbsMinA (config 4, B200:
+// A = 625 probs 92 -> 51 ms, collapse 119 -> 46 ms; A = 25 collapse 65 -> 36 ms,
+// probs 40 either way; A = 5 probs 32 ms gathered vs 41 ms staged).
+constexpr uint32_t kStreamsProbsMinA = 64;
+bool streams_stage(const shs_engine* e, uint32_t s) {
+    return e->a_pows[s] != 1 && e->a_pows[s] <= kStreamsMaxA && e->N >= kTileAutoMinN &&
+           e->opt.tiling != SHS_TILING_OFF;
+}
+
+size_t streams_smem(const StageParams& p) { return sizeof(double2) * p.A * p.W; }
+
 StageParams params_for(const shs_engine* e, uint32_t s) {
     StageParams p{};
     p.X = e->X;
@@ -183,6 +197,12 @@ StageParams params_for(const shs_engine* e, uint32_t s) {
     p.nb = e->nb;
     p.partials = e->partials;
     p.nchunks = e->nchunks;
+    if (streams_stage(e, s)) {
+        p.A = static_cast<uint32_t>(e->a_pows[s]);
+        p.W = (kChunk + 2 * p.A - 1) / p.A | 1u;  // ceil((A - 1 + kChunk) / A), odd
+        p.invA = 1.0f / static_cast<float>(p.A);
+        p.invW = 1.0f / static_cast<float>(p.W);
+    }
     return p;
 }
 
@@ -220,12 +240,18 @@ int grid_for(const shs_engine* e) {
 
 template <bool G, bool E1>
 void launch_probs(shs_engine* e, const StageParams& p) {
-    k_stage_probs<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
+    if (G && p.A >= kStreamsProbsMinA)
+        k_stage_probs<kSrcStreams, E1><<<grid_for(e), kThreads, streams_smem(p), e->stream>>>(p);
+    else
+        k_stage_probs<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
 }
 
 template <bool G, bool E1>
 void launch_collapse(shs_engine* e, const StageParams& p) {
-    k_stage_collapse<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
+    if (G && p.A)
+        k_stage_collapse<kSrcStreams, E1><<<grid_for(e), kThreads, streams_smem(p), e->stream>>>(p);
+    else
+        k_stage_collapse<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
 }
 
 void release(shs_engine* e) {
@@ -653,6 +679,13 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     e->grid_cap = std::max(1, occ) * e->num_sms;
     // one persistent TMA-pipelined CTA per SM for the tiled passes
+    // kSrcStreams: up to kStreamsMaxA * 5 staged amplitudes (80 KB) of dynamic smem
+    for (auto fn : {k_stage_probs<kSrcStreams, false>, k_stage_probs<kSrcStreams, true>,
+                    k_stage_collapse<kSrcStreams, false>, k_stage_collapse<kSrcStreams, true>}) {
+        ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double2) * kStreamsMaxA * 5));
+        if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(streams)");
+    }
     for (auto fn : {k_tiled<true, false>, k_tiled<true, true>}) {
         ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tile_smem_bytes<true>()));

@@ -10,6 +10,11 @@
 //               add / conditional subtract) — single engine only (z0 = 0)
 //   kSrcDirect  sel[z] itself (identity stage: a_pow = 1)
 //   kSrcBuffer  P[z - z0], the value a separate exchange already gathered
+//   kSrcStreams small multipliers A (the last stages: a, a^2, a^4 ...): with
+//               z = A q + r, src z = q + r a_inv mod N, so a chunk's gathered
+//               side is A contiguous runs (one per residue r); they are staged
+//               through shared memory with coalesced loads instead of one
+//               scattered 16 B request per amplitude — single engine only
 // and kE1 replaces sel by the implicit run start e_1 (no memory traffic).
 #pragma once
 
@@ -17,7 +22,9 @@
 
 namespace shs {
 
-enum SrcMode : int { kSrcGather = 0, kSrcDirect = 1, kSrcBuffer = 2 };
+enum SrcMode : int { kSrcGather = 0, kSrcDirect = 1, kSrcBuffer = 2, kSrcStreams = 3 };
+
+constexpr uint32_t kStreamsMaxA = 1024;  // kSrcStreams: A <= this (<= 80 KB staged per CTA)
 
 struct StageParams {
     const double2* X;   // sel over [z0, zend), local index z - z0
@@ -33,7 +40,20 @@ struct StageParams {
     unsigned long long* partials;  // [gridDim.x][2][kDigits]
     uint64_t nchunks;
     int sel;          // collapse: group kept
+    // kSrcStreams: the stage multiplier A, the staged run stride W (odd: the
+    // residue-major reads are bank-conflict free), 1/A and 1/W for small divisions
+    uint32_t A, W;
+    float invA, invW;
 };
+
+// floor(d / D) for d < 2^20, D <= 2^11, from a float reciprocal and one correction
+__device__ __forceinline__ uint32_t small_div(uint32_t d, uint32_t D, float invD) {
+    uint32_t q = __float2uint_rz(__fmul_rn(__uint2float_rn(d) + 0.5f, invD));
+    if (q * D > d) --q;
+    else if ((q + 1) * D <= d) ++q;
+    return q;
+}
+
 
 // amplitude at GLOBAL index z; under kE1 the run-start state e_1 (inv = 1)
 template <bool kE1>
@@ -41,6 +61,38 @@ __device__ __forceinline__ double2 load_amp(const double2* __restrict__ X, uint6
                                             uint64_t z0) {
     if (kE1) return make_double2(z == 1 ? 1.0 : 0.0, 0.0);
     return __ldg(X + (z - z0));
+}
+
+// kSrcStreams: stage the gathered side of chunk c, buf[r * W + w] = sel[src z]
+// for z = A (q_lo + w) + r in the chunk (q_lo = floor(chunk start / A)).
+// Returns rho = chunk start mod A once this thread's copies have landed; callers
+// fence buf with __syncthreads().
+template <bool kE1>
+__device__ __forceinline__ uint32_t stage_streams(const StageParams& p, uint64_t c,
+                                                  double2* __restrict__ buf) {
+    const uint64_t zc = c * kChunk;
+    const uint64_t q_lo = zc / p.A;
+    const uint32_t rho = static_cast<uint32_t>(zc - q_lo * p.A);
+    const uint32_t nf = p.A * p.W;
+    for (uint32_t f = threadIdx.x; f < nf; f += kThreads) {
+        const uint32_t r = small_div(f, p.W, p.invW);
+        const uint32_t w = f - r * p.W;
+        const uint32_t d = w * p.A + r;  // z - zc + rho
+        if (d >= rho && d - rho < kChunk && zc + (d - rho) < p.zend) {
+            uint64_t src = mulmod_shoup(r, p.m, p.m_sh, p.N) + q_lo + w;
+            if (src >= p.N) src -= p.N;
+            if (kE1) {
+                buf[f] = load_amp<kE1>(p.X, src, 0);
+            } else {  // asynchronous 16 B copy (LDGSTS): the loop never waits on DRAM
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(buf + f))),
+                             "l"(p.X + src)
+                             : "memory");
+            }
+        }
+    }
+    if (!kE1) asm volatile("cp.async.wait_all;" ::: "memory");
+    return rho;
 }
 
 // (sel[z], gathered[z]) for the kPer elements zg + e*kBlock of one thread
@@ -55,12 +107,26 @@ __device__ __forceinline__ void load_pairs(const StageParams& p, uint64_t zg, do
             xa[e] = load_amp<kE1>(p.X, z, p.z0);
             if (kMode == kSrcGather) xs[e] = load_amp<kE1>(p.X, src, p.z0);
             else if (kMode == kSrcBuffer) xs[e] = p.Xs[z - p.z0];
+            else if (kMode == kSrcStreams) xs[e] = xa[e];  // replaced from the staged runs
             else xs[e] = xa[e];
         } else {
             xa[e] = make_double2(0.0, 0.0);
             xs[e] = xa[e];
         }
         if (kMode == kSrcGather) src = addmod(src, p.m_step, p.N);
+    }
+}
+
+// kSrcStreams: the gathered values of this thread's kPer elements from the staged runs
+__device__ __forceinline__ void read_streams(const StageParams& p, uint32_t rho,
+                                             const double2* __restrict__ buf,
+                                             double2 (&xs)[kPer]) {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        const uint32_t d = rho + threadIdx.x + e * kBlock;
+        const uint32_t w = small_div(d, p.A, p.invA);
+        const uint32_t r = d - w * p.A;
+        xs[e] = buf[r * p.W + w];
     }
 }
 
@@ -79,6 +145,7 @@ __device__ __forceinline__ void write_cta_digits(unsigned long long (*digits)[kD
 
 template <int kMode, bool kE1>
 __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
+    extern __shared__ double2 streams_buf[];      // kSrcStreams: [A][W]
     __shared__ double nrm[2 * kPer][kBlock + 1];  // +1: conflict-free column walks
     __shared__ unsigned long long digits[2][kDigits];
     const int tid = threadIdx.x;
@@ -90,7 +157,14 @@ __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = p.z0 + c * kChunk + tid;
         double2 xa[kPer], xs[kPer];
+        uint32_t rho = 0;
+        if (kMode == kSrcStreams) rho = stage_streams<kE1>(p, c, streams_buf);
         load_pairs<kMode, kE1>(p, zg, xa, xs);
+        if (kMode == kSrcStreams) {
+            __syncthreads();  // staged runs complete (the previous chunk's reads ended
+                              // before its fold barrier)
+            read_streams(p, rho, streams_buf, xs);
+        }
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             double h0r, h0i, h1r, h1i;
@@ -194,11 +268,21 @@ static __global__ void __launch_bounds__(kFinalizeThreads) k_sum_partials(const 
 
 template <int kMode, bool kE1>
 __global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
+    extern __shared__ double2 streams_buf[];  // kSrcStreams: [A][W]
     const int tid = threadIdx.x;
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = p.z0 + c * kChunk + tid;
         double2 xa[kPer], xs[kPer];
+        uint32_t rho = 0;
+        if (kMode == kSrcStreams) {
+            __syncthreads();  // the previous chunk's reads of the staged runs ended
+            rho = stage_streams<kE1>(p, c, streams_buf);
+        }
         load_pairs<kMode, kE1>(p, zg, xa, xs);
+        if (kMode == kSrcStreams) {
+            __syncthreads();
+            read_streams(p, rho, streams_buf, xs);
+        }
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const uint64_t z = zg + uint64_t(e) * kBlock;

@@ -297,6 +297,37 @@ def test_tiled_work_split_vs_direct(cuda_ok, N, a):
         prefix |= b << s
 
 
+@pytest.mark.parametrize("N,a", [(16777207, 2), (268435247, 3), (4194301, 7)])
+def test_small_multiplier_streams_vs_gather(cuda_ok, N, a):
+    """The last stages (multipliers a, a^2, a^4 ... <= 1024) stage their A
+    gathered runs through shared memory (kSrcStreams, from the run start e_1 and
+    from a general state): bit-identical to the per-amplitude gather."""
+    rng = np.random.default_rng(N + a)
+    fast, ref = engine(N, a), engine(N, a, tiling="off")
+    pows = fast.stage_multipliers()
+    s0 = fast.t - 6
+    assert sum(1 for s in range(s0, fast.t) if 1 < pows[s] <= 1024) >= 2
+    fast.state_init()
+    ref.state_init()
+    prefix = 0
+    for s in range(s0, fast.t):
+        p = fast.stage_probs(s, prefix)
+        assert p == ref.stage_probs(s, prefix), s
+        d0, d1 = fast.block_sums()
+        e0, e1 = ref.block_sums()
+        assert np.array_equal(d0, e0) and np.array_equal(d1, e1), s
+        if s + 1 == fast.t:
+            break
+        b = int(rng.integers(2)) if min(p) > 1e-300 else int(p[1] > p[0])
+        fast.stage_collapse(b, p[b])
+        ref.stage_collapse(b, p[b])
+        for first in [0, N - 4096] + [int(x) for x in rng.integers(0, N - 4096, 6)]:
+            for x in (0, 1):
+                assert np.array_equal(arr(fast.state_read(x, first, 4096)),
+                                      arr(ref.state_read(x, first, 4096))), (s, first)
+        prefix |= b << s
+
+
 # ------------------------------------------------- full-size properties
 def test_c3_size_run_properties(cuda_ok, oracle):
     """N = 16777207 (config 3): first stages match the oracle exactly; the full
