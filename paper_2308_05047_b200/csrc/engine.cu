@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +82,8 @@ struct shs_engine {
     double* head = nullptr;  // [max_rows][2][256]
     double* tail = nullptr;  // [max_rows][2]
     uint2* split = nullptr;  // [t][tiled_cap + 1] CTA range starts of the tiled stages
+    unsigned long long* band_ctr = nullptr;  // k_tiled<., false> dynamic band counter
+    uint64_t band_issued = 0;                // its value before the next launch
     bool kahan = false;      // resolved combine mode
     // state
     bool e1 = true;
@@ -225,6 +228,8 @@ TileParams tile_params_for(const shs_engine* e, uint32_t s) {
     p.ntiles = pl.ntiles;
     p.split = e->split + uint64_t(s) * (e->tiled_cap + 1);
     p.bulk_rounds = pl.bulk_rounds;
+    p.band_ctr = e->band_ctr;
+    p.band_base = e->band_issued;
     p.sc = e->sc;
     p.S = e->S;
     p.nb = e->nb;
@@ -270,6 +275,7 @@ void release(shs_engine* e) {
     cudaFree(e->head);
     cudaFree(e->tail);
     cudaFree(e->split);
+    cudaFree(e->band_ctr);
     cudaFree(e->d_apows);
     cudaFree(e->d_ainvs);
     cudaFree(e->d_ainvsh);
@@ -348,10 +354,12 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
         const int g2 = static_cast<int>(
             std::min<uint64_t>((2 * tp.H + 255) / 256, static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
-            if (pl.split_tail)
+            if (pl.split_tail) {
                 k_tiled<true, true><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
-            else
+            } else {
                 k_tiled<true, false><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
+                e->band_issued += pl.ntiles;
+            }
             k_tile_fixup<<<g2, 256, 0, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
         nparts = g1 + g2;
@@ -405,10 +413,12 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
         const int g1 = pl.split_tail ? pl.grid
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         rc = launch(e, 2, [&] {
-            if (pl.split_tail)
+            if (pl.split_tail) {
                 k_tiled<false, true><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
-            else
+            } else {
                 k_tiled<false, false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+                e->band_issued += pl.ntiles;
+            }
         });
     } else {
         StageParams p = params_for(e, e->ps);
@@ -666,9 +676,13 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     e->num_sms = prop.multiProcessorCount;
     e->tiled_cap = e->num_sms;
     e->max_rows = 0;
+    // test hook: SHS_TILE_SPLIT=0 / 1 forces the tiled kernels' work-split variant
+    const char* force_split = std::getenv("SHS_TILE_SPLIT");
     for (auto& pl : e->plans) {
         if (!pl.tiled) continue;
         make_tile_split(pl, e->tiled_cap);
+        if (force_split && (force_split[0] == '0' || force_split[0] == '1'))
+            pl.split_tail = force_split[0] == '1';
         if (o.tiling == SHS_TILING_AUTO &&
             pl.chunks < kTileMinChunksPerCTA * static_cast<uint64_t>(e->tiled_cap))
             pl.tiled = false;
@@ -705,6 +719,9 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         return fail(ce, "cudaMalloc(partials)");
     if ((ce = cudaMalloc(&e->d_out, 4 * sizeof(double))) != cudaSuccess)
         return fail(ce, "cudaMalloc(out)");
+    if ((ce = cudaMalloc(&e->band_ctr, sizeof(unsigned long long))) != cudaSuccess ||
+        (ce = cudaMemset(e->band_ctr, 0, sizeof(unsigned long long))) != cudaSuccess)
+        return fail(ce, "cudaMalloc(band_ctr)");
     if ((ce = cudaHostAlloc(&e->h_out, 4 * sizeof(double), cudaHostAllocDefault)) != cudaSuccess)
         return fail(ce, "cudaHostAlloc");
     e->device_bytes = part_bytes + 32;  // the N-amplitude buffers come with the first stage

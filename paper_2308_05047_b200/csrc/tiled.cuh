@@ -90,6 +90,8 @@ struct TileParams {
     uint64_t H, u, v, du, dv;
     uint64_t ntiles;    // bands of kRows rows
     uint64_t bulk_rounds;  // whole bands per CTA, round-robin (CtaWork)
+    unsigned long long* band_ctr;  // CtaWork<false>: bands handed out (monotonic over launches)
+    uint64_t band_base;            // band_ctr at this launch
     const uint2* split;    // [gridDim.x + 1] (band, chunk): each CTA's remainder range
     StageScalars sc;
     double* S;          // block partials, S0 [0, nb), S1 [nb, 2nb)
@@ -177,6 +179,7 @@ struct TileSmem {
     double nrm[kProbs ? kNormBufs : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
     uint64_t full[kStages], empty[kStages];
     unsigned long long digits[2][kDigits];
+    uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
 };
 
 template <bool kProbs>
@@ -258,13 +261,54 @@ __device__ __forceinline__ uint64_t tile_rows_split(const TileParams& p, uint64_
 template <bool kSplit>
 struct CtaWork;
 
+// CtaWork<false> hands out whole bands dynamically: CTA g starts with band g,
+// then its producer thread P0 takes the next band from a global counter, two
+// bands ahead, into the shared queue bandq (so a band's successor and hence its
+// "last" flag are known before its chunks are issued). Stragglers (SMs that get
+// less DRAM bandwidth) no longer set the kernel time: with static round-robin
+// bands the slowest CTA of a config-4 collapse ended 15% after the median.
+// Results do not depend on the order (block partials land in fixed slots; the
+// exact accumulator is order-independent). The counter advances by exactly
+// ntiles - gridDim.x + gridDim.x = ntiles per launch (bands gridDim.x ..
+// ntiles - 1 plus one terminal fetch per CTA), so the host keeps band_base
+// without resetting it. The chain warps read bandq[k] only after consuming band
+// k - 1, whose chunks P0 issued after writing it (mbarrier release -> consumer
+// acquire -> named barrier).
+constexpr int kBandQ = 16;  // > kStages + kNormBufs: the chain lags <= 8 chunks (bands)
+constexpr int kProducerBar = 1 + 2 * kNormBufs;  // named barrier of the producer warps
+
 template <>
 struct CtaWork<false> {
-    uint64_t b, nt;
-    __device__ __forceinline__ explicit CtaWork(const TileParams& p) : b(blockIdx.x), nt(p.ntiles) {}
+    uint32_t* q;
+    uint64_t b, nt, k;
+    bool producer, p0;
+    __device__ __forceinline__ uint64_t fetch(const TileParams& p) const {
+        return gridDim.x + (atomicAdd(p.band_ctr, 1ull) - p.band_base);
+    }
+    __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t* queue, bool is_producer)
+        : q(queue), b(blockIdx.x), nt(p.ntiles), k(0), producer(is_producer) {
+        p0 = producer && threadIdx.x == 32 * kProducerWarp;
+        if (p0) {
+            q[0] = static_cast<uint32_t>(b);
+            const uint64_t b1 = fetch(p);
+            q[1] = static_cast<uint32_t>(b1 < nt ? b1 : nt);
+        }
+        if (producer) named_sync(kProducerBar, kProducers);
+    }
     __device__ __forceinline__ bool valid() const { return b < nt; }
-    __device__ __forceinline__ void next() { b += gridDim.x; }
-    __device__ __forceinline__ bool last() const { return b + gridDim.x >= nt; }
+    __device__ __forceinline__ void next(const TileParams& p) {
+        if (p0) {
+            const uint64_t b1 = q[(k + 1) % kBandQ];
+            if (b1 < nt) {
+                const uint64_t b2 = fetch(p);
+                q[(k + 2) % kBandQ] = static_cast<uint32_t>(b2 < nt ? b2 : nt);
+            }
+        }
+        if (producer) named_sync(kProducerBar, kProducers);
+        ++k;
+        b = q[k % kBandQ];
+    }
+    __device__ __forceinline__ bool last() const { return q[(k + 1) % kBandQ] >= nt; }
     __device__ __forceinline__ uint64_t band() const { return b; }
     __device__ __forceinline__ uint64_t lo() const { return 0; }
     __device__ __forceinline__ uint64_t hi() const { return ~0ull; }
@@ -274,7 +318,7 @@ template <>
 struct CtaWork<true> {
     uint64_t k, K, b, b_first, b_last, lo_col, hi_col, nt;
     bool bulk, tail_empty;
-    __device__ __forceinline__ explicit CtaWork(const TileParams& p) {
+    __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t*, bool) {
         const uint2 s0 = p.split[blockIdx.x], s1 = p.split[blockIdx.x + 1];
         b_first = s0.x;
         lo_col = uint64_t(s0.y) * kCols;
@@ -288,7 +332,7 @@ struct CtaWork<true> {
         b = bulk ? blockIdx.x : b_first;
     }
     __device__ __forceinline__ bool valid() const { return bulk || (!tail_empty && b <= b_last); }
-    __device__ __forceinline__ void next() {
+    __device__ __forceinline__ void next(const TileParams&) {
         if (bulk) {
             if (++k < K && b + gridDim.x < nt) {
                 b += gridDim.x;
@@ -380,6 +424,10 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
     TileSmem<kProbs>& sm = *reinterpret_cast<TileSmem<kProbs>*>(smem_raw);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+#ifdef SHS_CTA_TRACE
+    uint64_t trace_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
+#endif
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -406,7 +454,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         const int dst_r0 = pt / kCols, dst_c = pt % kCols;
         int stage = 0;
         uint32_t phase = 0;
-        for (CtaWork<kSplit> wk(p); wk.valid(); wk.next()) {
+        for (CtaWork<kSplit> wk(p, sm.bandq, true); wk.valid(); wk.next(p)) {
             const uint64_t j0 = wk.band() * kRows;
             const uint64_t lo_col = wk.lo();
             LaneRows lr;
@@ -545,7 +593,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         DigitWindow win;
         window_reset(win);
         uint64_t k = 0;
-        for (CtaWork<kSplit> wk(p); wk.valid(); wk.next()) {
+        for (CtaWork<kSplit> wk(p, sm.bandq, false); wk.valid(); wk.next(p)) {
             const uint64_t j0 = wk.band() * kRows;
             const uint64_t lo_col = wk.lo();
             LaneRows lr;
@@ -634,6 +682,17 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
         __syncthreads();
         write_partials(sm.digits, p.partials + uint64_t(blockIdx.x) * 2 * kDigits, tid);
     }
+#ifdef SHS_CTA_TRACE
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t t1;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        printf("CTA %d %d %d sm %u t0 %llu t1 %llu\n", int(kProbs), int(kSplit), blockIdx.x, smid,
+               (unsigned long long)trace_t0, (unsigned long long)t1);
+    }
+#endif
 }
 
 // The block straddling the boundary between a row and its z-order predecessor:

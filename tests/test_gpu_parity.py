@@ -267,13 +267,19 @@ def test_errors_are_raised(cuda_ok):
         eng.stage_collapse(1, 0.0)
 
 
-@pytest.mark.parametrize("N,a", [(16777207, 1234567), (268435247, 3)])
-def test_tiled_work_split_vs_direct(cuda_ok, N, a):
-    """The tiled kernels in both work-split modes (N = 2^24: few bands, CTA
-    ranges cut inside bands; N = 2^28: 8192 bands round-robin) against the
-    direct-gather kernels: bit-identical 256-block partials and states."""
+@pytest.mark.parametrize("N,a,split", [(16777207, 1234567, ""), (268435247, 3, ""),
+                                       (268435247, 3, "0"), (16777207, 1234567, "0")])
+def test_tiled_work_split_vs_direct(cuda_ok, monkeypatch, N, a, split):
+    """The tiled kernels in both work-split variants against the direct-gather
+    kernels: bit-identical 256-block partials and states. Default: few bands
+    (CTA ranges cut inside bands); SHS_TILE_SPLIT=0 forces whole bands handed
+    out dynamically (the config-4 variant; at N = 2^28, 1024 bands for 148 CTAs)."""
+    if split:
+        monkeypatch.setenv("SHS_TILE_SPLIT", split)
     rng = np.random.default_rng(N)
-    tiled, direct = engine(N, a), engine(N, a, tiling="off")
+    tiled = engine(N, a)
+    monkeypatch.delenv("SHS_TILE_SPLIT", raising=False)
+    direct = engine(N, a, tiling="off")
     t = 6  # the first stages of the full schedule: "random" multipliers
     assert sum(tiled.tile_plan(s)["tiled"] for s in range(1, t)) >= t - 2
     tiled.state_init()
