@@ -18,6 +18,7 @@
 #pragma once
 
 #include "device_math.cuh"
+#include "measure.cuh"
 
 namespace shs {
 
@@ -45,34 +46,6 @@ struct BatchParams {
     int32_t* bits_out;        // [count][t][4] or null: sampled, observed, flip, error branch
     int32_t* status;          // [count]: 0 ok, SHS_ERROR, SHS_DEGENERATE_BRANCH
 };
-
-// ---- Philox4x32-10 (rng.hpp:16-31) and RngStream draws (rng.hpp:63-66)
-__device__ __forceinline__ void philox_dev(uint64_t key, uint32_t c[4]) {
-    uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
-#pragma unroll
-    for (int round = 0; round < 10; ++round) {
-        const uint64_t p0 = uint64_t(0xD2511F53u) * c[0];
-        const uint64_t p1 = uint64_t(0xCD9E8D57u) * c[2];
-        const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c[1] ^ k0;
-        const uint32_t n1 = static_cast<uint32_t>(p1);
-        const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c[3] ^ k1;
-        const uint32_t n3 = static_cast<uint32_t>(p0);
-        c[0] = n0;
-        c[1] = n1;
-        c[2] = n2;
-        c[3] = n3;
-        k0 += 0x9E3779B9u;
-        k1 += 0xBB67AE85u;
-    }
-}
-
-__device__ __forceinline__ double rng_double_dev(uint64_t seed, uint32_t a, uint32_t b,
-                                                 uint32_t domain, uint32_t index) {
-    uint32_t c[4] = {index, a, b, domain};
-    philox_dev(seed, c);
-    const uint64_t u = (uint64_t(c[0]) << 32) | c[1];
-    return __dmul_rn(static_cast<double>(u >> 11), 0x1.0p-53);
-}
 
 __device__ __forceinline__ double kahan_blocks(const double* x, int n) {
     double s = 0, c = 0;
@@ -152,32 +125,10 @@ static __global__ void __launch_bounds__(kBatchThreads) k_batch_runs(BatchParams
                 const double p1 = kahan_blocks(bsum + nb, nb);
                 sh_p0 = p0;
                 sh_p1 = p1;
-                int status = 0;
-                if (bp.check_norms && fabs(__dsub_rn(__dadd_rn(p0, p1), 1.0)) > 1e-9)
-                    status = SHS_ERROR;
-                // sample_measurement (statevector.cpp:236-256, noise.cpp:128-145)
-                uint32_t draw = 0;
-                int sbit, obit, ebranch = 0, flip = 0;
-                if (bp.kind == SHS_ERR_QUANTUM_MEASURE) {
-                    const double dxy = __dadd_rn(bp.px, bp.py);
-                    const double p1p = __dadd_rn(__dmul_rn(__dsub_rn(1.0, dxy), p1),
-                                                 __dmul_rn(dxy, __dsub_rn(1.0, p1)));
-                    sbit = rng_double_dev(bp.seed, idx32, s, 0, draw++) < p1p ? 1 : 0;
-                    const double p_bit = sbit == 1 ? p1 : __dsub_rn(1.0, p1);
-                    const double p_other = __dsub_rn(1.0, p_bit);
-                    const double p_bit_prime = sbit == 1 ? p1p : __dsub_rn(1.0, p1p);
-                    const double p_err =
-                        p_bit_prime > 0.0 ? __ddiv_rn(__dmul_rn(dxy, p_other), p_bit_prime) : 0.0;
-                    ebranch = rng_double_dev(bp.seed, idx32, s, 0, draw++) < p_err ? 1 : 0;
-                    obit = sbit;
-                } else {
-                    sbit = rng_double_dev(bp.seed, idx32, s, 0, draw++) < p1 ? 1 : 0;
-                    obit = sbit;
-                    if (bp.kind == SHS_ERR_CLASSICAL_MEASURE) {
-                        flip = rng_double_dev(bp.seed, idx32, s, 0, draw++) < bp.delta ? 1 : 0;
-                        if (flip) obit = 1 - sbit;
-                    }
-                }
+                MeasureCfg mc{bp.seed, idx32, bp.kind, bp.delta, bp.px, bp.py, bp.check_norms};
+                const DevMeasure mr = measure_dev(p0, p1, mc, s, s + 1 < bp.t);
+                const int sbit = mr.sbit, obit = mr.obit, flip = mr.flip, ebranch = mr.ebranch;
+                const int status = mr.status;
                 if (bp.p1_out) bp.p1_out[uint64_t(run) * bp.t + s] = p1;
                 if (bp.bits_out) {
                     int32_t* o = bp.bits_out + (uint64_t(run) * bp.t + s) * 4;
@@ -188,11 +139,8 @@ static __global__ void __launch_bounds__(kBatchThreads) k_batch_runs(BatchParams
                 }
                 observed |= static_cast<unsigned __int128>(obit) << s;
                 sampled |= static_cast<unsigned __int128>(sbit) << s;
-                const int src_group = ebranch ? 1 - sbit : sbit;
-                const double p_src = src_group == 1 ? p1 : p0;
-                if (s + 1 < bp.t && p_src < 1e-300) status = SHS_DEGENERATE_BRANCH;
-                sh_sel = src_group;
-                sh_inv_next = __ddiv_rn(1.0, __dsqrt_rn(p_src));
+                sh_sel = mr.src_group;
+                sh_inv_next = __ddiv_rn(1.0, __dsqrt_rn(mr.p_src));
                 if (status) {
                     bp.status[run] = status;
                     sh_stop = 1;

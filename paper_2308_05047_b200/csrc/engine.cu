@@ -112,6 +112,12 @@ struct shs_engine {
     void* d_batch_out = nullptr;
     size_t batch_out_bytes = 0;
     int batch_grid = 0;
+    // device-resident runs (engine_run_device), allocated on first use
+    DevStage* d_slots = nullptr;   // [2] stage scalars + collapse group
+    StageRec* h_rec = nullptr;     // [t] host-mapped per-stage records
+    StageRec* d_rec = nullptr;     // its device alias
+    cudaEvent_t meas_ev[2] = {nullptr, nullptr};
+    bool host_measure = false;     // SHS_HOST_MEASURE=1: the host-driven loop (A/B)
 };
 
 namespace {
@@ -283,6 +289,10 @@ void release(shs_engine* e) {
     cudaFree(e->d_batch_out);
     cudaFree(e->d_out);
     if (e->h_out) cudaFreeHost(e->h_out);
+    cudaFree(e->d_slots);
+    if (e->h_rec) cudaFreeHost(e->h_rec);
+    for (auto ev : e->meas_ev)
+        if (ev) cudaEventDestroy(ev);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -329,25 +339,32 @@ struct NvtxRange {
     ~NvtxRange() { nvtxRangePop(); }
 };
 
-int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) {
-    if (s >= e->t) return set_error(SHS_INVALID_ARGUMENT, "stage index out of range");
-    NvtxRange nvtx("shs stage probs");
-    int rc = ensure_buffers(e);
-    if (rc) return rc;
+// Host-side scalars of stage s for the observed prefix (statevector.cpp:338-349).
+StageScalars host_scalars(const shs_engine* e, uint32_t s, u128 prefix, double inv) {
     const double phi = stage_phase(s, prefix);
     const bool gather = e->a_pows[s] != 1;
-    e->sc.w0r = e->w[0];
-    e->sc.w0i = e->w[1];
-    e->sc.w1r = e->w[2];
-    e->sc.w1i = e->w[3];
-    e->sc.phr = 1.0 * std::cos(phi);  // std::polar(1.0, phi), statevector.cpp:338
-    e->sc.phi = 1.0 * std::sin(phi);
-    e->sc.inv = e->inv;
-    e->sc.phase_mul = (gather || phi != 0.0) ? 1 : 0;
-    e->ps = s;
-    int nparts = grid_for(e);
+    StageScalars sc{};
+    sc.w0r = e->w[0];
+    sc.w0i = e->w[1];
+    sc.w1r = e->w[2];
+    sc.w1i = e->w[3];
+    sc.phr = 1.0 * std::cos(phi);  // std::polar(1.0, phi), statevector.cpp:338
+    sc.phi = 1.0 * std::sin(phi);
+    sc.inv = inv;
+    sc.phase_mul = (gather || phi != 0.0) ? 1 : 0;
+    return sc;
+}
+
+// Probs pass of stage s on the current sel (tiled or direct kernels, plus the
+// tiled fixup). Scalars: e->sc, or the device slot `dev` when non-null.
+// *nparts = the exact-accumulator slots it filled.
+int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* nparts) {
+    const bool gather = e->a_pows[s] != 1;
+    int rc;
+    *nparts = grid_for(e);
     if (e->plans[s].tiled && !e->e1) {
         TileParams tp = tile_params_for(e, s);
+        tp.dev = dev;
         const TilePlanHost& pl = e->plans[s];
         const int g1 = pl.split_tail ? pl.grid
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
@@ -362,9 +379,10 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
             }
             k_tile_fixup<<<g2, 256, 0, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
-        nparts = g1 + g2;
+        *nparts = g1 + g2;
     } else {
         StageParams p = params_for(e, s);
+        p.dev = dev;
         rc = launch(e, 0, [&] {
             if (gather) {
                 if (e->e1) launch_probs<true, true>(e, p);
@@ -375,6 +393,57 @@ int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) 
             }
         });
     }
+    return rc;
+}
+
+// Collapse pass of stage s into the successor buffer (then swapped in).
+int launch_collapse_pass(shs_engine* e, uint32_t s, int src_group, const DevStage* dev) {
+    const bool gather = e->a_pows[s] != 1;
+    int rc;
+    if (e->plans[s].tiled && !e->e1) {
+        TileParams tp = tile_params_for(e, s);
+        tp.sel = src_group;
+        tp.dev = dev;
+        const TilePlanHost& pl = e->plans[s];
+        const int g1 = pl.split_tail ? pl.grid
+                                     : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
+        rc = launch(e, 2, [&] {
+            if (pl.split_tail) {
+                k_tiled<false, true><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+            } else {
+                k_tiled<false, false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+                e->band_issued += pl.ntiles;
+            }
+        });
+    } else {
+        StageParams p = params_for(e, s);
+        p.sel = src_group;
+        p.dev = dev;
+        rc = launch(e, 2, [&] {
+            if (gather) {
+                if (e->e1) launch_collapse<true, true>(e, p);
+                else launch_collapse<true, false>(e, p);
+            } else {
+                if (e->e1) launch_collapse<false, true>(e, p);
+                else launch_collapse<false, false>(e, p);
+            }
+        });
+    }
+    if (rc) return rc;
+    std::swap(e->X, e->Y);
+    e->e1 = false;
+    return SHS_OK;
+}
+
+int stage_probs(shs_engine* e, uint32_t s, u128 prefix, double* p0, double* p1) {
+    if (s >= e->t) return set_error(SHS_INVALID_ARGUMENT, "stage index out of range");
+    NvtxRange nvtx("shs stage probs");
+    int rc = ensure_buffers(e);
+    if (rc) return rc;
+    e->sc = host_scalars(e, s, prefix, e->inv);
+    e->ps = s;
+    int nparts = 0;
+    rc = launch_probs_pass(e, s, nullptr, &nparts);
     if (rc) return rc;
     rc = launch(e, 1, [&] {
         k_finalize<<<1, kFinalizeThreads, 0, e->stream>>>(e->partials, nparts, e->S, e->nb, e->kahan ? 1 : 0,
@@ -404,47 +473,137 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
     if (p_src < kDegenerateMass)  // statevector.cpp:388-390 / 265-266
         return set_error(SHS_DEGENERATE_BRANCH,
                          "impossible measurement branch at stage " + std::to_string(e->ps));
-    const bool gather = e->a_pows[e->ps] != 1;
-    int rc;
-    if (e->plans[e->ps].tiled && !e->e1) {
-        TileParams tp = tile_params_for(e, e->ps);
-        tp.sel = src_group;
-        const TilePlanHost& pl = e->plans[e->ps];
-        const int g1 = pl.split_tail ? pl.grid
-                                     : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
-        rc = launch(e, 2, [&] {
-            if (pl.split_tail) {
-                k_tiled<false, true><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
-            } else {
-                k_tiled<false, false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
-                e->band_issued += pl.ntiles;
-            }
-        });
-    } else {
-        StageParams p = params_for(e, e->ps);
-        p.sel = src_group;
-        rc = launch(e, 2, [&] {
-            if (gather) {
-                if (e->e1) launch_collapse<true, true>(e, p);
-                else launch_collapse<true, false>(e, p);
-            } else {
-                if (e->e1) launch_collapse<false, true>(e, p);
-                else launch_collapse<false, false>(e, p);
-            }
-        });
-    }
+    int rc = launch_collapse_pass(e, e->ps, src_group, nullptr);
     if (rc) return rc;
-    std::swap(e->X, e->Y);
-    e->e1 = false;
     e->inv = 1.0 / std::sqrt(p_src);  // statevector.cpp:391
     e->pending = false;
     if (wait) return sync(e);
     return SHS_OK;
 }
 
-int engine_run(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
-               shs_stage_trace* trace) {
-    NvtxRange nvtx("shs run");
+// Device-resident run (the default for engine_run): per stage the host queues
+//   probs(s) -> k_finalize_measure(s) -> collapse(s)
+// and the device measures and collapses without a host round trip. The host
+// stays one stage behind: before queueing stage s's measurement it waits for
+// stage s-1's record (the GPU is then running collapse(s-1) with probs(s)
+// queued) to learn the observed prefix, from which it computes both candidate
+// phases of stage s+1 with glibc (statevector.cpp:338). Results, errors and
+// the final engine state equal the host-driven loop's (engine_run_host).
+int ensure_device_run(shs_engine* e) {
+    if (e->d_slots) return SHS_OK;
+    SHS_CUDA(cudaMalloc(&e->d_slots, 2 * sizeof(DevStage)));
+    SHS_CUDA(cudaHostAlloc(&e->h_rec, sizeof(StageRec) * e->t, cudaHostAllocMapped));
+    SHS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_rec), e->h_rec, 0));
+    for (auto& ev : e->meas_ev) SHS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->device_bytes += 2 * sizeof(DevStage);
+    return SHS_OK;
+}
+
+int engine_run_device(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
+                      shs_stage_trace* trace) {
+    NvtxRange nvtx("shs run (device-resident)");
+    int rc = ensure_buffers(e);
+    if (rc) return rc;
+    if ((rc = ensure_device_run(e))) return rc;
+    state_init(e);
+    std::memset(e->h_rec, 0, sizeof(StageRec) * e->t);
+    MeasureCfg mc{seed, static_cast<u32>(idx), e->err.kind, e->err.delta, e->err.px, e->err.py,
+                  e->opt.check_norms};
+    u128 observed = 0, sampled = 0;
+    double inv = 1.0;                        // host mirror of stage s's inv
+    StageScalars sc = host_scalars(e, 0, 0, 1.0);
+    // read stage r's record (its measure kernel has completed) and fold it in
+    auto absorb = [&](uint32_t r) -> int {
+        cudaError_t ce = cudaEventSynchronize(e->meas_ev[r & 1]);
+        if (ce != cudaSuccess)
+            return set_error(SHS_CUDA_ERROR, std::string("event sync: ") + cudaGetErrorString(ce));
+        StageRec rec;  // written by the device; complete once its event has
+        std::memcpy(&rec, e->h_rec + r, sizeof(rec));
+        if (!rec.done) return set_error(SHS_CUDA_ERROR, "stage record missing");
+        if (trace) {
+            trace[r].cbit = r;
+            trace[r].p1 = rec.p1;
+            trace[r].sampled_bit = rec.sbit;
+            trace[r].observed_bit = rec.obit;
+            trace[r].classical_flip = static_cast<uint8_t>(rec.flip);
+            trace[r].quantum_error_branch = static_cast<uint8_t>(rec.ebranch);
+        }
+        e->p0 = rec.p0;
+        e->p1 = rec.p1;
+        if (rec.status == SHS_ERROR)
+            return set_error(SHS_ERROR, "statevector norm drifted beyond 1e-9 at stage " +
+                                            std::to_string(r));
+        if (rec.status == SHS_DEGENERATE_BRANCH)
+            return set_error(SHS_DEGENERATE_BRANCH,
+                             "impossible measurement branch at stage " + std::to_string(r));
+        observed |= u128{static_cast<unsigned>(rec.obit)} << r;
+        sampled |= u128{static_cast<unsigned>(rec.sbit)} << r;
+        if (r + 1 < e->t) {
+            const int src_group = rec.ebranch ? 1 - rec.sbit : rec.sbit;
+            inv = 1.0 / std::sqrt(src_group == 1 ? rec.p1 : rec.p0);  // statevector.cpp:391
+            sc = host_scalars(e, r + 1, observed, inv);
+        }
+        return SHS_OK;
+    };
+    auto fail = [&](int code) {
+        cudaStreamSynchronize(e->stream);  // queued stages fold zeros (inv = 0): drain them
+        if (e->timing) resolve_marks(e);
+        e->pending = false;
+        return code;
+    };
+    for (uint32_t s = 0; s < e->t; ++s) {
+        DevStage* cur = e->d_slots + (s & 1);
+        DevStage* nxt = e->d_slots + ((s + 1) & 1);
+        int nparts = 0;
+        e->sc = sc;  // stage 0's kernel arguments (later stages read the slot)
+        if ((rc = launch_probs_pass(e, s, s == 0 ? nullptr : cur, &nparts))) return fail(rc);
+        // the observed prefix through stage s-1
+        if (s > 0 && (rc = absorb(s - 1))) return fail(rc);
+        MeasureStep ms{};
+        ms.cfg = mc;
+        ms.s = s;
+        ms.collapse = s + 1 < e->t ? 1 : 0;
+        ms.init_cur = s == 0 ? 1 : 0;
+        ms.sc0 = sc;
+        ms.cur = cur;
+        ms.next = nxt;
+        if (s + 1 < e->t) {
+            for (int bit = 0; bit < 2; ++bit) {
+                const StageScalars c =
+                    host_scalars(e, s + 1, observed | (u128{static_cast<unsigned>(bit)} << s), 0.0);
+                ms.nph.phr[bit] = c.phr;
+                ms.nph.phi[bit] = c.phi;
+                ms.nph.phase_mul[bit] = c.phase_mul;
+            }
+        }
+        ms.rec = e->d_rec;
+        rc = launch(e, 1, [&] {
+            k_finalize_measure<<<1, kFinalizeThreads, 0, e->stream>>>(e->partials, nparts, e->S, e->nb,
+                                                                  e->kahan ? 1 : 0, ms);
+        });
+        if (rc) return fail(rc);
+        if (cudaEventRecord(e->meas_ev[s & 1], e->stream) != cudaSuccess)
+            return fail(set_error(SHS_CUDA_ERROR, "event record"));
+        if (s + 1 < e->t && (rc = launch_collapse_pass(e, s, 0, cur))) return fail(rc);
+    }
+    if ((rc = absorb(e->t - 1))) return fail(rc);
+    if ((rc = sync(e))) return rc;
+    // engine state as the host-driven loop leaves it: stage t-1 pending
+    e->ps = e->t - 1;
+    e->inv = inv;
+    e->sc = sc;
+    e->pending = true;
+    u128 j = observed;
+    if (e->err.kind == SHS_ERR_BITFLIP)
+        j = bitflip_bitstring(j, e->t, e->err.delta, seed, static_cast<u32>(idx));
+    *j_out = j;
+    if (js_out) *js_out = sampled;
+    return SHS_OK;
+}
+
+int engine_run_host(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
+                    shs_stage_trace* trace) {
+    NvtxRange nvtx("shs run (host-driven)");
     state_init(e);
     u128 observed = 0, sampled = 0;
     for (uint32_t s = 0; s < e->t; ++s) {
@@ -475,6 +634,12 @@ int engine_run(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
     *j_out = j;
     if (js_out) *js_out = sampled;
     return SHS_OK;
+}
+
+int engine_run(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
+               shs_stage_trace* trace) {
+    return e->host_measure ? engine_run_host(e, seed, idx, j_out, js_out, trace)
+                           : engine_run_device(e, seed, idx, j_out, js_out, trace);
 }
 
 bool batchable(const shs_engine* e) { return e->N <= kBatchMaxN && e->t <= kBatchMaxT; }
@@ -711,6 +876,10 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<collapse>)");
     }
     e->fixup_cap = 2 * e->num_sms;
+    {
+        const char* hm = std::getenv("SHS_HOST_MEASURE");
+        e->host_measure = hm && hm[0] == '1';
+    }
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");
     const size_t part_bytes = sizeof(unsigned long long) * 2 * kDigits *

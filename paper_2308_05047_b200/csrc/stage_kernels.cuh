@@ -19,6 +19,7 @@
 #pragma once
 
 #include "device_math.cuh"
+#include "measure.cuh"
 
 namespace shs {
 
@@ -44,6 +45,7 @@ struct StageParams {
     // residue-major reads are bank-conflict free), 1/A and 1/W for small divisions
     uint32_t A, W;
     float invA, invW;
+    const DevStage* dev;  // device-resident run: sc / sel from this slot instead
 };
 
 // floor(d / D) for d < 2^20, D <= 2^11, from a float reciprocal and one correction
@@ -146,6 +148,7 @@ __device__ __forceinline__ void write_cta_digits(unsigned long long (*digits)[kD
 template <int kMode, bool kE1>
 __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
     extern __shared__ double2 streams_buf[];      // kSrcStreams: [A][W]
+    const StageScalars sc = p.dev ? p.dev->sc : p.sc;
     __shared__ double nrm[2 * kPer][kBlock + 1];  // +1: conflict-free column walks
     __shared__ unsigned long long digits[2][kDigits];
     const int tid = threadIdx.x;
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             double h0r, h0i, h1r, h1i;
-            stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
             const bool live = zg + uint64_t(e) * kBlock < p.zend;
             nrm[e][tid] = live ? cnorm(h0r, h0i) : 0.0;
             nrm[kPer + e][tid] = live ? cnorm(h1r, h1i) : 0.0;
@@ -250,6 +253,80 @@ static __global__ void __launch_bounds__(kFinalizeThreads) k_finalize(const unsi
     if (threadIdx.x < 2) out[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
 }
 
+// Stage s of a device-resident run (engine.cu engine_run_device): p0/p1 as
+// k_finalize, then the measurement on the device (measure.cuh), the collapse
+// group into slot s & 1 and the next stage's scalars into slot (s + 1) & 1 —
+// its phase picked from the host's two candidates by the observed bit, its inv
+// = 1/sqrt(p_src) correctly rounded like the host's 1.0 / std::sqrt
+// (statevector.cpp:391). A failed stage (norm drift, degenerate branch) zeroes
+// the next inv so the stages the host already queued fold zeros until it
+// reads the status one stage later and stops.
+struct MeasureStep {
+    MeasureCfg cfg;
+    uint32_t s;
+    int collapse;        // s + 1 < t
+    int init_cur;        // stage 0: slot s & 1 takes sc0 (its probs pass used kernel args)
+    StageScalars sc0;
+    DevStage* cur;       // slot s & 1
+    DevStage* next;      // slot (s + 1) & 1
+    NextPhase nph;
+    StageRec* rec;       // [t], host-mapped
+};
+
+static __global__ void __launch_bounds__(kFinalizeThreads)
+    k_finalize_measure(const unsigned long long* __restrict__ partials, int nparts,
+                       const double* __restrict__ S, uint64_t nb, int kahan, MeasureStep ms) {
+    __shared__ unsigned long long acc[2][kDigits];
+    __shared__ double pp[2];
+    if (kahan) {
+        if (threadIdx.x == 0) {
+            double s0 = 0, c0 = 0, s1 = 0, c1 = 0;
+            for (uint64_t b = 0; b < nb; ++b) {
+                const double x0 = S[b], x1 = S[nb + b];
+                if (x0 != 0.0) {
+                    double y = __dsub_rn(x0, c0);
+                    double t = __dadd_rn(s0, y);
+                    c0 = __dsub_rn(__dsub_rn(t, s0), y);
+                    s0 = t;
+                }
+                if (x1 != 0.0) {
+                    double y = __dsub_rn(x1, c1);
+                    double t = __dadd_rn(s1, y);
+                    c1 = __dsub_rn(__dsub_rn(t, s1), y);
+                    s1 = t;
+                }
+            }
+            pp[0] = s0;
+            pp[1] = s1;
+        }
+    } else {
+        sum_slots(partials, nparts, acc);
+        if (threadIdx.x < 2) pp[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const double p0 = pp[0], p1 = pp[1];
+    const DevMeasure mr = measure_dev(p0, p1, ms.cfg, ms.s, ms.collapse != 0);
+    StageScalars n = ms.init_cur ? ms.sc0 : ms.cur->sc;
+    if (ms.init_cur) ms.cur->sc = ms.sc0;
+    ms.cur->sel = mr.src_group;
+    n.phr = ms.nph.phr[mr.obit];
+    n.phi = ms.nph.phi[mr.obit];
+    n.phase_mul = ms.nph.phase_mul[mr.obit];
+    n.inv = mr.status ? 0.0 : __ddiv_rn(1.0, __dsqrt_rn(mr.p_src));
+    ms.next->sc = n;
+    StageRec r;
+    r.p0 = p0;
+    r.p1 = p1;
+    r.sbit = mr.sbit;
+    r.obit = mr.obit;
+    r.flip = mr.flip;
+    r.ebranch = mr.ebranch;
+    r.status = mr.status;
+    r.done = 1;
+    ms.rec[ms.s] = r;
+}
+
 // The exact digits of this engine's (or shard's) partial masses: sum of the
 // per-CTA digit slots, carry-normalised to 32-bit digits (for an allreduce).
 static __global__ void __launch_bounds__(kFinalizeThreads) k_sum_partials(const unsigned long long* __restrict__ partials, int nparts,
@@ -269,6 +346,8 @@ static __global__ void __launch_bounds__(kFinalizeThreads) k_sum_partials(const 
 template <int kMode, bool kE1>
 __global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
     extern __shared__ double2 streams_buf[];  // kSrcStreams: [A][W]
+    const StageScalars sc = p.dev ? p.dev->sc : p.sc;
+    const int sel = p.dev ? p.dev->sel : p.sel;
     const int tid = threadIdx.x;
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = p.z0 + c * kChunk + tid;
@@ -287,9 +366,9 @@ __global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
         for (int e = 0; e < kPer; ++e) {
             const uint64_t z = zg + uint64_t(e) * kBlock;
             double h0r, h0i, h1r, h1i;
-            stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
             if (z < p.zend)
-                p.Y[z - p.z0] = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+                p.Y[z - p.z0] = sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
         }
     }
 }

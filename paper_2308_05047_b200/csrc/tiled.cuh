@@ -100,6 +100,7 @@ struct TileParams {
     double* head;       // [H][2][256] head norms of each row (before its first boundary)
     double* tail;       // [H][2]      predecessor's tail partial, indexed by successor row
     int sel;            // collapse: group kept
+    const DevStage* dev;  // device-resident run: sc / sel from this slot instead
 };
 
 __device__ __forceinline__ uint64_t tile_row_len(uint64_t j, const TileParams& p) {
@@ -424,6 +425,8 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
     TileSmem<kProbs>& sm = *reinterpret_cast<TileSmem<kProbs>*>(smem_raw);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    const StageScalars sc = p.dev ? p.dev->sc : p.sc;
+    const int sel = p.dev ? p.dev->sel : p.sel;
 #ifdef SHS_CTA_TRACE
     uint64_t trace_t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
@@ -543,12 +546,12 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                 const uint32_t rlo = kSplit ? st.row_lo[r] : 0u, rn = st.row_n[r];
                 const bool live = pos - rlo < rn;
                 double h0r, h0i, h1r, h1i;
-                stage_pair(p.sc, st.dst[r][c], st.src[c][r], h0r, h0i, h1r, h1i);
+                stage_pair(sc, st.dst[r][c], st.src[c][r], h0r, h0i, h1r, h1i);
                 if (kProbs) {
                     sm.nrm[b][0][r][c] = live ? cnorm(h0r, h0i) : 0.0;
                     sm.nrm[b][1][r][c] = live ? cnorm(h1r, h1i) : 0.0;
                 } else if (kSectorShift) {
-                    const double2 hv = p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+                    const double2 hv = sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
                     const uint64_t rz = st.row_z[r];
                     if ((rz & 1) == 0) {
                         if (live) p.Y[rz + pos] = hv;
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
                     }
                 } else if (live) {
                     p.Y[st.row_z[r] + pos] =
-                        p.sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+                        sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
                 }
             }
             __syncwarp();
