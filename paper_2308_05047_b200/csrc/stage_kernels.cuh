@@ -210,6 +210,7 @@ __device__ __forceinline__ void sum_slots(const unsigned long long* __restrict__
     const int i = threadIdx.x % (2 * kDigits), l = threadIdx.x / (2 * kDigits);
     if (l < kFinalizeSlices) {
         unsigned long long s = 0;
+#pragma unroll 8
         for (int c = l; c < nparts; c += kFinalizeSlices) s += partials[uint64_t(c) * 2 * kDigits + i];
         red[l][i] = s;
     }

@@ -699,40 +699,70 @@ __global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams 
 }
 
 // The block straddling the boundary between a row and its z-order predecessor:
-// S_b = fold(predecessor's tail partial, this row's head norms). One thread per
-// (row, group); the head loads are issued 16 ahead of the (inherently serial)
-// fold, each thread's 16 from the same one or two L1 lines.
+// S_b = fold(predecessor's tail partial, this row's head norms), in z order.
+// A CTA takes kFixItems (row, group) items at a time: all 256 threads stage
+// the items' head runs (<= 2 KB each, coalesced) into shared memory, then one
+// warp folds them — lane i runs item i's serial chain, reading a padded row
+// (conflict-free), so 32 chains advance per instruction instead of one
+// thread walking its run from HBM.
+constexpr int kFixItems = 32;
+constexpr int kFixStride = 257;  // doubles per staged head run (+1: conflict-free lanes)
+constexpr size_t kFixSmem = sizeof(double) * kFixItems * kFixStride;
+
 static __global__ void __launch_bounds__(256) k_tile_fixup(TileParams p, unsigned long long* slots) {
+    extern __shared__ double fix_buf[];  // [kFixItems][kFixStride]
     __shared__ unsigned long long digits[2][kDigits];
+    __shared__ uint32_t item_hl[kFixItems];
+    __shared__ uint64_t item_z[kFixItems];
     const int tid = threadIdx.x;
     for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&digits[0][0])[i] = 0ull;
-    __syncthreads();
-    DigitWindow w0, w1;
-    window_reset(w0);
-    window_reset(w1);
-    for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + tid; idx < 2 * p.H;
-         idx += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t j = idx >> 1;
-        const int g = static_cast<int>(idx & 1);
-        const uint64_t z = mulmod_shoup(j, p.A, p.A_sh, p.N);
-        const uint32_t hl = static_cast<uint32_t>((256 - (z & 255)) & 255);
-        if (hl == 0) continue;
-        double s = p.tail[j * 2 + g];
-        const double* head = p.head + (j * 2 + g) * 256;
-        uint32_t q = 0;
-        for (; q + 16 <= hl; q += 16) {
-            double v[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) v[u] = head[q + u];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) s = __dadd_rn(s, v[u]);
+    DigitWindow win;
+    window_reset(win);
+    const uint64_t items = 2 * p.H;
+    for (uint64_t base = uint64_t(blockIdx.x) * kFixItems; base < items;
+         base += uint64_t(gridDim.x) * kFixItems) {
+        __syncthreads();  // the previous group's staged runs are folded
+        if (tid < kFixItems) {
+            const uint64_t idx = base + tid;
+            uint32_t hl = 0;
+            uint64_t z = 0;
+            if (idx < items) {
+                z = mulmod_shoup(idx >> 1, p.A, p.A_sh, p.N);
+                hl = static_cast<uint32_t>((256 - (z & 255)) & 255);
+            }
+            item_hl[tid] = hl;
+            item_z[tid] = z;
         }
-        for (; q < hl; ++q) s = __dadd_rn(s, head[q]);
-        p.S[g * p.nb + (z >> 8)] = s;
-        window_add(g ? w1 : w0, s, digits[g]);
+        __syncthreads();
+#pragma unroll 8
+        for (int i = 0; i < kFixItems; ++i) {
+            const uint32_t hl = item_hl[i];
+            if (static_cast<uint32_t>(tid) < hl)
+                fix_buf[i * kFixStride + tid] = p.head[(base + i) * 256 + tid];
+        }
+        __syncthreads();
+        if (tid < kFixItems) {
+            const uint32_t hl = item_hl[tid];
+            const uint64_t idx = base + tid;
+            if (hl) {
+                const int g = static_cast<int>(idx & 1);
+                double s = p.tail[idx];  // tail[j * 2 + g]
+                const double* row = fix_buf + tid * kFixStride;
+                uint32_t q = 0;
+                for (; q + 8 <= hl; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = row[q + u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+                }
+                for (; q < hl; ++q) s = __dadd_rn(s, row[q]);
+                p.S[g * p.nb + (item_z[tid] >> 8)] = s;
+                window_add(win, s, digits[g]);  // g = tid & 1: base is even
+            }
+        }
     }
-    window_flush(w0, digits[0]);
-    window_flush(w1, digits[1]);
+    if (tid < kFixItems) window_flush(win, digits[tid & 1]);
     __syncthreads();
     write_partials(digits, slots + uint64_t(blockIdx.x) * 2 * kDigits, tid);
 }
