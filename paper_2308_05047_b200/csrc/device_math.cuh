@@ -56,11 +56,27 @@ struct StageScalars {
     int phase_mul;              // gather || phi != 0 (statevector.cpp:345 / 349)
 };
 
+// A copy of shared-memory stage scalars that the compiler cannot hoist out of a loop.
+__device__ __forceinline__ StageScalars load_scalars(const StageScalars& s) {
+    const volatile StageScalars& v = s;
+    StageScalars r;
+    r.w0r = v.w0r;
+    r.w0i = v.w0i;
+    r.w1r = v.w1r;
+    r.w1i = v.w1i;
+    r.phr = v.phr;
+    r.phi = v.phi;
+    r.inv = v.inv;
+    r.phase_mul = v.phase_mul;
+    return r;
+}
+
 // Post-Hadamard pair of one amplitude index:
 //   u  = w0 * (x * inv)                 g0[z] after reset   (statevector.cpp:396-397)
 //   v  = (w1 * (xs * inv)) [* ph]       g1[src z] * ph      (statevector.cpp:345 / 360)
 //   h0 = (u + v) * k, h1 = (u - v) * k                      (statevector.cpp:361-362)
-__device__ __forceinline__ void stage_pair(const StageScalars& sc, double2 x, double2 xs,
+template <class SC>
+__device__ __forceinline__ void stage_pair(const SC& sc, double2 x, double2 xs,
                                            double& h0r, double& h0i, double& h1r,
                                            double& h1i) {
     double xr = __dmul_rn(x.x, sc.inv), xi = __dmul_rn(x.y, sc.inv);

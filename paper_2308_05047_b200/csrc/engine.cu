@@ -249,20 +249,35 @@ int grid_for(const shs_engine* e) {
     return static_cast<int>(std::min<uint64_t>(e->nchunks, static_cast<uint64_t>(e->grid_cap)));
 }
 
-template <bool G, bool E1>
-void launch_probs(shs_engine* e, const StageParams& p) {
+template <bool G, bool E1, bool D>
+void launch_probs_v(shs_engine* e, const StageParams& p) {
     if (G && p.A >= kStreamsProbsMinA)
-        k_stage_probs<kSrcStreams, E1><<<grid_for(e), kThreads, streams_smem(p), e->stream>>>(p);
+        k_stage_probs<kSrcStreams, E1, D><<<grid_for(e), kThreads, streams_smem(p), e->stream>>>(p);
     else
-        k_stage_probs<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
+        k_stage_probs<G ? kSrcGather : kSrcDirect, E1, D><<<grid_for(e), kThreads, 0, e->stream>>>(p);
 }
 
+// stage 0 (E1) always runs on host scalars (inv = 1, phi = 0)
+template <bool G, bool E1>
+void launch_probs(shs_engine* e, const StageParams& p) {
+    if (!E1 && p.dev) launch_probs_v<G, false, true>(e, p);
+    else launch_probs_v<G, E1, false>(e, p);
+}
+
+template <bool G, bool E1, bool D>
+void launch_collapse_v(shs_engine* e, const StageParams& p) {
+    if (G && p.A)
+        k_stage_collapse<kSrcStreams, E1, D><<<grid_for(e), kThreads, streams_smem(p), e->stream>>>(p);
+    else
+        k_stage_collapse<G ? kSrcGather : kSrcDirect, E1, D><<<grid_for(e), kThreads, 0, e->stream>>>(p);
+}
+
+// stage 0's collapse (E1) reads the slot too in a device-resident run (its group
+// is measured on the device)
 template <bool G, bool E1>
 void launch_collapse(shs_engine* e, const StageParams& p) {
-    if (G && p.A)
-        k_stage_collapse<kSrcStreams, E1><<<grid_for(e), kThreads, streams_smem(p), e->stream>>>(p);
-    else
-        k_stage_collapse<G ? kSrcGather : kSrcDirect, E1><<<grid_for(e), kThreads, 0, e->stream>>>(p);
+    if (p.dev) launch_collapse_v<G, E1, true>(e, p);
+    else launch_collapse_v<G, E1, false>(e, p);
 }
 
 void release(shs_engine* e) {
@@ -854,13 +869,15 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         if (pl.tiled) e->max_rows = std::max(e->max_rows, pl.H);
     }
     int occ = 0;
-    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcGather, false>, kThreads, 0);
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcGather, false, false>, kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     e->grid_cap = std::max(1, occ) * e->num_sms;
     // one persistent TMA-pipelined CTA per SM for the tiled passes
     // kSrcStreams: up to kStreamsMaxA * 5 staged amplitudes (80 KB) of dynamic smem
-    for (auto fn : {k_stage_probs<kSrcStreams, false>, k_stage_probs<kSrcStreams, true>,
-                    k_stage_collapse<kSrcStreams, false>, k_stage_collapse<kSrcStreams, true>}) {
+    for (auto fn : {k_stage_probs<kSrcStreams, false, false>, k_stage_probs<kSrcStreams, true, false>,
+                    k_stage_probs<kSrcStreams, false, true>,
+                    k_stage_collapse<kSrcStreams, false, false>, k_stage_collapse<kSrcStreams, true, false>,
+                    k_stage_collapse<kSrcStreams, false, true>, k_stage_collapse<kSrcStreams, true, true>}) {
         ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(double2) * kStreamsMaxA * 5));
         if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(streams)");

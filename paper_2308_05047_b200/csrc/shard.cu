@@ -244,7 +244,7 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
     }
     sh->num_sms = prop.multiProcessorCount;
     int occ = 0;
-    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcBuffer, false>,
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage_probs<kSrcBuffer, false, false>,
                                                        kThreads, 0);
     if (ce != cudaSuccess) return fail(ce, "occupancy");
     sh->grid_cap = std::max(1, occ) * sh->num_sms;
@@ -408,12 +408,12 @@ int shs_shard_probs(shs_shard* sh, uint32_t s, uint64_t lo, uint64_t hi,
         const int g = grid(sh);
         int rc = shard_launch(sh, 0, [&] {
             if (sh->e1) {
-                if (gather) k_stage_probs<kSrcGather, true><<<g, kThreads, 0, sh->stream>>>(p);
-                else k_stage_probs<kSrcDirect, true><<<g, kThreads, 0, sh->stream>>>(p);
+                if (gather) k_stage_probs<kSrcGather, true, false><<<g, kThreads, 0, sh->stream>>>(p);
+                else k_stage_probs<kSrcDirect, true, false><<<g, kThreads, 0, sh->stream>>>(p);
             } else if (ex) {
-                k_stage_probs<kSrcBuffer, false><<<g, kThreads, 0, sh->stream>>>(p);
+                k_stage_probs<kSrcBuffer, false, false><<<g, kThreads, 0, sh->stream>>>(p);
             } else {
-                k_stage_probs<kSrcDirect, false><<<g, kThreads, 0, sh->stream>>>(p);
+                k_stage_probs<kSrcDirect, false, false><<<g, kThreads, 0, sh->stream>>>(p);
             }
             k_sum_partials<<<1, kFinalizeThreads, 0, sh->stream>>>(sh->partials, g, sh->d_digits);
         });
@@ -443,12 +443,12 @@ int shs_shard_collapse(shs_shard* sh, int32_t src_group, double p_src) {
         const int g = grid(sh);
         int rc = shard_launch(sh, 2, [&] {
             if (sh->e1) {
-                if (gather) k_stage_collapse<kSrcGather, true><<<g, kThreads, 0, sh->stream>>>(p);
-                else k_stage_collapse<kSrcDirect, true><<<g, kThreads, 0, sh->stream>>>(p);
+                if (gather) k_stage_collapse<kSrcGather, true, false><<<g, kThreads, 0, sh->stream>>>(p);
+                else k_stage_collapse<kSrcDirect, true, false><<<g, kThreads, 0, sh->stream>>>(p);
             } else if (ex) {  // in place over P
-                k_stage_collapse<kSrcBuffer, false><<<g, kThreads, 0, sh->stream>>>(p);
+                k_stage_collapse<kSrcBuffer, false, false><<<g, kThreads, 0, sh->stream>>>(p);
             } else {
-                k_stage_collapse<kSrcDirect, false><<<g, kThreads, 0, sh->stream>>>(p);
+                k_stage_collapse<kSrcDirect, false, false><<<g, kThreads, 0, sh->stream>>>(p);
             }
         });
         if (rc) return rc;

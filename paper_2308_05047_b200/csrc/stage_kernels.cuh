@@ -145,14 +145,21 @@ __device__ __forceinline__ void write_cta_digits(unsigned long long (*digits)[kD
     }
 }
 
-template <int kMode, bool kE1>
+// kDev: the stage scalars come from p.dev (device-resident runs), staged in
+// shared memory and read at every use (volatile); otherwise they are the kernel
+// arguments p.sc, read as constant-bank operands. (Holding device-loaded
+// scalars in registers makes ptxas give up the batching of the 2 kPer loads
+// for occupancy: +25% on the gather stages.)
+template <int kMode, bool kE1, bool kDev>
 __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
     extern __shared__ double2 streams_buf[];      // kSrcStreams: [A][W]
-    const StageScalars sc = p.dev ? p.dev->sc : p.sc;
     __shared__ double nrm[2 * kPer][kBlock + 1];  // +1: conflict-free column walks
     __shared__ unsigned long long digits[2][kDigits];
+    __shared__ StageScalars s_sc;
     const int tid = threadIdx.x;
     for (int i = tid; i < 2 * kDigits; i += kThreads) (&digits[0][0])[i] = 0ull;
+    if (kDev && tid == 0) s_sc = p.dev->sc;
+    const volatile StageScalars& dsc = s_sc;
     DigitWindow win;
     window_reset(win);
     __syncthreads();
@@ -171,7 +178,8 @@ __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             double h0r, h0i, h1r, h1i;
-            stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            if (kDev) stage_pair(dsc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            else stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
             const bool live = zg + uint64_t(e) * kBlock < p.zend;
             nrm[e][tid] = live ? cnorm(h0r, h0i) : 0.0;
             nrm[kPer + e][tid] = live ? cnorm(h1r, h1i) : 0.0;
@@ -344,12 +352,19 @@ static __global__ void __launch_bounds__(kFinalizeThreads) k_sum_partials(const 
     }
 }
 
-template <int kMode, bool kE1>
+template <int kMode, bool kE1, bool kDev>
 __global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
     extern __shared__ double2 streams_buf[];  // kSrcStreams: [A][W]
-    const StageScalars sc = p.dev ? p.dev->sc : p.sc;
-    const int sel = p.dev ? p.dev->sel : p.sel;
+    __shared__ StageScalars s_sc;             // kDev: as k_stage_probs
+    __shared__ int s_sel;
     const int tid = threadIdx.x;
+    if (kDev && tid == 0) {
+        s_sc = p.dev->sc;
+        s_sel = p.dev->sel;
+    }
+    if (kDev) __syncthreads();
+    const volatile StageScalars& dsc = s_sc;
+    const int sel = kDev ? s_sel : p.sel;
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = p.z0 + c * kChunk + tid;
         double2 xa[kPer], xs[kPer];
@@ -367,7 +382,9 @@ __global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
         for (int e = 0; e < kPer; ++e) {
             const uint64_t z = zg + uint64_t(e) * kBlock;
             double h0r, h0i, h1r, h1i;
-            stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            // stage 0 (kE1): the scalars are the host's even in a device-resident run
+            if (kDev && !kE1) stage_pair(dsc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+            else stage_pair(p.sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
             if (z < p.zend)
                 p.Y[z - p.z0] = sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
         }
