@@ -383,9 +383,49 @@ def small_n_throughput(shs):
             sec = re.time_runs(2, 0, k)
             entry["reference_cpu_runs_per_s_1core"] = k / sec
             entry["reference_sample"] = f"{k} IterativeShorEngine::run calls of N={N}, a={a}, 1 thread"
+        if name == "config2_N21_N35":
+            entry["statistics"] = config2_statistics(shs, engines, problems, ref)
         out[name] = entry
         for e in engines:
             e.close()
+    return out
+
+
+def config2_statistics(shs, engines, problems, ref):
+    """Config 2's success-probability statistics: run_problem (harness.cpp:109-148)
+    for every coprime base of N = 21 and 35, M = 1024 shots each — runs on the
+    batched engine, Shor post-processing on the device (§8 f4), tallies on the
+    host — with the mean success / success+lucky fractions per N, beside the
+    reference's run_problem for the same problems on one host core."""
+    factors = {21: (3, 7), 35: (5, 7)}
+    M = 1024
+    probs = [shs.FactoringProblem.make(N, a, p=factors[N][0], q=factors[N][1], seed=1000 + i)
+             for i, (N, a) in enumerate(problems)]
+    for p, e in zip(probs, engines):
+        shs.run_problem(p, M, engine=e)  # warm
+    t0 = time.perf_counter()
+    results = [shs.run_problem(p, M, engine=e) for p, e in zip(probs, engines)]
+    dt = time.perf_counter() - t0
+    out = {"M": M, "problems": len(probs), "seconds": dt,
+           "shots_per_s": len(probs) * M / dt}
+    for N in (21, 35):
+        rs = [r for r in results if r.problem.N == N]
+        out[f"N{N}"] = {"bases": len(rs),
+                        "mean_success": statistics.mean(r.success_fraction() for r in rs),
+                        "mean_success_lucky": statistics.mean(r.success_lucky_fraction()
+                                                              for r in rs)}
+    import numpy as np
+    j = np.zeros((1 << 20, 2), dtype=np.uint64)
+    j[:, 0] = np.arange(1 << 20, dtype=np.uint64) * np.uint64(2654435761) % np.uint64(1 << 22)
+    shs.shor_postprocess_array(j[:1024], 22, 4087, 1001)  # warm
+    t0 = time.perf_counter()
+    shs.shor_postprocess_array(j, 22, 4087, 1001)
+    out["postprocess_bitstrings_per_s"] = len(j) / (time.perf_counter() - t0)
+    if ref is not None:
+        p = probs[-1]
+        t0 = time.perf_counter()
+        ref.run_problem(p.N, p.a, p.p, p.q, p.L, p.t, p.seed, M)
+        out["reference_run_problem_shots_per_s_1core"] = M / (time.perf_counter() - t0)
     return out
 
 

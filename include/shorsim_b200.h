@@ -254,6 +254,26 @@ void* shs_shard_stream(const shs_shard* shard);
 int shs_exhaustive_distribution(const shs_problem* problem, const shs_error* error,
                                 uint64_t node_budget, int32_t device, double* out);
 
+/* ---- Shor standard post-processing on the device (proj/src/postprocess.cpp:55-89) ----
+ * shor_standard_procedure(j, t, N, a, known_order) for a batch of bit strings
+ * (u128 j as {lo, hi} pairs), one device thread each. classification follows
+ * shorsim::Classification (postprocess.hpp:12); order_match: 0/1, or 2 when no
+ * known order is given (std::nullopt). Errors as the reference: t >= 128 or
+ * j >= 2^t -> SHS_INVALID_ARGUMENT (numtheory.cpp:237-239). */
+enum { SHS_CLASS_SUCCESS = 0, SHS_CLASS_LUCKY_NE = 1, SHS_CLASS_LUCKY_NO = 2,
+       SHS_CLASS_LUCKY_OO = 3, SHS_CLASS_FAIL = 4 };
+typedef struct {
+    int32_t classification;
+    uint8_t r_even, a_r_is_one, a_half_not_minus_one, order_match;
+    uint64_t k[2], r[2];        /* the convergent k / r used (u128 as {lo, hi}) */
+    uint32_t n_factors;         /* nontrivial divisors found, ascending */
+    uint32_t pad;
+    uint64_t factors[4];
+} shs_shor_outcome;
+int shs_shor_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t N, uint64_t a,
+                         uint64_t known_order, int32_t has_known_order, int32_t device,
+                         shs_shor_outcome* out);
+
 /* thread-local message of the last failing call */
 const char* shs_last_error(void);
 /* library build string (arch, flags) */

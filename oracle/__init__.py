@@ -284,6 +284,12 @@ class Reference:
                                              C.c_int, C.POINTER(i32)]
         L.ref_exhaustive.argtypes = [u64, u64, C.c_uint, C.c_uint, C.c_int, dbl, dbl, dbl, dbl,
                                      C.c_int, C.POINTER(dbl)]
+        L.ref_shor_standard_procedure.argtypes = [u64, u64, C.c_uint, u64, u64, u64, C.c_int,
+                                                  C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)]
+        L.ref_multiplicative_order.argtypes = [u64, u64, u64, u64, C.POINTER(u64)]
+        L.ref_run_problem.argtypes = [u64, u64, u64, u64, C.c_uint, C.c_uint, u64, C.c_uint,
+                                      C.c_int, dbl, dbl, dbl, dbl, C.c_int, C.c_uint,
+                                      C.POINTER(u64), C.POINTER(u64), C.c_uint]
 
     def philox(self, key, ctr):
         out = (u32 * 4)()
@@ -321,6 +327,40 @@ class Reference:
 
     def state(self, n, err=None, shards=4):
         return RefState(self, n, err or make_error(), shards)
+
+    def shor_standard_procedure(self, j, t, N, a, known_order=None):
+        """proj/src/postprocess.cpp:55-89, fields as shs_shor_outcome."""
+        ints, kr, f = (i32 * 6)(), (u64 * 4)(), (u64 * 4)()
+        _check(self.lib.ref_shor_standard_procedure(
+            j & (2**64 - 1), j >> 64, t, N, a, known_order or 0, 0 if known_order is None else 1,
+            ints, kr, f), self.lib)
+        return {"classification": ints[0], "r_even": ints[1], "a_r_is_one": ints[2],
+                "a_half_not_minus_one": ints[3], "order_match": ints[4],
+                "k": kr[0] | (kr[1] << 64), "r": kr[2] | (kr[3] << 64),
+                "factors": list(f[:ints[5]])}
+
+    def multiplicative_order(self, a, N, p=0, q=0):
+        out = u64()
+        _check(self.lib.ref_multiplicative_order(a, N, p, q, C.byref(out)), self.lib)
+        return out.value
+
+    def run_problem(self, N, a, p, q, L, t, seed, M, err=None, qubit_ceiling=26):
+        """run_problem (proj/src/harness.cpp:109-148) on the reference engine."""
+        err = err or make_error()
+        counts, cap = (u64 * 13)(), 256
+        recip = (u64 * (2 * cap))()
+        _check(self.lib.ref_run_problem(N, a, p, q, L, t, seed, M, err.kind, err.delta, err.px,
+                                        err.py, err.pz, err.has_pauli, qubit_ceiling, counts,
+                                        recip, cap), self.lib)
+        keys = ["order", "success", "lucky_ne", "lucky_no", "lucky_oo", "fail",
+                "first_factor_index", "first_order_index", "r_overflow", "r_other",
+                "r_total_lucky", "order_solvable"]
+        out = {k: counts[i] for i, k in enumerate(keys)}
+        for k in ("first_factor_index", "first_order_index"):
+            out[k] = out[k] or None
+        out["order_solvable"] = bool(out["order_solvable"])
+        out["r_reciprocal"] = {recip[2 * i]: recip[2 * i + 1] for i in range(min(counts[12], cap))}
+        return out
 
 
 class RefEngine:

@@ -9,6 +9,9 @@
 //   build_permutation_plan      proj/src/statevector.cpp:133-154
 //   exhaustive_joint_distribution proj/src/statevector.cpp:533-579
 //   philox::block               proj/include/shorsim/rng.hpp:16-31
+//   shor_standard_procedure     proj/src/postprocess.cpp:55-89
+//   run_problem                 proj/src/harness.cpp:109-148
+//   multiplicative_order        proj/src/numtheory.cpp:207-234
 // Nothing here re-implements reference logic; it only marshals arguments.
 #include <chrono>
 #include <cstdint>
@@ -16,7 +19,9 @@
 #include <exception>
 #include <string>
 
+#include "shorsim/harness.hpp"
 #include "shorsim/noise.hpp"
+#include "shorsim/postprocess.hpp"
 #include "shorsim/numtheory.hpp"
 #include "shorsim/problems.hpp"
 #include "shorsim/statevector.hpp"
@@ -273,6 +278,80 @@ int ref_exhaustive(uint64_t N, uint64_t a, unsigned L, unsigned t, int kind, dou
         auto d = exhaustive_joint_distribution(make_problem(N, a, L, t),
                                                make_error(kind, delta, px, py, pz, has_pauli));
         std::memcpy(out, d.data(), d.size() * sizeof(double));
+    });
+}
+
+// shor_standard_procedure: ints = {classification, r_even, a_r_is_one,
+// a_half_not_minus_one, order_match (0/1, 2 = none), n_factors}; kr = {k_lo,
+// k_hi, r_lo, r_hi}; factors[4].
+int ref_shor_standard_procedure(uint64_t j_lo, uint64_t j_hi, unsigned t, uint64_t N, uint64_t a,
+                                uint64_t known_order, int has_order, int32_t ints[6],
+                                uint64_t kr[4], uint64_t factors[4]) {
+    return guarded([&] {
+        u128 j = (u128{j_hi} << 64) | j_lo;
+        std::optional<u64> ko;
+        if (has_order) ko = known_order;
+        PostProcessOutcome o = shor_standard_procedure(j, t, N, a, ko);
+        ints[0] = static_cast<int32_t>(o.classification);
+        ints[1] = o.checks.r_even;
+        ints[2] = o.checks.a_r_is_one;
+        ints[3] = o.checks.a_half_not_minus_one;
+        ints[4] = o.order_match ? (*o.order_match ? 1 : 0) : 2;
+        ints[5] = static_cast<int32_t>(o.factors.size());
+        kr[0] = static_cast<uint64_t>(o.convergent.k);
+        kr[1] = static_cast<uint64_t>(o.convergent.k >> 64);
+        kr[2] = static_cast<uint64_t>(o.convergent.r);
+        kr[3] = static_cast<uint64_t>(o.convergent.r >> 64);
+        for (size_t i = 0; i < 4; ++i) factors[i] = i < o.factors.size() ? o.factors[i] : 0;
+    });
+}
+
+int ref_multiplicative_order(uint64_t a, uint64_t N, uint64_t p, uint64_t q, uint64_t* out) {
+    return guarded([&] {
+        std::optional<std::pair<u64, u64>> kf;
+        if (p && q) kf = std::make_pair(p, q);
+        *out = multiplicative_order(a, N, kf).value;
+    });
+}
+
+// run_problem (simulator backend, Shor post-processing) on the reference engine:
+// counts = {order, success, lucky_ne, lucky_no, lucky_oo, fail, first_factor_index
+// (0 = none), first_order_index (0 = none), r_overflow, r_other, r_total_lucky,
+// order_solvable, n_reciprocal}; recip = {D, count} pairs (up to cap).
+int ref_run_problem(uint64_t N, uint64_t a, uint64_t p, uint64_t q, unsigned L, unsigned t,
+                    uint64_t seed, unsigned M, int kind, double delta, double px, double py,
+                    double pz, int has_pauli, unsigned qubit_ceiling, uint64_t counts[13],
+                    uint64_t* recip, unsigned cap) {
+    return guarded([&] {
+        FactoringProblem prob = make_problem(N, a, L, t);
+        prob.p = p;
+        prob.q = q;
+        prob.seed = seed;
+        CampaignSpec spec;
+        spec.M = M;
+        spec.error = make_error(kind, delta, px, py, pz, has_pauli);
+        spec.sim.qubit_ceiling = qubit_ceiling;
+        ProblemResult r = run_problem(prob, spec);
+        counts[0] = r.order;
+        counts[1] = r.success;
+        counts[2] = r.lucky_ne;
+        counts[3] = r.lucky_no;
+        counts[4] = r.lucky_oo;
+        counts[5] = r.fail;
+        counts[6] = r.first_factor_index ? *r.first_factor_index : 0;
+        counts[7] = r.first_order_index ? *r.first_order_index : 0;
+        counts[8] = r.r_ratio.overflow;
+        counts[9] = r.r_ratio.other;
+        counts[10] = r.r_ratio.total_lucky;
+        counts[11] = r.order_solvable ? 1 : 0;
+        counts[12] = r.r_ratio.reciprocal.size();
+        unsigned i = 0;
+        for (const auto& [D, c] : r.r_ratio.reciprocal) {
+            if (i >= cap) break;
+            recip[2 * i] = D;
+            recip[2 * i + 1] = c;
+            ++i;
+        }
     });
 }
 

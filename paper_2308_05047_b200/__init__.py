@@ -30,4 +30,13 @@ from .engine import (  # noqa: F401
     run_iterative_shor,
     sample_measurement,
 )
+from .postprocess import (  # noqa: F401
+    Classification,
+    PostProcessOutcome,
+    ProblemResult,
+    multiplicative_order,
+    run_problem,
+    shor_postprocess_array,
+    shor_standard_procedure,
+)
 from .sharded import DistGroup, LocalGroup, Shard, ShardedShorEngine, digits_to_probs  # noqa: F401

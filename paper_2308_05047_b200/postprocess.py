@@ -1,0 +1,242 @@
+"""Shor post-processing and the per-problem statistics (§8 f4), the step right
+after the path.
+
+* ``shor_postprocess_array`` — shor_standard_procedure
+  (/root/reference/proj/src/postprocess.cpp:55-89) for a whole batch of bit
+  strings on the device (``shs_shor_postprocess``, csrc/postprocess.cu).
+* ``shor_standard_procedure`` — the same for one bit string, returning the
+  reference's ``PostProcessOutcome`` fields.
+* ``multiplicative_order`` — ground-truth order from the known factors
+  (numtheory.cpp:207-234), host integer code.
+* ``run_problem`` — ``run_problem`` (proj/src/harness.cpp:109-148, simulator
+  backend, Shor mode): M shots through the engine (whole runs on the device
+  for small problems), post-processed on the device, tallied like
+  ``note_outcome`` (harness.cpp:82-104).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import _lib as L
+from .engine import (ErrorConfig, FactoringProblem, IterativeShorEngine, SimulatorOptions,
+                     _raise)
+
+
+class Classification(enum.IntEnum):  # postprocess.hpp:12
+    success = 0
+    lucky_ne = 1
+    lucky_no = 2
+    lucky_oo = 3
+    fail = 4
+
+
+class shs_shor_outcome(C.Structure):
+    _fields_ = [("classification", C.c_int32), ("r_even", C.c_uint8), ("a_r_is_one", C.c_uint8),
+                ("a_half_not_minus_one", C.c_uint8), ("order_match", C.c_uint8),
+                ("k", C.c_uint64 * 2), ("r", C.c_uint64 * 2), ("n_factors", C.c_uint32),
+                ("pad", C.c_uint32), ("factors", C.c_uint64 * 4)]
+
+
+OUTCOME_DTYPE = np.dtype([("classification", np.int32), ("r_even", np.uint8),
+                          ("a_r_is_one", np.uint8), ("a_half_not_minus_one", np.uint8),
+                          ("order_match", np.uint8), ("k", np.uint64, 2), ("r", np.uint64, 2),
+                          ("n_factors", np.uint32), ("pad", np.uint32), ("factors", np.uint64, 4)])
+assert OUTCOME_DTYPE.itemsize == C.sizeof(shs_shor_outcome)
+
+
+@dataclass
+class StandardChecks:
+    r_even: bool = False
+    a_r_is_one: bool = False
+    a_half_not_minus_one: bool = False
+
+    def all(self) -> bool:
+        return self.r_even and self.a_r_is_one and self.a_half_not_minus_one
+
+
+@dataclass
+class PostProcessOutcome:
+    classification: Classification = Classification.fail
+    convergent: Tuple[int, int] = (0, 1)  # (k, r)
+    checks: StandardChecks = field(default_factory=StandardChecks)
+    order_match: Optional[bool] = None
+    factors: List[int] = field(default_factory=list)
+
+
+def shor_postprocess_array(j: np.ndarray, t: int, N: int, a: int,
+                           known_order: Optional[int] = None, device: int = 0) -> np.ndarray:
+    """shor_standard_procedure for every row of j (uint64, shape (count, 2) =
+    (lo, hi) words, as IterativeShorEngine.run_batch_array returns), on the
+    device. Returns a structured array of OUTCOME_DTYPE."""
+    j = np.ascontiguousarray(j, dtype=np.uint64).reshape(-1, 2)
+    out = np.zeros(len(j), dtype=OUTCOME_DTYPE)
+    _raise(L.load().shs_shor_postprocess(j.ctypes.data_as(C.POINTER(C.c_uint64)), len(j), t, N, a,
+                                       known_order or 0, 0 if known_order is None else 1, device,
+                                       out.ctypes.data))
+    return out
+
+
+def outcome_from_record(rec) -> PostProcessOutcome:
+    om = int(rec["order_match"])
+    return PostProcessOutcome(
+        classification=Classification(int(rec["classification"])),
+        convergent=(int(rec["k"][0]) | (int(rec["k"][1]) << 64),
+                    int(rec["r"][0]) | (int(rec["r"][1]) << 64)),
+        checks=StandardChecks(bool(rec["r_even"]), bool(rec["a_r_is_one"]),
+                              bool(rec["a_half_not_minus_one"])),
+        order_match=None if om == 2 else bool(om),
+        factors=[int(x) for x in rec["factors"][:int(rec["n_factors"])]])
+
+
+def shor_standard_procedure(j: int, t: int, N: int, a: int, known_order: Optional[int] = None,
+                            device: int = 0) -> PostProcessOutcome:
+    """postprocess.cpp:55-89 for one bit string (on the device)."""
+    arr = np.array([[j & (2**64 - 1), j >> 64]], dtype=np.uint64)
+    return outcome_from_record(shor_postprocess_array(arr, t, N, a, known_order, device)[0])
+
+
+# ------------------------------------------------------------- ground truth
+def _factorize(n: int) -> Dict[int, int]:
+    """Prime factorisation by trial division (the multiplicative_order helper
+    for lambda = lcm(p-1, q-1); fine for the moduli this engine holds)."""
+    out: Dict[int, int] = {}
+    d = 2
+    while d * d <= n:
+        while n % d == 0:
+            out[d] = out.get(d, 0) + 1
+            n //= d
+        d += 1 if d == 2 else 2
+    if n > 1:
+        out[n] = out.get(n, 0) + 1
+    return out
+
+
+def multiplicative_order(a: int, N: int, known_factors: Optional[Tuple[int, int]] = None) -> int:
+    """Exact order of a mod N (numtheory.cpp:207-234): brute force below 2^20,
+    else among the divisors of lcm(p-1, q-1) from the known factors."""
+    if N < 2:
+        raise ValueError("multiplicative_order: modulus < 2")
+    a %= N
+    if math.gcd(a, N) != 1:
+        raise ValueError("multiplicative_order: gcd(a, N) != 1")
+    if a == 1:
+        return 1
+    if N < (1 << 20) and not known_factors:
+        x, r = a, 1
+        while x != 1:
+            x = x * a % N
+            r += 1
+        return r
+    if not known_factors:
+        raise ValueError("multiplicative_order: large modulus needs known factors")
+    p, q = known_factors
+    if p * q != N:
+        raise ValueError("multiplicative_order: p*q != N")
+    lam = (p - 1) * (q - 1) // math.gcd(p - 1, q - 1)
+    order = lam
+    for prime, e in sorted(_factorize(lam).items()):
+        for _ in range(e):
+            if order % prime == 0 and pow(a, order // prime, N) == 1:
+                order //= prime
+            else:
+                break
+    return order
+
+
+# ---------------------------------------------------------- run_problem
+@dataclass
+class RRatioHistogram:  # harness.hpp:39-44
+    reciprocal: Dict[int, int] = field(default_factory=dict)
+    overflow: int = 0
+    other: int = 0
+    total_lucky: int = 0
+
+
+@dataclass
+class ProblemResult:  # harness.hpp:46-61
+    problem: FactoringProblem
+    order: int = 1
+    M: int = 0
+    success: int = 0
+    lucky_ne: int = 0
+    lucky_no: int = 0
+    lucky_oo: int = 0
+    fail: int = 0
+    first_factor_index: Optional[int] = None
+    first_order_index: Optional[int] = None
+    r_ratio: RRatioHistogram = field(default_factory=RRatioHistogram)
+    order_solvable: bool = False
+
+    def lucky_total(self) -> int:
+        return self.lucky_ne + self.lucky_no + self.lucky_oo
+
+    def success_fraction(self) -> float:
+        return self.success / self.M
+
+    def success_lucky_fraction(self) -> float:
+        return (self.success + self.lucky_total()) / self.M
+
+
+def tally(result: ProblemResult, outcomes: np.ndarray) -> ProblemResult:
+    """note_outcome (harness.cpp:82-104) over a batch, in shot order."""
+    cls = outcomes["classification"]
+    counts = np.bincount(cls, minlength=5)
+    result.success += int(counts[Classification.success])
+    result.lucky_ne += int(counts[Classification.lucky_ne])
+    result.lucky_no += int(counts[Classification.lucky_no])
+    result.lucky_oo += int(counts[Classification.lucky_oo])
+    result.fail += int(counts[Classification.fail])
+    got = np.flatnonzero(outcomes["n_factors"] > 0)
+    if len(got) and result.first_factor_index is None:
+        result.first_factor_index = int(got[0]) + 1
+    r = outcomes["r"][:, 0]  # r < N < 2^64: the low word
+    hit = np.flatnonzero(r == np.uint64(result.order))
+    if len(hit) and result.first_order_index is None:
+        result.first_order_index = int(hit[0]) + 1
+    lucky = (cls == Classification.lucky_ne) | (cls == Classification.lucky_no) | \
+            (cls == Classification.lucky_oo)
+    rl = r[lucky].astype(object)
+    h = result.r_ratio
+    h.total_lucky += len(rl)
+    for rv in rl:
+        rv = int(rv)
+        if rv > result.order:
+            h.overflow += 1
+        elif rv != 0 and result.order % rv == 0:
+            D = result.order // rv
+            h.reciprocal[D] = h.reciprocal.get(D, 0) + 1
+        else:
+            h.other += 1
+    return result
+
+
+def run_problem(problem: FactoringProblem, M: int, error: Optional[ErrorConfig] = None,
+                options: Optional[SimulatorOptions] = None,
+                engine: Optional[IterativeShorEngine] = None) -> ProblemResult:
+    """run_problem (harness.cpp:109-148; simulator backend, Shor mode): shots
+    m = 0 .. M-1 are engine.run(problem.seed, m) — whole runs on the device for
+    small problems — then shor_standard_procedure with the known order on the
+    device, tallied in shot order."""
+    if not problem.p or not problem.q:
+        raise ValueError("campaign problems need known factors for verification labels")
+    res = ProblemResult(problem=problem, M=M)
+    res.order = multiplicative_order(problem.a, problem.N, (problem.p, problem.q))
+    res.order_solvable = res.order % 2 == 0 and \
+        pow(problem.a, res.order // 2, problem.N) != problem.N - 1
+    own = engine is None
+    if own:
+        engine = IterativeShorEngine(problem, error or ErrorConfig(), options or SimulatorOptions())
+    try:
+        j = engine.run_batch_array(problem.seed, 0, M)
+        dev = (options or SimulatorOptions()).device
+        outcomes = shor_postprocess_array(j, problem.t, problem.N, problem.a, res.order, dev)
+    finally:
+        if own:
+            engine.close()
+    return tally(res, outcomes)

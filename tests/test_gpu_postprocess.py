@@ -1,0 +1,95 @@
+"""§8 f4: Shor post-processing on the device against the unmodified reference
+(oracle/_ref: shor_standard_procedure, proj/src/postprocess.cpp:55-89, and
+run_problem, proj/src/harness.cpp:109-148): every outcome field identical
+(integer work: bit-exact is the bar)."""
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def fields(o):
+    return {"classification": int(o.classification), "r_even": int(o.checks.r_even),
+            "a_r_is_one": int(o.checks.a_r_is_one),
+            "a_half_not_minus_one": int(o.checks.a_half_not_minus_one),
+            "order_match": 2 if o.order_match is None else int(o.order_match),
+            "k": o.convergent[0], "r": o.convergent[1], "factors": o.factors}
+
+
+CASES = [(15, 7, 8, (3, 5)), (21, 2, 9, (3, 7)), (35, 3, 11, (5, 7)), (4087, 1001, 24, (61, 67)),
+         (16777207, 2, 48, (4093, 4099)), (4294967213, 5, 64, (57139, 75167)),
+         (34359737977, 3, 70, (117517, 292381)), (8589933181, 3974323683, 100, (89597, 95873))]
+
+
+@pytest.mark.parametrize("N,a,t,pq", CASES)
+def test_standard_procedure_matches_reference(cuda_ok, reference, N, a, t, pq):
+    import paper_2308_05047_b200 as shs
+    from paper_2308_05047_b200.postprocess import outcome_from_record
+    rng = random.Random(N ^ t)
+    order = shs.multiplicative_order(a, N, pq)
+    assert order == reference.multiplicative_order(a, N, *pq)
+    js = [0, 1, 2, (1 << t) - 1, 1 << (t - 1)]
+    # peaks j ~ k 2^t / r (the interesting continued fractions) and random strings
+    js += [(k * (1 << t)) // order + d for k in rng.sample(range(order), min(order, 40))
+           for d in (-1, 0, 1)]
+    js += [rng.getrandbits(t) for _ in range(200)]
+    js = [j for j in js if 0 <= j < (1 << t)]
+    arr = np.array([[j & (2**64 - 1), j >> 64] for j in js], dtype=np.uint64)
+    for ko in (order, None):
+        out = shs.shor_postprocess_array(arr, t, N, a, ko)
+        for j, rec in zip(js, out):
+            assert fields(outcome_from_record(rec)) == \
+                reference.shor_standard_procedure(j, t, N, a, ko), (j, ko)
+
+
+def test_standard_procedure_errors(cuda_ok):
+    import paper_2308_05047_b200 as shs
+    with pytest.raises(ValueError):  # convergents: t must be < 128
+        shs.shor_standard_procedure(1, 128, 15, 7)
+    with pytest.raises(ValueError):  # convergents: j >= 2^t
+        shs.shor_standard_procedure(256, 8, 15, 7)
+    with pytest.raises(ValueError):
+        shs.shor_standard_procedure(1 << 70, 70, 34359737977, 3)
+    assert shs.shor_standard_procedure((1 << 70) - 1, 70, 34359737977, 3).convergent[1] >= 1
+
+
+def _all_bases(N):
+    import math
+    return [a for a in range(2, N) if math.gcd(a, N) == 1]
+
+
+@pytest.mark.parametrize("N,pq", [(21, (3, 7)), (35, (5, 7))])
+def test_run_problem_matches_reference(cuda_ok, reference, N, pq):
+    """Config 2: every coprime base, M shots each, the per-problem statistics
+    equal the reference's run_problem (same engine bit strings, same labels)."""
+    import paper_2308_05047_b200 as shs
+    from oracle import make_error
+    M = 256
+    for i, a in enumerate(_all_bases(N)):
+        prob = shs.FactoringProblem.make(N, a, p=pq[0], q=pq[1], seed=1000 + i)
+        got = shs.run_problem(prob, M)
+        ref = reference.run_problem(N, a, pq[0], pq[1], prob.L, prob.t, prob.seed, M,
+                                    make_error())
+        assert got.order == ref["order"] and got.order_solvable == ref["order_solvable"]
+        assert (got.success, got.lucky_ne, got.lucky_no, got.lucky_oo, got.fail) == \
+            (ref["success"], ref["lucky_ne"], ref["lucky_no"], ref["lucky_oo"], ref["fail"]), a
+        assert got.first_factor_index == ref["first_factor_index"]
+        assert got.first_order_index == ref["first_order_index"]
+        h = got.r_ratio
+        assert (h.overflow, h.other, h.total_lucky) == \
+            (ref["r_overflow"], ref["r_other"], ref["r_total_lucky"])
+        assert h.reciprocal == ref["r_reciprocal"]
+
+
+def test_run_problem_with_error_model(cuda_ok, reference):
+    import paper_2308_05047_b200 as shs
+    from oracle import make_error
+    prob = shs.FactoringProblem.make(35, 2, p=5, q=7, seed=77)
+    err = shs.ErrorConfig(shs.ErrorKind.classical_measure, 0.05)
+    got = shs.run_problem(prob, 512, err)
+    ref = reference.run_problem(35, 2, 5, 7, prob.L, prob.t, 77, 512,
+                                make_error("classical_measure", 0.05))
+    assert (got.success, got.lucky_ne, got.lucky_no, got.lucky_oo, got.fail) == \
+        (ref["success"], ref["lucky_ne"], ref["lucky_no"], ref["lucky_oo"], ref["fail"])
