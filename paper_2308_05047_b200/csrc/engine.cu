@@ -387,9 +387,9 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
             std::min<uint64_t>((2 * tp.H + kFixItems - 1) / kFixItems, static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
             if (pl.split_tail) {
-                k_tiled<true, true><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
+                k_tiled<true, true><<<g1, tile_threads<true, true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
             } else {
-                k_tiled<true, false><<<g1, tile_threads<true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
+                k_tiled<true, false><<<g1, tile_threads<true, false>(), tile_smem_bytes<true>(), e->stream>>>(tp);
                 e->band_issued += pl.ntiles;
             }
             k_tile_fixup<<<g2, 256, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
@@ -424,9 +424,9 @@ int launch_collapse_pass(shs_engine* e, uint32_t s, int src_group, const DevStag
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         rc = launch(e, 2, [&] {
             if (pl.split_tail) {
-                k_tiled<false, true><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+                k_tiled<false, true><<<g1, tile_threads<false, true>(), tile_smem_bytes<false>(), e->stream>>>(tp);
             } else {
-                k_tiled<false, false><<<g1, tile_threads<false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
+                k_tiled<false, false><<<g1, tile_threads<false, false>(), tile_smem_bytes<false>(), e->stream>>>(tp);
                 e->band_issued += pl.ntiles;
             }
         });

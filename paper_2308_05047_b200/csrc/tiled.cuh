@@ -59,7 +59,7 @@ namespace shs {
 constexpr int kRows = SHS_TILE_ROWS;    // rows per tile (gathered-side run length)
 constexpr int kCols = SHS_TILE_COLS;    // columns per chunk (direct-side run length)
 constexpr int kStages = SHS_RING_STAGES;  // copy ring depth
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 8;  // exchange kernels and the split tiled variant
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kProducerWarps = 4;
 constexpr int kProducers = 32 * kProducerWarps;
@@ -73,6 +73,23 @@ constexpr int kNormSync = kConsumers + 32 * kChainWarps;        // named-barrier
 static_assert(kRows <= 64 && (kRows & (kRows - 1)) == 0, "kRows: power of two <= 64");
 constexpr int kRowsPerLane = kRows > 32 ? kRows / 32 : 1;       // row bookkeeping per lane
 static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0, "kCols");
+// Consumer warps of k_tiled<., kSplit>: 16 for the round-robin whole-band
+// variant (config 4: -2.3% per stage vs 8; more warps hide the shared-memory
+// and FP64 latencies of the per-element math), 8 for the split variant (16 spill
+// there and cost 15% at config 3).
+#ifndef SHS_RR_CONSUMER_WARPS
+#define SHS_RR_CONSUMER_WARPS 16
+#endif
+template <bool kSplit>
+struct TileCfg {
+    static constexpr int kCW = kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
+    static constexpr int kCons = 32 * kCW;
+    static constexpr int kProdWarp = kCW;                   // first producer warp
+    static constexpr int kChainWarp0 = kCW + kProducerWarps;  // first chain warp (probs only)
+    static constexpr int kRowsPerCons = kRows * kCols / kCons;
+    static constexpr int kNSync = kCons + 32 * kChainWarps;   // norm named-barrier thread count
+    static_assert(kCons % kCols == 0 && kRowsPerCons >= 1, "consumer layout");
+};
 #ifndef SHS_NORM_BUFS
 #define SHS_NORM_BUFS 4
 #endif
@@ -183,9 +200,9 @@ struct TileSmem {
     uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
 };
 
-template <bool kProbs>
+template <bool kProbs, bool kSplit>
 constexpr int tile_threads() {
-    return 32 * (kConsumerWarps + kProducerWarps + (kProbs ? kChainWarps : 0));
+    return 32 * (TileCfg<kSplit>::kCW + kProducerWarps + (kProbs ? kChainWarps : 0));
 }
 
 template <bool kProbs>
@@ -288,7 +305,7 @@ struct CtaWork<false> {
     }
     __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t* queue, bool is_producer)
         : q(queue), b(blockIdx.x), nt(p.ntiles), k(0), producer(is_producer) {
-        p0 = producer && threadIdx.x == 32 * kProducerWarp;
+        p0 = producer && threadIdx.x == 32 * TileCfg<false>::kProdWarp;
         if (p0) {
             q[0] = static_cast<uint32_t>(b);
             const uint64_t b1 = fetch(p);
@@ -420,11 +437,16 @@ __device__ __forceinline__ void store_rows(const LaneRows& lr, int lane, uint64_
 }
 
 template <bool kProbs, bool kSplit>
-__global__ void __launch_bounds__(tile_threads<kProbs>(), 1) k_tiled(TileParams p) {
+__global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(TileParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmem<kProbs>& sm = *reinterpret_cast<TileSmem<kProbs>*>(smem_raw);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    using Cfg = TileCfg<kSplit>;
+    constexpr int kConsumerWarps = Cfg::kCW, kConsumers = Cfg::kCons;
+    constexpr int kProducerWarp = Cfg::kProdWarp, kChainWarp = Cfg::kChainWarp0;
+    constexpr int kRowsPerConsumer = Cfg::kRowsPerCons, kNormSync = Cfg::kNSync;
+    (void)kConsumers;
     const StageScalars sc = p.dev ? p.dev->sc : p.sc;
     const int sel = p.dev ? p.dev->sel : p.sel;
 #ifdef SHS_CTA_TRACE
