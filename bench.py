@@ -40,6 +40,9 @@ WORKLOADS = {
     # config 3 (BASELINE.json configs[2]): ~24-bit semiprime
     "c3": dict(N=16777207, a=2, p=4093, q=4099,
                desc="config 3: N=16777207=4093*4099, a=2 (order 2794836), t=48"),
+    # profiling size for the round-robin tiled variant (config 4's): 17 GB per buffer
+    "n30": dict(N=1073217479, a=2, p=32749, q=32771,
+                desc="30-qubit profiling size: N=1073217479=32749*32771, a=2 (order 536575980), t=60"),
     # profiling size: 4.3 GB per buffer (34x L2), fast ncu replays
     "n29": dict(N=268435247, a=3, p=12589, q=21323,
                 desc="29-qubit profiling size: N=268435247=12589*21323, a=3 (order 67100334), t=56"),

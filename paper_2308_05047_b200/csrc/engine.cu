@@ -384,7 +384,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         const int g1 = pl.split_tail ? pl.grid
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         const int g2 = static_cast<int>(
-            std::min<uint64_t>((2 * tp.H + kFixItems - 1) / kFixItems, static_cast<uint64_t>(e->fixup_cap)));
+            std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
             if (pl.split_tail) {
                 k_tiled<true, true><<<g1, tile_threads<true, true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
@@ -392,7 +392,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
                 k_tiled<true, false><<<g1, tile_threads<true, false>(), tile_smem_bytes<true>(), e->stream>>>(tp);
                 e->band_issued += pl.ntiles;
             }
-            k_tile_fixup<<<g2, 256, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
+            k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
         *nparts = g1 + g2;
     } else {
@@ -895,7 +895,7 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     ce = cudaFuncSetAttribute(k_tile_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(kFixSmem));
     if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tile_fixup)");
-    e->fixup_cap = 3 * e->num_sms;  // 3 x 66 KB of staged head runs per SM
+    e->fixup_cap = 3 * e->num_sms;  // 3 x 68 KB of transposed head slabs per SM
     {
         const char* hm = std::getenv("SHS_HOST_MEASURE");
         e->host_measure = hm && hm[0] == '1';

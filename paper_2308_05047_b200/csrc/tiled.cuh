@@ -722,69 +722,66 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
 
 // The block straddling the boundary between a row and its z-order predecessor:
 // S_b = fold(predecessor's tail partial, this row's head norms), in z order.
-// A CTA takes kFixItems (row, group) items at a time: all 256 threads stage
-// the items' head runs (<= 2 KB each, coalesced) into shared memory, then one
-// warp folds them — lane i runs item i's serial chain, reading a padded row
-// (conflict-free), so 32 chains advance per instruction instead of one
-// thread walking its run from HBM.
-constexpr int kFixItems = 32;
-constexpr int kFixStride = 257;  // doubles per staged head run (+1: conflict-free lanes)
-constexpr size_t kFixSmem = sizeof(double) * kFixItems * kFixStride;
+// Each warp takes 32 (row, group) items at a time and walks their head runs
+// (<= 255 norms each) in 32-column slabs: for every item the warp loads the
+// slab's 32 norms coalesced (256 B), transposes them through a padded
+// shared-memory tile, and lane i folds item i's 32 values in order — 32 serial
+// chains per warp, every warp of the CTA folding.
+constexpr int kFixWarps = 8;
+constexpr int kFixStride = 33;  // doubles per transposed row (+1: conflict-free lanes)
+constexpr size_t kFixSmem = sizeof(double) * kFixWarps * 32 * kFixStride;
 
-static __global__ void __launch_bounds__(256) k_tile_fixup(TileParams p, unsigned long long* slots) {
-    extern __shared__ double fix_buf[];  // [kFixItems][kFixStride]
+static __global__ void __launch_bounds__(32 * kFixWarps, 2) k_tile_fixup(TileParams p, unsigned long long* slots) {
+    extern __shared__ double fix_buf[];  // [kFixWarps][32][kFixStride]
     __shared__ unsigned long long digits[2][kDigits];
-    __shared__ uint32_t item_hl[kFixItems];
-    __shared__ uint64_t item_z[kFixItems];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&digits[0][0])[i] = 0ull;
+    __syncthreads();
+    double* buf = fix_buf + warp * 32 * kFixStride;
     DigitWindow win;
     window_reset(win);
+    const int g = lane & 1;  // item base + lane has group (base + lane) & 1, base even
     const uint64_t items = 2 * p.H;
-    for (uint64_t base = uint64_t(blockIdx.x) * kFixItems; base < items;
-         base += uint64_t(gridDim.x) * kFixItems) {
-        __syncthreads();  // the previous group's staged runs are folded
-        if (tid < kFixItems) {
-            const uint64_t idx = base + tid;
-            uint32_t hl = 0;
-            uint64_t z = 0;
-            if (idx < items) {
-                z = mulmod_shoup(idx >> 1, p.A, p.A_sh, p.N);
-                hl = static_cast<uint32_t>((256 - (z & 255)) & 255);
-            }
-            item_hl[tid] = hl;
-            item_z[tid] = z;
+    for (uint64_t base = (uint64_t(blockIdx.x) * kFixWarps + warp) * 32; base < items;
+         base += uint64_t(gridDim.x) * kFixWarps * 32) {
+        const uint64_t idx = base + lane;
+        uint32_t hl = 0;
+        uint64_t z = 0;
+        if (idx < items) {
+            z = mulmod_shoup(idx >> 1, p.A, p.A_sh, p.N);
+            hl = static_cast<uint32_t>((256 - (z & 255)) & 255);
         }
-        __syncthreads();
+        double s = hl ? p.tail[idx] : 0.0;  // tail[j * 2 + g]
+        const uint32_t maxhl = __reduce_max_sync(0xffffffffu, hl);
+        // slab c0 of every item, lane = column: loaded one slab ahead of the fold
+        double v[32];
+        auto load_slab = [&](uint32_t c0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t hli = __shfl_sync(0xffffffffu, hl, i);
+                v[i] = c0 + lane < hli ? p.head[(base + i) * 256 + c0 + lane] : 0.0;
+            }
+        };
+        if (maxhl) load_slab(0);
+        for (uint32_t c0 = 0; c0 < maxhl; c0 += 32) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) buf[i * kFixStride + lane] = v[i];
+            __syncwarp();
+            if (c0 + 32 < maxhl) load_slab(c0 + 32);
+            const double* row = buf + lane * kFixStride;
 #pragma unroll 8
-        for (int i = 0; i < kFixItems; ++i) {
-            const uint32_t hl = item_hl[i];
-            if (static_cast<uint32_t>(tid) < hl)
-                fix_buf[i * kFixStride + tid] = p.head[(base + i) * 256 + tid];
-        }
-        __syncthreads();
-        if (tid < kFixItems) {
-            const uint32_t hl = item_hl[tid];
-            const uint64_t idx = base + tid;
-            if (hl) {
-                const int g = static_cast<int>(idx & 1);
-                double s = p.tail[idx];  // tail[j * 2 + g]
-                const double* row = fix_buf + tid * kFixStride;
-                uint32_t q = 0;
-                for (; q + 8 <= hl; q += 8) {
-                    double v[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) v[u] = row[q + u];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
-                }
-                for (; q < hl; ++q) s = __dadd_rn(s, row[q]);
-                p.S[g * p.nb + (item_z[tid] >> 8)] = s;
-                window_add(win, s, digits[g]);  // g = tid & 1: base is even
+            for (int cc = 0; cc < 32; ++cc) {
+                const double x = row[cc];
+                if (c0 + cc < hl) s = __dadd_rn(s, x);
             }
+            __syncwarp();
+        }
+        if (hl) {
+            p.S[g * p.nb + (z >> 8)] = s;
+            window_add(win, s, digits[g]);
         }
     }
-    if (tid < kFixItems) window_flush(win, digits[tid & 1]);
+    window_flush(win, digits[g]);
     __syncthreads();
     write_partials(digits, slots + uint64_t(blockIdx.x) * 2 * kDigits, tid);
 }
