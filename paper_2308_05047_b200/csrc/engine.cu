@@ -182,6 +182,11 @@ int sync(shs_engine* e) {
 // stall the staged CTAs, only from A = kStreamsProbsMinA (config 4, B200:
 // A = 625 probs 92 -> 51 ms, collapse 119 -> 46 ms; A = 25 collapse 65 -> 36 ms,
 // probs 40 either way; A = 5 probs 32 ms gathered vs 41 ms staged).
+// Head scratch a small-multiplier tile plan may use (tile_plan.hpp
+// make_small_a_plan): up to half a state buffer (config 4, A = 625: 28 GB
+// beside the 137 GB state on a 180 GB B200).
+uint64_t small_a_scratch(uint64_t N) { return N * sizeof(double2) / 2; }
+
 constexpr uint32_t kStreamsProbsMinA = 64;
 bool streams_stage(const shs_engine* e, uint32_t s) {
     return e->a_pows[s] != 1 && e->a_pows[s] <= kStreamsMaxA && e->N >= kTileAutoMinN &&
@@ -827,7 +832,8 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
                                    [&](const auto& kv) { return kv.first == e->a_pows[s]; });
             if (it == cache.end()) {
                 cache.emplace_back(e->a_pows[s],
-                                   make_tile_plan(e->a_pows[s], e->a_invs[s], e->N, o.tiling));
+                                   make_tile_plan(e->a_pows[s], e->a_invs[s], e->N, o.tiling,
+                                                  small_a_scratch(e->N)));
                 it = cache.end() - 1;
             }
             e->plans[s] = it->second;

@@ -98,10 +98,40 @@ inline void make_tile_split(TilePlanHost& pl, int cap) {
 // every candidate. Multipliers without such an H (tiny A, or A/N with a huge
 // partial quotient) keep the direct gather, whose warps then read a few long
 // runs anyway.
-inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling) {
+// Small multipliers (kTileMinRow <= A, N / A > the scan's row cap): the rows
+// z_j = j A are the consecutive A-long runs of Z_N (u = 1, v = H - 1, the last
+// row A + N mod A long), H = floor(N / A). The tile is then the same
+// 32-row x 32-column transpose (gathered runs j..j+31 + i m); the price is one
+// head run per row in the fixup scratch (H x 4 KB), so the single engine takes
+// it only while that scratch stays within max_scratch bytes.
+inline TilePlanHost make_small_a_plan(uint64_t A, uint64_t m, uint64_t N, uint64_t max_scratch) {
+    TilePlanHost pl;
+    if (A < kTileMinRow || A >= N / kTileMinRowsPlan) return pl;
+    const uint64_t H = N / A;
+    if (H <= kTileMaxRows || H * 2 * 257 * sizeof(double) > max_scratch) return pl;
+    pl.tiled = true;
+    pl.H = H;
+    pl.u = 1;
+    pl.v = H - 1;
+    pl.du = A;
+    pl.dv = A + N % A;
+    pl.A = A;
+    pl.A_sh = shoup(A, N);
+    pl.m = m;
+    pl.m_sh = shoup(m, N);
+    pl.ntiles = (pl.H + kRows - 1) / kRows;
+    return pl;
+}
+
+inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling,
+                                   uint64_t small_a_scratch = 0) {
     TilePlanHost pl;
     if (tiling == SHS_TILING_OFF || A == 1) return pl;
     if (tiling == SHS_TILING_AUTO && N < kTileAutoMinN) return pl;
+    if (small_a_scratch) {
+        pl = make_small_a_plan(A, m, N, small_a_scratch);
+        if (pl.tiled) return pl;
+    }
     const uint64_t hmax = std::min<uint64_t>(N / kTileAvgRow, kTileMaxRows);
     std::vector<uint64_t> cands;
     for (uint64_t h = 2; h <= hmax; h *= 2) {

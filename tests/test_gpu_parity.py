@@ -303,16 +303,23 @@ def test_tiled_work_split_vs_direct(cuda_ok, monkeypatch, N, a, split):
         prefix |= b << s
 
 
-@pytest.mark.parametrize("N,a", [(16777207, 2), (268435247, 3), (4194301, 7)])
+@pytest.mark.parametrize("N,a", [(16777207, 2), (268435247, 3), (4194301, 7), (268435247, 5)])
 def test_small_multiplier_streams_vs_gather(cuda_ok, N, a):
     """The last stages (multipliers a, a^2, a^4 ... <= 1024) stage their A
     gathered runs through shared memory (kSrcStreams, from the run start e_1 and
-    from a general state): bit-identical to the per-amplitude gather."""
+    from a general state), or, for 512 <= A with more than 2^18 A-long rows
+    (N = 268435247, A = 625: the config-4 case), run as tiles of the consecutive
+    rows j A (tile_plan.hpp make_small_a_plan): bit-identical to the
+    per-amplitude gather."""
     rng = np.random.default_rng(N + a)
     fast, ref = engine(N, a), engine(N, a, tiling="off")
     pows = fast.stage_multipliers()
     s0 = fast.t - 6
     assert sum(1 for s in range(s0, fast.t) if 1 < pows[s] <= 1024) >= 2
+    for s in range(s0, fast.t):
+        if 512 <= pows[s] and N // pows[s] > (1 << 18):
+            pl = fast.tile_plan(s)
+            assert pl["tiled"] and pl["H"] == N // pows[s] and pl["u"] == 1, pl
     fast.state_init()
     ref.state_init()
     prefix = 0
@@ -397,6 +404,12 @@ def test_tile_plans_partition_and_auto_selection(cuda_ok):
             if pl["tiled"]:
                 ntiled += 1
                 H = pl["H"]
+                if pl["u"] == 1 and H == N // pows[s] and H > (1 << 18):
+                    # small-multiplier plan: the A-long runs j A, the last one A + N mod A
+                    A = pows[s]
+                    assert 512 <= A and pl["du"] == A and pl["dv"] == A + N % A
+                    assert pl["v"] == H - 1 and (H - 1) * A + pl["dv"] == N
+                    continue
                 assert pl["du"] >= 512 and pl["dv"] >= 512 and H <= N // 640
                 assert pl["du"] + pl["dv"] <= 3 * (N // H + 1) and H >= 256
         assert ntiled >= eng.t - 6, (N, ntiled)  # all but stage 0 and the tiny multipliers
