@@ -400,17 +400,20 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
             k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
         *nparts = g1 + g2;
+    } else if (e->e1) {
+        // stage 0 from the implicit e_1: two live amplitudes (k_stage_probs_e1)
+        StageParams p = params_for(e, s);
+        rc = launch(e, 0, [&] {
+            cudaMemsetAsync(e->S, 0, sizeof(double) * 2 * e->nb, e->stream);
+            k_stage_probs_e1<<<1, 32, 0, e->stream>>>(p, e->a_pows[s]);
+        });
+        *nparts = 1;
     } else {
         StageParams p = params_for(e, s);
         p.dev = dev;
         rc = launch(e, 0, [&] {
-            if (gather) {
-                if (e->e1) launch_probs<true, true>(e, p);
-                else launch_probs<true, false>(e, p);
-            } else {
-                if (e->e1) launch_probs<false, true>(e, p);
-                else launch_probs<false, false>(e, p);
-            }
+            if (gather) launch_probs<true, false>(e, p);
+            else launch_probs<false, false>(e, p);
         });
     }
     return rc;
