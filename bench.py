@@ -288,19 +288,30 @@ def run_ours(args):
                 "share_of_step": kernels[dom]["avg_ms"] / ms_per_step,
                 "bytes_per_amp": per_amp[dom]}
 
-    # end to end: the public call a user makes (C ABI, host results), full run
-    e2e_runs = max(1, args.e2e_runs)
-    t0 = time.perf_counter()
-    for i in range(e2e_runs):
-        res = eng.run(seed, 1000 + i)
-    run_s = (time.perf_counter() - t0) / e2e_runs
-    if ws > 1:
-        tr = torch.tensor([run_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(tr, op=dist.ReduceOp.MAX)
-        run_s = float(tr.item())
+    # end to end: the public call a user makes (C ABI, host results), full run.
+    # e2e.value: every stage dense over all N amplitudes (the reference's work,
+    # apples to apples with the kernel numbers); s_per_run: the default run()
+    # with its sparse prefix (the first stages on the support of the state,
+    # bit-identical results), the "s per full iterative-Shor run" metric.
+    def timed_runs(sparse):
+        eng.set_sparse(sparse)
+        e2e_runs = max(1, args.e2e_runs)
+        t0 = time.perf_counter()
+        for i in range(e2e_runs):
+            r = eng.run(seed, 1000 + i)
+        sec = (time.perf_counter() - t0) / e2e_runs
+        if ws > 1:
+            tr = torch.tensor([sec], device=dev, dtype=torch.float64)
+            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+            sec = float(tr.item())
+        return sec, r
+    run_s_dense, res = timed_runs(False)
+    run_s, res_sparse = timed_runs(True)
+    sparse_stages = eng.sparse_stages()
+    assert res_sparse.bits.j == res.bits.j and res_sparse.j_sampled == res.j_sampled
 
     value = ws * N / (ms_per_step * 1e-3)
-    e2e_value = ws * N * t / run_s
+    e2e_value = ws * N * t / run_s_dense
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -311,6 +322,8 @@ def run_ours(args):
                    "l2": "state 540x larger than the 126 MB L2: no flush needed",
                    "parallelism": "1 GPU" if ws == 1 else f"{ws} independent replicas"},
         "s_per_run": run_s,
+        "s_per_run_dense": run_s_dense,
+        "sparse_prefix_stages": sparse_stages,
         "stage_hbm_gbs": 80 * N / (ms_per_step * 1e-3) / 1e9,
         "stage_frac_of_hbm": 80 * N / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
         "wall_ms_per_step": 1e3 * wall / args.steps,
@@ -318,9 +331,12 @@ def run_ours(args):
         "roofline": roofline, "kernels": kernels,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 16,
-                "what": "IterativeShorEngine.run(seed, idx) through the C ABI: t stages, "
-                        "p0/p1 read back every stage, bit string returned to the host; "
-                        "inputs are the problem scalars (kernel arguments)",
+                "what": "IterativeShorEngine.run(seed, idx) through the C ABI with every stage "
+                        "dense (set_sparse(False)): t stages, p0/p1 decided on the device, "
+                        "bit string returned to the host; inputs are the problem scalars "
+                        "(kernel arguments). The default run() (sparse prefix) is s_per_run, "
+                        "same bit string",
+                "s_per_run_default": run_s,
                 "last_j": str(res.bits.j)},
         "gpu_launches": launches, "clocks": clock_info,
     }
@@ -436,7 +452,8 @@ def config3_runs(shs):
     """Config 3 (BASELINE.json configs[2]): N = 16777207, t = 48, full runs
     through the C ABI with each of the paper's error models at p_error = 0.01
     (acceptance criterion 8's settings, proj/tests/acceptance/acceptance_main.cpp:
-    367-378), amplitude updates/s = N t / run time."""
+    367-378): s per run with every stage dense (amplitude updates/s = N t / that)
+    and with the default sparse prefix."""
     w = WORKLOADS["c3"]
     N, a = w["N"], w["a"]
     prob = shs.FactoringProblem.make(N, a)
@@ -452,13 +469,22 @@ def config3_runs(shs):
     out = {"N": N, "a": a, "t": prob.t}
     for name, err in models.items():
         eng = shs.IterativeShorEngine(prob, err, shs.SimulatorOptions(qubit_ceiling=64))
-        eng.run(7, 0)  # warm
-        t0 = time.perf_counter()
-        runs = 3
-        for i in range(runs):
-            eng.run(7, 1 + i)
-        dt = (time.perf_counter() - t0) / runs
-        out[name] = {"s_per_run": dt, "amp_updates_per_s": N * prob.t / dt}
+        entry = {}
+        for sparse in (False, True):  # every stage dense; the default run() (sparse prefix)
+            eng.set_sparse(sparse)
+            eng.run(7, 0)  # warm
+            t0 = time.perf_counter()
+            runs = 3
+            for i in range(runs):
+                eng.run(7, 1 + i)
+            dt = (time.perf_counter() - t0) / runs
+            if sparse:
+                entry["s_per_run"] = dt
+                entry["sparse_prefix_stages"] = eng.sparse_stages()
+            else:
+                entry["s_per_run_dense"] = dt
+                entry["amp_updates_per_s_dense"] = N * prob.t / dt
+        out[name] = entry
         eng.close()
     return out
 
@@ -560,6 +586,8 @@ def run_sharded(args):
                    "shard_amplitudes": nloc, "parallelism": f"{ws} shards (block-sharded state)",
                    "l2": "state far larger than L2: no flush needed"},
         "s_per_run": run_s,
+        "s_per_run_dense": run_s_dense,
+        "sparse_prefix_stages": sparse_stages,
         "kernels_max_over_ranks_ms": kms,
         "roofline": {"kernel": "k_stage_probs/collapse (shard-local) + k_exchange", "bound": "hbm",
                      "achieved": 96 * nloc / ((kms["probs"] + kms["collapse"] + kms["exchange"]) * 1e-3) / 1e9,

@@ -108,6 +108,8 @@ SIGNATURES = [
     ("shs_shard_stream", vp, [vp]),
     ("shs_exhaustive_distribution", C.c_int, [C.POINTER(shs_problem), C.POINTER(shs_error), u64,
                                               i32, C.POINTER(dbl)]),
+    ("shs_engine_set_sparse", C.c_int, [C.c_void_p, i32]),
+    ("shs_engine_sparse_stages", u32, [C.c_void_p]),
     ("shs_shor_postprocess", C.c_int, [C.POINTER(u64), u32, u32, u64, u64, u64, i32, i32,
                                        C.c_void_p]),
     ("shs_last_error", C.c_char_p, []),

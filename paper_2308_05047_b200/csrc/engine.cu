@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/shorsim_b200.h"
@@ -37,6 +38,7 @@
 #include "tile_plan.hpp"
 #include "tiled.cuh"
 #include "batch.cuh"
+#include "sparse.cuh"
 
 using namespace shs;
 
@@ -118,6 +120,18 @@ struct shs_engine {
     StageRec* d_rec = nullptr;     // its device alias
     cudaEvent_t meas_ev[2] = {nullptr, nullptr};
     bool host_measure = false;     // SHS_HOST_MEASURE=1: the host-driven loop (A/B)
+    // sparse prefix of device-resident runs (sparse.cuh): stages 0 .. sparse_n-1
+    // on the support, carved out of Y (unused until the first dense stage)
+    uint32_t sparse_n = 0;
+    bool sparse_on = true;         // shs_engine_set_sparse
+    uint64_t* sZ[2] = {nullptr, nullptr};
+    double2* sV[2] = {nullptr, nullptr};
+    uint64_t* sKeys = nullptr;
+    uint32_t* sIdx = nullptr;
+    uint32_t* sIdx2 = nullptr;
+    double* sNrm = nullptr;
+    void* sTemp = nullptr;
+    size_t sTempBytes = 0;
 };
 
 namespace {
@@ -320,6 +334,88 @@ void release(shs_engine* e) {
 // The two N-amplitude buffers (sel and its successor) and the block partials
 // are allocated on first use, so engines used only for validation or index
 // maps never reserve 2 x 16 N bytes of HBM.
+// Smallest j in [1, M) with A^j = 1 (mod N), or 0 when there is none
+// (baby-step giant-step, O(sqrt M) multiplications). A is a unit mod N.
+uint64_t small_order(uint64_t A, uint64_t N, uint64_t M) {
+    if (A % N == 1) return 1;
+    uint64_t m = 1;
+    while (m * m < M) ++m;
+    std::unordered_map<uint64_t, uint64_t> baby;
+    baby.reserve(2 * m);
+    uint64_t x = 1;
+    for (uint64_t i = 0; i < m; ++i) {
+        if (i > 0 && x == 1) return i < M ? i : 0;
+        baby.emplace(x, i);
+        x = mulmod(x, A, N);
+    }
+    uint64_t ginv = 0, g = 0;  // x = A^m
+    if (mod_inverse(x, N, &ginv, &g) != SHS_OK) return 0;
+    uint64_t y = 1;
+    for (uint64_t q = 1; q <= m; ++q) {
+        y = mulmod(y, ginv, N);  // A^(-q m)
+        auto it = baby.find(y);
+        if (it != baby.end()) {
+            const uint64_t j = q * m + it->second;
+            return j < M ? j : 0;
+        }
+    }
+    return 0;
+}
+
+constexpr uint64_t kSparseMinN = 1ull << 22;  // sparse prefix from 64 MB of state
+constexpr uint64_t kSparseDensity = 64;       // support <= N / 64
+
+// Stages run on the support: the largest n <= t - 1 with 2^n <= N / 64 whose
+// last multiplier A_{n-1} has order >= 2^n (then every earlier stage's has
+// too: ord(A_s) >= ord(A_{n-1}) / 2^(n-1-s)), so the orbit never wraps.
+uint32_t plan_sparse_prefix(const shs_engine* e) {
+    if (e->N < kSparseMinN || e->kahan) return 0;
+    const uint64_t cap = e->N / kSparseDensity;
+    uint32_t n = 0;
+    while (n + 1 <= e->t - 1 && (uint64_t(1) << (n + 1)) <= cap) ++n;
+    if (n == 0) return 0;
+    const uint64_t ord = small_order(e->a_pows[n - 1], e->N, uint64_t(1) << n);
+    if (ord == 0) return n;
+    // ord(A_{n-1}) < 2^n: the largest s with ord(A_s) >= 2^(s+1)
+    for (uint32_t m = n; m > 0; --m) {
+        uint64_t o = ord;
+        for (uint32_t k = 0; k < n - m && o % 2 == 0; ++k) o /= 2;  // ord(A_{m-1})
+        if (o >= (uint64_t(1) << m)) return m;
+    }
+    return 0;
+}
+
+// Sparse buffers inside the current Y (free until the first dense collapse of a
+// run; carved again at every run start since X / Y swap): Z0 Z1 (u64), V0 V1
+// (double2), sorted keys (u64), idx idx2 (u32), nrm (2 doubles) per support
+// element, then the radix sort's scratch.
+int carve_sparse(shs_engine* e) {
+    const uint64_t K = uint64_t(1) << e->sparse_n;
+    char* p = reinterpret_cast<char*>(e->Y);
+    auto take = [&](size_t bytes) {
+        char* q = p;
+        p += (bytes + 255) & ~size_t(255);
+        return q;
+    };
+    e->sZ[0] = reinterpret_cast<uint64_t*>(take(8 * K));
+    e->sZ[1] = reinterpret_cast<uint64_t*>(take(8 * K));
+    e->sV[0] = reinterpret_cast<double2*>(take(16 * K));
+    e->sV[1] = reinterpret_cast<double2*>(take(16 * K));
+    e->sKeys = reinterpret_cast<uint64_t*>(take(8 * K));
+    e->sIdx = reinterpret_cast<uint32_t*>(take(4 * K));
+    e->sIdx2 = reinterpret_cast<uint32_t*>(take(4 * K));
+    e->sNrm = reinterpret_cast<double*>(take(16 * K));
+    if (!e->sTempBytes) {
+        SHS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, e->sTempBytes, e->sZ[0], e->sKeys,
+                                                 e->sIdx, e->sIdx2, static_cast<int>(K), 0, 64,
+                                                 e->stream));
+    }
+    e->sTemp = take(e->sTempBytes);
+    if (static_cast<size_t>(p - reinterpret_cast<char*>(e->Y)) > sizeof(double2) * e->N)
+        return set_error(SHS_CUDA_ERROR, "sparse prefix buffers exceed the state buffer");
+    return SHS_OK;
+}
+
 int ensure_buffers(shs_engine* e) {
     if (e->X) return SHS_OK;
     const size_t amp_bytes = sizeof(double2) * e->N;
@@ -504,6 +600,75 @@ int stage_collapse(shs_engine* e, int src_group, double p_src, bool wait) {
     return SHS_OK;
 }
 
+// Sparse prefix stage s (sparse.cuh) on the support of 2^s elements:
+// expand (both norms per new orbit index) -> radix sort by z -> in-order block
+// folds into exact digit slots. *nparts = the fold's CTAs.
+SparseParams sparse_params(shs_engine* e, uint32_t s, const DevStage* dev) {
+    SparseParams p{};
+    p.Zo = e->sZ[s & 1];
+    p.Vo = e->sV[s & 1];
+    p.Ko = uint64_t(1) << s;
+    p.A = e->a_pows[s];
+    p.A_sh = shoup(p.A, e->N);
+    p.N = e->N;
+    p.sc = e->sc;
+    p.dev = dev;
+    p.Zn = e->sZ[(s + 1) & 1];
+    p.Vn = e->sV[(s + 1) & 1];
+    p.idx = e->sIdx;
+    p.nrm = e->sNrm;
+    return p;
+}
+
+int sparse_grid(const shs_engine* e, uint64_t n) {
+    return static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((n + kSparseThreads - 1) / kSparseThreads, e->grid_cap)));
+}
+
+int launch_sparse_probs(shs_engine* e, uint32_t s, const DevStage* dev, int* nparts) {
+    SparseParams p = sparse_params(e, s, dev);
+    const uint64_t Kn = 2 * p.Ko;
+    int end_bit = 1;
+    while (end_bit < 64 && (e->N - 1) >> end_bit) ++end_bit;
+    const int gf = sparse_grid(e, Kn);
+    cudaError_t sort_err = cudaSuccess;
+    int rc = launch(e, 0, [&] {
+        if (s == 0) k_sparse_init<<<1, 1, 0, e->stream>>>(e->sZ[0], e->sV[0]);
+        k_sparse_expand<<<sparse_grid(e, p.Ko), kSparseThreads, 0, e->stream>>>(p);
+        size_t bytes = e->sTempBytes;
+        sort_err = cub::DeviceRadixSort::SortPairs(e->sTemp, bytes, p.Zn, e->sKeys, e->sIdx,
+                                                   e->sIdx2, static_cast<int>(Kn), 0, end_bit,
+                                                   e->stream);
+        k_sparse_fold<<<gf, kSparseThreads, 0, e->stream>>>(e->sKeys, e->sIdx2, e->sNrm, Kn,
+                                                           e->partials);
+    });
+    if (rc) return rc;
+    if (sort_err != cudaSuccess)
+        return set_error(SHS_CUDA_ERROR, std::string("sparse sort: ") + cudaGetErrorString(sort_err));
+    e->launches += 2;  // expand + fold (and the sort's own kernels) beside the counted one
+    *nparts = gf;
+    return SHS_OK;
+}
+
+int launch_sparse_collapse(shs_engine* e, uint32_t s, const DevStage* dev) {
+    SparseParams p = sparse_params(e, s, dev);
+    return launch(e, 2, [&] {
+        k_sparse_collapse<<<sparse_grid(e, p.Ko), kSparseThreads, 0, e->stream>>>(p, 0);
+    });
+}
+
+// the dense sel (X) from the support entering stage s
+int materialize_sparse(shs_engine* e, uint32_t s) {
+    const uint64_t K = uint64_t(1) << s;
+    SHS_CUDA(cudaMemsetAsync(e->X, 0, sizeof(double2) * e->N, e->stream));
+    int rc = launch(e, -1, [&] {
+        k_sparse_scatter<<<sparse_grid(e, K), kSparseThreads, 0, e->stream>>>(e->sZ[s & 1],
+                                                                           e->sV[s & 1], K, e->X);
+    });
+    e->e1 = false;
+    return rc;
+}
+
 // Device-resident run (the default for engine_run): per stage the host queues
 //   probs(s) -> k_finalize_measure(s) -> collapse(s)
 // and the device measures and collapses without a host round trip. The host
@@ -574,12 +739,19 @@ int engine_run_device(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_ou
         e->pending = false;
         return code;
     };
+    const uint32_t nsp = e->sparse_on ? e->sparse_n : 0;  // stages on the support
+    if (nsp && (rc = carve_sparse(e))) return rc;
     for (uint32_t s = 0; s < e->t; ++s) {
         DevStage* cur = e->d_slots + (s & 1);
         DevStage* nxt = e->d_slots + ((s + 1) & 1);
         int nparts = 0;
         e->sc = sc;  // stage 0's kernel arguments (later stages read the slot)
-        if ((rc = launch_probs_pass(e, s, s == 0 ? nullptr : cur, &nparts))) return fail(rc);
+        if (s < nsp) {
+            if ((rc = launch_sparse_probs(e, s, s == 0 ? nullptr : cur, &nparts))) return fail(rc);
+        } else {
+            if (s == nsp && nsp && (rc = materialize_sparse(e, s))) return fail(rc);
+            if ((rc = launch_probs_pass(e, s, s == 0 ? nullptr : cur, &nparts))) return fail(rc);
+        }
         // the observed prefix through stage s-1
         if (s > 0 && (rc = absorb(s - 1))) return fail(rc);
         MeasureStep ms{};
@@ -607,7 +779,10 @@ int engine_run_device(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_ou
         if (rc) return fail(rc);
         if (cudaEventRecord(e->meas_ev[s & 1], e->stream) != cudaSuccess)
             return fail(set_error(SHS_CUDA_ERROR, "event record"));
-        if (s + 1 < e->t && (rc = launch_collapse_pass(e, s, 0, cur))) return fail(rc);
+        if (s + 1 < e->t) {
+            rc = s < nsp ? launch_sparse_collapse(e, s, cur) : launch_collapse_pass(e, s, 0, cur);
+            if (rc) return fail(rc);
+        }
     }
     if ((rc = absorb(e->t - 1))) return fail(rc);
     if ((rc = sync(e))) return rc;
@@ -923,6 +1098,7 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     if ((ce = cudaHostAlloc(&e->h_out, 4 * sizeof(double), cudaHostAllocDefault)) != cudaSuccess)
         return fail(ce, "cudaHostAlloc");
     e->device_bytes = part_bytes + 32;  // the N-amplitude buffers come with the first stage
+    e->sparse_n = plan_sparse_prefix(e);
     state_init(e);
     *out = e;
     return SHS_OK;
@@ -931,6 +1107,16 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
 void shs_engine_destroy(shs_engine* e) { release(e); }
 
 uint32_t shs_engine_stages(const shs_engine* e) { return e ? e->t : 0; }
+
+int shs_engine_set_sparse(shs_engine* e, int32_t enable) {
+    if (!e) return set_error(SHS_INVALID_ARGUMENT, "null engine");
+    e->sparse_on = enable != 0;
+    return SHS_OK;
+}
+
+uint32_t shs_engine_sparse_stages(const shs_engine* e) {
+    return e && e->sparse_on ? e->sparse_n : 0;
+}
 
 int shs_engine_stage_multipliers(const shs_engine* e, uint64_t* out) {
     if (!e || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");

@@ -397,6 +397,14 @@ class IterativeShorEngine:
     def stream_handle(self) -> int:
         return self._lib.shs_engine_stream(self._h) or 0
 
+    def set_sparse(self, enable: bool) -> None:
+        """Sparse prefix of run() (on by default where it applies): the first
+        stages on the support of the state, bit-identical results."""
+        _raise(self._lib.shs_engine_set_sparse(self._h, 1 if enable else 0))
+
+    def sparse_stages(self) -> int:
+        return self._lib.shs_engine_sparse_stages(self._h)
+
     def launch_count(self) -> int:
         return self._lib.shs_engine_launch_count(self._h)
 

@@ -71,3 +71,50 @@ def test_device_run_interleaves_with_step_api(cuda_ok, monkeypatch):
     b = dev.run(5, 1)
     same_run(a, host.run(5, 0))
     same_run(b, host.run(5, 1))
+
+
+# ---------------------------------------------------------------- sparse prefix
+def _runs(eng, seed, n):
+    return [eng.run(seed, i) for i in range(n)]
+
+
+@pytest.mark.parametrize("N,a,t", [(16777207, 2, None), (16777207, 3, None), (16777207, 2, 10),
+                                   (67108859, 5, 20)])
+@pytest.mark.parametrize("ei", [0, 3, 5])
+def test_sparse_prefix_equals_dense(cuda_ok, monkeypatch, N, a, t, ei):
+    """The first stages on the support of the state (sparse.cuh) against the
+    dense device-resident run and the host-driven loop: identical bit strings,
+    sampled bits and p1 traces (every stage, every error model)."""
+    err = ERRS[ei]
+    sp, host = pair(monkeypatch, N, a, t, err)
+    dense = engine(N, a, t, err)
+    dense.set_sparse(False)
+    assert sp.sparse_stages() >= 8 and dense.sparse_stages() == 0
+    for r, d, h in zip(_runs(sp, 19, 2), _runs(dense, 19, 2), _runs(host, 19, 2)):
+        same_run(r, d)
+        same_run(r, h)
+    # the pending last stage is the same dense state
+    for first in (0, N // 2, N - 4096):
+        for x in (0, 1):
+            assert np.array_equal(np.asarray(sp.stage_read(x, first, 4096)),
+                                  np.asarray(dense.stage_read(x, first, 4096)))
+
+
+def test_sparse_prefix_stops_before_the_orbit_wraps(cuda_ok):
+    """a of small order (1364 | ord): the host's baby-step giant-step check caps
+    the sparse prefix where 2^(s+1) would exceed ord(A_s); results still equal
+    the dense run."""
+    import paper_2308_05047_b200 as shs
+    N, lam = 16777207, 2794836
+    a = pow(2, lam // 1364, N)
+    o = shs.multiplicative_order(a, N, (4093, 4099))
+    assert o <= 1364
+    sp = engine(N, a)
+    dense = engine(N, a)
+    dense.set_sparse(False)
+    n = sp.sparse_stages()
+    pows = sp.stage_multipliers()
+    for s in range(n):  # no wrap inside the prefix
+        assert shs.multiplicative_order(pows[s], N, (4093, 4099)) >= 2 ** (s + 1)
+    for r, d in zip(_runs(sp, 3, 3), _runs(dense, 3, 3)):
+        same_run(r, d)
