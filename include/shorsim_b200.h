@@ -141,7 +141,7 @@ int shs_engine_run_sequential(shs_engine* engine, uint64_t seed, uint64_t idx0, 
 int shs_engine_stage_multipliers(const shs_engine* engine, uint64_t* out);
 /* sparse prefix of runs: the first stages computed on the support of the
  * state (2^(s+1) amplitudes after stage s), bit-identical p0/p1 and bit
- * strings; on by default where it applies (N >= 2^22, support <= N / 64, the
+ * strings; on by default where it applies (N >= 2^22, support <= N / 16, the
  * orbit does not wrap). shs_engine_sparse_stages = stages it covers (0: none). */
 int shs_engine_set_sparse(shs_engine* engine, int32_t enable);
 uint32_t shs_engine_sparse_stages(const shs_engine* engine);

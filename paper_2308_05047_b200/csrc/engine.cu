@@ -363,14 +363,17 @@ uint64_t small_order(uint64_t A, uint64_t N, uint64_t M) {
 }
 
 constexpr uint64_t kSparseMinN = 1ull << 22;  // sparse prefix from 64 MB of state
-constexpr uint64_t kSparseDensity = 64;       // support <= N / 64
+constexpr uint64_t kSparseDensity = 16;       // support <= N / 16 (A/B: 64 / 32 / 16 / 8 -> config 4 2345 / 2299 / 2269 / 2290 ms per run)
 
-// Stages run on the support: the largest n <= t - 1 with 2^n <= N / 64 whose
+// Stages run on the support: the largest n <= t - 1 with 2^n <= N / 16 whose
 // last multiplier A_{n-1} has order >= 2^n (then every earlier stage's has
 // too: ord(A_s) >= ord(A_{n-1}) / 2^(n-1-s)), so the orbit never wraps.
 uint32_t plan_sparse_prefix(const shs_engine* e) {
     if (e->N < kSparseMinN || e->kahan) return 0;
-    const uint64_t cap = e->N / kSparseDensity;
+    uint64_t density = kSparseDensity;
+    if (const char* d = std::getenv("SHS_SPARSE_DENSITY"))  // A/B hook (>= 8: buffers fit Y)
+        density = std::max<uint64_t>(8, std::strtoull(d, nullptr, 10));
+    const uint64_t cap = e->N / density;
     uint32_t n = 0;
     while (n + 1 <= e->t - 1 && (uint64_t(1) << (n + 1)) <= cap) ++n;
     if (n == 0) return 0;

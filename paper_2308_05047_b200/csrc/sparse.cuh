@@ -6,7 +6,7 @@
 // and stage s maps orbit index k to the two new indices 2k (z = A_{s-1}^k: the
 // direct term, the gathered term is outside the support) and 2k+1
 // (z = A_{s-1}^k A_s: the gathered term, the direct term is outside). The
-// engine keeps (z, value) pairs in orbit order while 2^(s+1) <= N / 64 and the
+// engine keeps (z, value) pairs in orbit order while 2^(s+1) <= N / 16 and the
 // orbit does not wrap (the host proves ord(A) >= 2^(s+1) once per engine by a
 // baby-step giant-step search), then scatters them into the dense buffer.
 //
