@@ -433,6 +433,12 @@ def config2_statistics(shs, engines, problems, ref):
                         "mean_success": statistics.mean(r.success_fraction() for r in rs),
                         "mean_success_lucky": statistics.mean(r.success_lucky_fraction()
                                                               for r in rs)}
+    t0 = time.perf_counter()  # Ekerå's pipeline on the same shots (post_mode="ekera")
+    ek = [shs.run_problem(p, M, engine=e, post_mode="ekera") for p, e in zip(probs, engines)]
+    out["ekera"] = {"seconds": time.perf_counter() - t0}
+    for N in (21, 35):
+        rs = [r for r in ek if r.problem.N == N]
+        out["ekera"][f"N{N}_mean_success"] = statistics.mean(r.success_fraction() for r in rs)
     import numpy as np
     j = np.zeros((1 << 20, 2), dtype=np.uint64)
     j[:, 0] = np.arange(1 << 20, dtype=np.uint64) * np.uint64(2654435761) % np.uint64(1 << 22)

@@ -280,6 +280,30 @@ int shs_shor_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t
                          uint64_t known_order, int32_t has_known_order, int32_t device,
                          shs_shor_outcome* out);
 
+/* ---- Ekerå post-processing on the device (proj/src/postprocess.cpp:92-171) ----
+ * ekera_postprocess(j, t, N, a, params, RngStream(seed, idx0 + i, 1, postprocess),
+ * known_order) for a batch of bit strings; params as EkeraParams
+ * (postprocess.hpp:43-53; for_problem(L, t) = {B = L, c = 1, k = 100,
+ * varsigma = 1, m = L, ell = t - L}). */
+typedef struct {
+    uint64_t B, c;
+    uint32_t k, varsigma, m, ell;
+} shs_ekera_params;
+typedef struct {
+    int32_t classification;     /* SHS_CLASS_SUCCESS or SHS_CLASS_FAIL */
+    uint8_t order_match;        /* 0/1, 2 = no known order */
+    uint8_t has_recovered_order, has_offset, pad;
+    uint64_t k[2], r[2];        /* extract_denominator(j) */
+    uint64_t recovered_order;
+    int64_t candidate_offset;   /* the j' = j + offset that factored N */
+    uint32_t n_factors, pad2;
+    uint64_t factors[4];
+} shs_ekera_outcome;
+int shs_ekera_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t N, uint64_t a,
+                          const shs_ekera_params* params, uint64_t seed, uint64_t idx0,
+                          uint64_t known_order, int32_t has_known_order, int32_t device,
+                          shs_ekera_outcome* out);
+
 /* thread-local message of the last failing call */
 const char* shs_last_error(void);
 /* library build string (arch, flags) */

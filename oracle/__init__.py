@@ -287,9 +287,12 @@ class Reference:
         L.ref_shor_standard_procedure.argtypes = [u64, u64, C.c_uint, u64, u64, u64, C.c_int,
                                                   C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)]
         L.ref_multiplicative_order.argtypes = [u64, u64, u64, u64, C.POINTER(u64)]
+        L.ref_ekera_postprocess.argtypes = [u64, u64, C.c_uint, u64, u64, u64, u64, C.c_uint,
+                                            C.c_uint, C.c_uint, C.c_uint, u64, u32, u64, C.c_int,
+                                            C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)]
         L.ref_run_problem.argtypes = [u64, u64, u64, u64, C.c_uint, C.c_uint, u64, C.c_uint,
                                       C.c_int, dbl, dbl, dbl, dbl, C.c_int, C.c_uint,
-                                      C.POINTER(u64), C.POINTER(u64), C.c_uint]
+                                      C.POINTER(u64), C.POINTER(u64), C.c_uint, C.c_int]
 
     def philox(self, key, ctr):
         out = (u32 * 4)()
@@ -339,19 +342,35 @@ class Reference:
                 "k": kr[0] | (kr[1] << 64), "r": kr[2] | (kr[3] << 64),
                 "factors": list(f[:ints[5]])}
 
+    def ekera_postprocess(self, j, t, N, a, params, seed, idx, known_order=None):
+        """proj/src/postprocess.cpp:138-171 with RngStream(seed, idx, 1, postprocess);
+        params = (B, c, k, varsigma, m, ell)."""
+        ints, us, f = (i32 * 5)(), (u64 * 6)(), (u64 * 4)()
+        B, c, k, vs, m, ell = params
+        _check(self.lib.ref_ekera_postprocess(j & (2**64 - 1), j >> 64, t, N, a, B, c, k, vs, m,
+                                              ell, seed, idx, known_order or 0,
+                                              0 if known_order is None else 1, ints, us, f),
+               self.lib)
+        off = us[5] - (1 << 64) if us[5] >= (1 << 63) else us[5]
+        return {"classification": ints[0], "order_match": ints[1],
+                "recovered_order": us[4] if ints[2] else None,
+                "candidate_offset": off if ints[3] else None,
+                "k": us[0] | (us[1] << 64), "r": us[2] | (us[3] << 64),
+                "factors": list(f[:ints[4]])}
+
     def multiplicative_order(self, a, N, p=0, q=0):
         out = u64()
         _check(self.lib.ref_multiplicative_order(a, N, p, q, C.byref(out)), self.lib)
         return out.value
 
-    def run_problem(self, N, a, p, q, L, t, seed, M, err=None, qubit_ceiling=26):
+    def run_problem(self, N, a, p, q, L, t, seed, M, err=None, qubit_ceiling=26, post_mode="shor"):
         """run_problem (proj/src/harness.cpp:109-148) on the reference engine."""
         err = err or make_error()
         counts, cap = (u64 * 13)(), 256
         recip = (u64 * (2 * cap))()
         _check(self.lib.ref_run_problem(N, a, p, q, L, t, seed, M, err.kind, err.delta, err.px,
                                         err.py, err.pz, err.has_pauli, qubit_ceiling, counts,
-                                        recip, cap), self.lib)
+                                        recip, cap, 1 if post_mode == "ekera" else 0), self.lib)
         keys = ["order", "success", "lucky_ne", "lucky_no", "lucky_oo", "fail",
                 "first_factor_index", "first_order_index", "r_overflow", "r_other",
                 "r_total_lucky", "order_solvable"]

@@ -11,6 +11,7 @@
 //   philox::block               proj/include/shorsim/rng.hpp:16-31
 //   shor_standard_procedure     proj/src/postprocess.cpp:55-89
 //   run_problem                 proj/src/harness.cpp:109-148
+//   ekera_postprocess           proj/src/postprocess.cpp:138-171
 //   multiplicative_order        proj/src/numtheory.cpp:207-234
 // Nothing here re-implements reference logic; it only marshals arguments.
 #include <chrono>
@@ -321,7 +322,7 @@ int ref_multiplicative_order(uint64_t a, uint64_t N, uint64_t p, uint64_t q, uin
 int ref_run_problem(uint64_t N, uint64_t a, uint64_t p, uint64_t q, unsigned L, unsigned t,
                     uint64_t seed, unsigned M, int kind, double delta, double px, double py,
                     double pz, int has_pauli, unsigned qubit_ceiling, uint64_t counts[13],
-                    uint64_t* recip, unsigned cap) {
+                    uint64_t* recip, unsigned cap, int post_ekera) {
     return guarded([&] {
         FactoringProblem prob = make_problem(N, a, L, t);
         prob.p = p;
@@ -331,6 +332,7 @@ int ref_run_problem(uint64_t N, uint64_t a, uint64_t p, uint64_t q, unsigned L, 
         spec.M = M;
         spec.error = make_error(kind, delta, px, py, pz, has_pauli);
         spec.sim.qubit_ceiling = qubit_ceiling;
+        spec.post_mode = post_ekera ? PostMode::ekera : PostMode::shor;
         ProblemResult r = run_problem(prob, spec);
         counts[0] = r.order;
         counts[1] = r.success;
@@ -352,6 +354,42 @@ int ref_run_problem(uint64_t N, uint64_t a, uint64_t p, uint64_t q, unsigned L, 
             recip[2 * i + 1] = c;
             ++i;
         }
+    });
+}
+
+// ekera_postprocess with RngStream(seed, idx, 1, postprocess) as run_problem uses it:
+// ints = {classification, order_match (0/1, 2 = none), has_recovered_order,
+// has_offset, n_factors}; u64s = {k_lo, k_hi, r_lo, r_hi, recovered_order,
+// offset (two's complement)}; factors[4].
+int ref_ekera_postprocess(uint64_t j_lo, uint64_t j_hi, unsigned t, uint64_t N, uint64_t a,
+                          uint64_t B, uint64_t c, unsigned k, unsigned varsigma, unsigned m,
+                          unsigned ell, uint64_t seed, uint32_t idx, uint64_t known_order,
+                          int has_order, int32_t ints[5], uint64_t u64s[6], uint64_t factors[4]) {
+    return guarded([&] {
+        u128 j = (u128{j_hi} << 64) | j_lo;
+        EkeraParams prm;
+        prm.B = B;
+        prm.c = c;
+        prm.k = k;
+        prm.varsigma = varsigma;
+        prm.m = m;
+        prm.ell = ell;
+        RngStream rng(seed, idx, 1, RngDomain::postprocess);
+        std::optional<u64> ko;
+        if (has_order) ko = known_order;
+        PostProcessOutcome o = ekera_postprocess(j, t, N, a, prm, rng, ko);
+        ints[0] = static_cast<int32_t>(o.classification);
+        ints[1] = o.order_match ? (*o.order_match ? 1 : 0) : 2;
+        ints[2] = o.recovered_order ? 1 : 0;
+        ints[3] = o.candidate_offset ? 1 : 0;
+        ints[4] = static_cast<int32_t>(o.factors.size());
+        u64s[0] = static_cast<uint64_t>(o.convergent.k);
+        u64s[1] = static_cast<uint64_t>(o.convergent.k >> 64);
+        u64s[2] = static_cast<uint64_t>(o.convergent.r);
+        u64s[3] = static_cast<uint64_t>(o.convergent.r >> 64);
+        u64s[4] = o.recovered_order ? *o.recovered_order : 0;
+        u64s[5] = o.candidate_offset ? static_cast<uint64_t>(static_cast<int64_t>(*o.candidate_offset)) : 0;
+        for (size_t i = 0; i < 4; ++i) factors[i] = i < o.factors.size() ? o.factors[i] : 0;
     });
 }
 

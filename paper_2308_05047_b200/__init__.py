@@ -32,6 +32,10 @@ from .engine import (  # noqa: F401
 )
 from .postprocess import (  # noqa: F401
     Classification,
+    EkeraOutcome,
+    EkeraParams,
+    ekera_postprocess,
+    ekera_postprocess_array,
     PostProcessOutcome,
     ProblemResult,
     multiplicative_order,

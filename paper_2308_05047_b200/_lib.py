@@ -112,6 +112,8 @@ SIGNATURES = [
     ("shs_engine_sparse_stages", u32, [C.c_void_p]),
     ("shs_shor_postprocess", C.c_int, [C.POINTER(u64), u32, u32, u64, u64, u64, i32, i32,
                                        C.c_void_p]),
+    ("shs_ekera_postprocess", C.c_int, [C.POINTER(u64), u32, u32, u64, u64, C.c_void_p, u64,
+                                        u64, u64, i32, i32, C.c_void_p]),
     ("shs_last_error", C.c_char_p, []),
     ("shs_build_info", C.c_char_p, []),
 ]

@@ -17,6 +17,7 @@
 
 #include "../../include/shorsim_b200.h"
 #include "host_model.hpp"
+#include "measure.cuh"
 
 using namespace shs;
 
@@ -136,6 +137,299 @@ __global__ void k_shor_postprocess(const uint64_t* __restrict__ j, uint32_t coun
     out[i] = o;
 }
 
+// ------------------------------------------------------------ Ekerå
+// ekera_postprocess (postprocess.cpp:138-171) per bit string: the ±B sweep of
+// j' = j + offset, each through extract_denominator, recover_order (the
+// smooth lift, postprocess.cpp:102-134) and factor_from_order
+// (postprocess.cpp:136-164) with the shot's RngStream (seed, m, 1, postprocess).
+//
+// recover_order returns ord(a) exactly when a^R = 1 for R = r * prod_{q <= cm}
+// q^floor(log_q 2^m) (every prime of R is stripped, in any order), else
+// nothing; here R is kept as an exponent vector over its primes (the q <= cm
+// and the primes of r, found by Miller-Rabin with the 12 bases that are exact
+// for 64-bit n, and Brent's rho), a^R by successive powering and ord(a) by
+// per-prime valuation: no big integers, the same result.
+
+__device__ uint64_t pp_mod_pow_u(uint64_t b, uint64_t e, uint64_t n) { return pp_mod_pow(b, e, n); }
+
+__device__ bool pp_mr_witness(uint64_t n, uint64_t a, uint64_t d, unsigned s) {
+    uint64_t x = pp_mod_pow(a % n, d, n);
+    if (x == 1 || x == n - 1) return false;
+    for (unsigned i = 1; i < s; ++i) {
+        x = pp_mulmod(x, x, n);
+        if (x == n - 1) return false;
+    }
+    return true;
+}
+
+__device__ bool pp_is_prime(uint64_t n) {  // is_probable_prime, numtheory.cpp:95-116
+    if (n < 2) return false;
+    const uint64_t bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    for (uint64_t p : bases) {
+        if (n == p) return true;
+        if (n % p == 0) return false;
+    }
+    uint64_t d = n - 1;
+    unsigned s = 0;
+    while ((d & 1) == 0) {
+        d >>= 1;
+        ++s;
+    }
+    for (uint64_t a : bases)
+        if (pp_mr_witness(n, a, d, s)) return false;
+    return true;
+}
+
+__device__ uint64_t pp_rho(uint64_t n) {  // a nontrivial divisor of composite n (Brent)
+    if ((n & 1) == 0) return 2;
+    for (uint64_t c = 1;; ++c) {
+        uint64_t x = 2, y = 2, d = 1, q = 1, ys = 2, r = 1;
+        auto step = [&](uint64_t v) { return (pp_mulmod(v, v, n) + c) % n; };
+        while (d == 1) {
+            x = y;
+            for (uint64_t i = 0; i < r; ++i) y = step(y);
+            for (uint64_t k = 0; k < r && d == 1; k += 64) {
+                ys = y;
+                const uint64_t lim = r - k < 64 ? r - k : 64;
+                for (uint64_t i = 0; i < lim; ++i) {
+                    y = step(y);
+                    q = pp_mulmod(q, x > y ? x - y : y - x, n);
+                }
+                d = pp_gcd(q, n);
+            }
+            r *= 2;
+        }
+        if (d == n) {
+            d = 1;
+            while (d == 1) {
+                ys = step(ys);
+                d = pp_gcd(x > ys ? x - ys : ys - x, n);
+            }
+        }
+        if (d != n) return d;
+    }
+}
+
+constexpr int kMaxPrimes = 32;
+
+// distinct primes of n (unsorted) appended to p[*np]
+__device__ void pp_prime_factors(uint64_t n, uint64_t* p, int* np) {
+    uint64_t stack[64];
+    int top = 0;
+    for (uint64_t q = 2; q < 100 && q * q <= n; ++q) {
+        if (n % q) continue;
+        p[(*np)++] = q;
+        while (n % q == 0) n /= q;
+    }
+    if (n > 1) stack[top++] = n;
+    while (top) {
+        const uint64_t m = stack[--top];
+        if (m == 1) continue;
+        if (pp_is_prime(m)) {
+            bool seen = false;
+            for (int i = 0; i < *np; ++i) seen |= p[i] == m;
+            if (!seen && *np < kMaxPrimes) p[(*np)++] = m;
+            continue;
+        }
+        const uint64_t d = pp_rho(m);
+        stack[top++] = d;
+        stack[top++] = m / d;
+    }
+}
+
+// recover_order: ord(a) when a^R = 1, else 0
+__device__ uint64_t pp_recover_order(uint64_t r, uint64_t a, uint64_t N, uint64_t c, uint64_t m) {
+    if (r == 0) r = 1;
+    uint64_t pr[kMaxPrimes], ex[kMaxPrimes];
+    int np = 0;
+    const uint64_t cm = c * m;
+    const unsigned __int128 cap = static_cast<unsigned __int128>(1) << m;
+    for (uint64_t q = 2; q <= cm; ++q) {  // primes <= cm: their lift exponent
+        bool prime = true;
+        for (uint64_t d = 2; d * d <= q; ++d) prime &= (q % d) != 0;
+        if (!prime) continue;
+        unsigned __int128 pw = q;
+        uint64_t e = 1;
+        while (pw * q <= cap) {
+            pw *= q;
+            ++e;
+        }
+        pr[np] = q;
+        ex[np] = e;
+        ++np;
+    }
+    const int nlift = np;
+    uint64_t rp[kMaxPrimes];
+    int nr = 0;
+    pp_prime_factors(r, rp, &nr);
+    for (int i = 0; i < nr; ++i) {
+        uint64_t v = 0, x = r;
+        while (x % rp[i] == 0) {
+            x /= rp[i];
+            ++v;
+        }
+        int at = -1;
+        for (int k = 0; k < nlift; ++k)
+            if (pr[k] == rp[i]) at = k;
+        if (at >= 0) {
+            ex[at] += v;
+        } else if (np < kMaxPrimes) {
+            pr[np] = rp[i];
+            ex[np] = v;
+            ++np;
+        }
+    }
+    auto pow_all = [&](int skip) {  // a^(R / q_skip^e_skip)
+        uint64_t x = a % N;
+        for (int k = 0; k < np; ++k) {
+            if (k == skip) continue;
+            for (uint64_t e = 0; e < ex[k]; ++e) x = pp_mod_pow(x, pr[k], N);
+        }
+        return x;
+    };
+    if (pow_all(-1) != 1) return 0;
+    uint64_t ord = 1;
+    for (int k = 0; k < np; ++k) {  // v_q(ord): smallest f with y^(q^f) = 1
+        uint64_t y = pow_all(k), f = 0;
+        while (y != 1) {
+            y = pp_mod_pow(y, pr[k], N);
+            ++f;
+        }
+        for (uint64_t i = 0; i < f; ++i) ord *= pr[k];
+    }
+    return ord;
+}
+
+struct PostRng {  // RngStream(seed, m, 1, postprocess), rng.hpp:52-83
+    uint64_t seed;
+    uint32_t a, b, index;
+    __device__ uint64_t next() {
+        uint32_t cc[4] = {index++, a, b, 5u};
+        philox_dev(seed, cc);
+        return (uint64_t(cc[0]) << 32) | cc[1];
+    }
+    __device__ uint64_t below(uint64_t n) {
+        const uint64_t limit = ~uint64_t(0) - ~uint64_t(0) % n;
+        uint64_t x;
+        do {
+            x = next();
+        } while (x >= limit);
+        return x % n;
+    }
+};
+
+__device__ void pp_sort(Factors& f) {
+    for (uint32_t u = 1; u < f.n; ++u)
+        for (uint32_t v = u; v > 0 && f.v[v - 1] > f.v[v]; --v) {
+            const uint64_t tmp = f.v[v];
+            f.v[v] = f.v[v - 1];
+            f.v[v - 1] = tmp;
+        }
+}
+
+// factor_from_order (postprocess.cpp:136-164)
+__device__ void pp_factor_from_order(uint64_t N, uint64_t order, PostRng& rng, uint32_t k_trials,
+                                     uint32_t varsigma, Factors& f) {
+    f.n = 0;
+    uint64_t odd = order;
+    unsigned d2 = 0;
+    while ((odd & 1) == 0) {
+        odd >>= 1;
+        ++d2;
+    }
+    const unsigned levels = d2 + 1 + (varsigma > 1 ? varsigma : 1);
+    for (uint32_t trial = 0; trial < k_trials; ++trial) {
+        const uint64_t x = 2 + rng.below(N - 2);
+        const uint64_t g = pp_gcd(x, N);
+        if (g != 1) {
+            add_nontrivial_factor(f, g, N);
+            pp_sort(f);
+            return;
+        }
+        uint64_t y = pp_mod_pow(x, odd, N);
+        for (unsigned level = 0; level < levels; ++level) {
+            if (y == 1) break;
+            add_nontrivial_factor(f, pp_gcd((y + N - 1) % N, N), N);
+            add_nontrivial_factor(f, pp_gcd((y + 1) % N, N), N);
+            if (f.n) {
+                pp_sort(f);
+                return;
+            }
+            y = pp_mulmod(y, y, N);
+        }
+    }
+}
+
+__device__ void pp_extract(u128d jj, uint32_t t, uint64_t N, u128d& bk, u128d& br) {
+    bk = 0;
+    br = 1;
+    if (jj == 0) return;
+    u128d p2 = 1, q2 = 0, p1 = 0, q1 = 1;
+    u128d num = u128d(1) << t, den = jj;
+    while (den != 0) {
+        const u128d aq = num / den, rem = num % den;
+        const u128d p = aq * p1 + p2, q = aq * q1 + q2;
+        if (q >= u128d(N)) break;
+        bk = p;
+        br = q;
+        p2 = p1;
+        p1 = p;
+        q2 = q1;
+        q1 = q;
+        num = den;
+        den = rem;
+    }
+}
+
+__global__ void k_ekera_postprocess(const uint64_t* __restrict__ j, uint32_t count, uint32_t t,
+                                    uint64_t N, uint64_t a, shs_ekera_params prm, uint64_t seed,
+                                    uint64_t idx0, uint64_t order, int has_order,
+                                    shs_ekera_outcome* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const u128d jj = (u128d(j[2 * i + 1]) << 64) | j[2 * i];
+    shs_ekera_outcome o{};
+    u128d bk, br;
+    pp_extract(jj, t, N, bk, br);
+    o.k[0] = static_cast<uint64_t>(bk);
+    o.k[1] = static_cast<uint64_t>(bk >> 64);
+    o.r[0] = static_cast<uint64_t>(br);
+    o.r[1] = static_cast<uint64_t>(br >> 64);
+    o.classification = SHS_CLASS_FAIL;
+    PostRng rng{seed, static_cast<uint32_t>(idx0 + i), 1u, 0u};
+    const u128d mask = t >= 128 ? ~u128d(0) : ((u128d(1) << t) - 1);
+    uint64_t rec = 0;
+    for (uint64_t step = 0; step <= prm.B; ++step) {
+        for (int sgn = -1; sgn <= 1; sgn += 2) {
+            if (step == 0 && sgn == 1) continue;  // offset 0 once
+            const u128d jp = (sgn < 0 ? jj - u128d(step) : jj + u128d(step)) & mask;
+            u128d ck, cr;
+            pp_extract(jp, t, N, ck, cr);
+            const uint64_t ordr = pp_recover_order(static_cast<uint64_t>(cr), a, N, prm.c, prm.m);
+            if (!ordr) continue;
+            if (!rec) rec = ordr;
+            Factors f{{0, 0, 0, 0}, 0};
+            pp_factor_from_order(N, ordr, rng, prm.k, prm.varsigma, f);
+            if (f.n) {
+                o.n_factors = f.n;
+                for (uint32_t u = 0; u < 4; ++u) o.factors[u] = u < f.n ? f.v[u] : 0;
+                o.has_recovered_order = 1;
+                o.recovered_order = ordr;
+                o.has_offset = 1;
+                o.candidate_offset = sgn < 0 ? -static_cast<int64_t>(step) : static_cast<int64_t>(step);
+                o.classification = SHS_CLASS_SUCCESS;
+                o.order_match = has_order ? (ordr == order ? 1 : 0) : 2;
+                out[i] = o;
+                return;
+            }
+        }
+    }
+    o.has_recovered_order = rec ? 1 : 0;
+    o.recovered_order = rec;
+    o.order_match = has_order ? ((rec && rec == order) ? 1 : 0) : 2;
+    out[i] = o;
+}
+
 }  // namespace
 
 extern "C" int shs_shor_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t N,
@@ -167,6 +461,46 @@ extern "C" int shs_shor_postprocess(const uint64_t* j, uint32_t count, uint32_t 
         dj, count, t, N, a, known_order, has_known_order ? 1 : 0, dout);
     if ((ce = cudaGetLastError()) != cudaSuccess) return fail(ce);
     if ((ce = cudaMemcpy(out, dout, sizeof(shs_shor_outcome) * count, cudaMemcpyDeviceToHost)) !=
+        cudaSuccess)
+        return fail(ce);
+    cudaFree(dj);
+    cudaFree(dout);
+    return SHS_OK;
+}
+
+extern "C" int shs_ekera_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t N,
+                                     uint64_t a, const shs_ekera_params* params, uint64_t seed,
+                                     uint64_t idx0, uint64_t known_order, int32_t has_known_order,
+                                     int32_t device, shs_ekera_outcome* out) {
+    if ((!j || !out || !params) && count) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    if (t >= 128) return set_error(SHS_INVALID_ARGUMENT, "convergents: t must be < 128");
+    if (N < 3) return set_error(SHS_INVALID_ARGUMENT, "modulus must be >= 3");
+    if (params->m > 63) return set_error(SHS_INVALID_ARGUMENT, "recover_order: m <= 63");
+    if (params->k == 0 || params->B > (uint64_t(1) << 20))
+        return set_error(SHS_INVALID_ARGUMENT, "ekera: k >= 1 and B <= 2^20");
+    for (uint32_t i = 0; i < count; ++i)
+        if ((t < 64 && (j[2 * i + 1] != 0 || (j[2 * i] >> t) != 0)) ||
+            (t >= 64 && (j[2 * i + 1] >> (t - 64)) != 0))
+            return set_error(SHS_INVALID_ARGUMENT, "convergents: j >= 2^t");
+    if (!count) return SHS_OK;
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce != cudaSuccess) return set_error(SHS_CUDA_ERROR, cudaGetErrorString(ce));
+    uint64_t* dj = nullptr;
+    shs_ekera_outcome* dout = nullptr;
+    auto fail = [&](cudaError_t e) {
+        cudaFree(dj);
+        cudaFree(dout);
+        return set_error(SHS_CUDA_ERROR, std::string("ekera: ") + cudaGetErrorString(e));
+    };
+    if ((ce = cudaMalloc(&dj, sizeof(uint64_t) * 2 * count)) != cudaSuccess) return fail(ce);
+    if ((ce = cudaMalloc(&dout, sizeof(shs_ekera_outcome) * count)) != cudaSuccess) return fail(ce);
+    if ((ce = cudaMemcpy(dj, j, sizeof(uint64_t) * 2 * count, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(ce);
+    const int threads = 64;
+    k_ekera_postprocess<<<(count + threads - 1) / threads, threads>>>(
+        dj, count, t, N, a, *params, seed, idx0, known_order, has_known_order ? 1 : 0, dout);
+    if ((ce = cudaGetLastError()) != cudaSuccess) return fail(ce);
+    if ((ce = cudaMemcpy(out, dout, sizeof(shs_ekera_outcome) * count, cudaMemcpyDeviceToHost)) !=
         cudaSuccess)
         return fail(ce);
     cudaFree(dj);

@@ -6,6 +6,9 @@ after the path.
   strings on the device (``shs_shor_postprocess``, csrc/postprocess.cu).
 * ``shor_standard_procedure`` — the same for one bit string, returning the
   reference's ``PostProcessOutcome`` fields.
+* ``ekera_postprocess_array`` / ``ekera_postprocess`` — Ekerå's pipeline
+  (postprocess.cpp:92-171: the ±B sweep, smooth-lift order recovery,
+  factoring from the order with the shot's RngStream) on the device.
 * ``multiplicative_order`` — ground-truth order from the known factors
   (numtheory.cpp:207-234), host integer code.
 * ``run_problem`` — ``run_problem`` (proj/src/harness.cpp:109-148, simulator
@@ -80,6 +83,74 @@ def shor_postprocess_array(j: np.ndarray, t: int, N: int, a: int,
                                        known_order or 0, 0 if known_order is None else 1, device,
                                        out.ctypes.data))
     return out
+
+
+@dataclass
+class EkeraParams:  # postprocess.hpp:43-53
+    B: int = 1
+    c: int = 1
+    k: int = 100
+    varsigma: int = 1
+    m: int = 1
+    ell: int = 0
+
+    @staticmethod
+    def for_problem(L: int, t: int) -> "EkeraParams":
+        """(B, c, k, varsigma) = (L, 1, 100, 1), m = L, ell = t - L (postprocess.cpp:92-101)."""
+        return EkeraParams(B=L, c=1, k=100, varsigma=1, m=L, ell=t - L if t > L else 0)
+
+
+class shs_ekera_params(C.Structure):
+    _fields_ = [("B", C.c_uint64), ("c", C.c_uint64), ("k", C.c_uint32),
+                ("varsigma", C.c_uint32), ("m", C.c_uint32), ("ell", C.c_uint32)]
+
+
+EKERA_DTYPE = np.dtype([("classification", np.int32), ("order_match", np.uint8),
+                        ("has_recovered_order", np.uint8), ("has_offset", np.uint8),
+                        ("pad", np.uint8), ("k", np.uint64, 2), ("r", np.uint64, 2),
+                        ("recovered_order", np.uint64), ("candidate_offset", np.int64),
+                        ("n_factors", np.uint32), ("pad2", np.uint32), ("factors", np.uint64, 4)])
+
+
+def ekera_postprocess_array(j: np.ndarray, t: int, N: int, a: int, params: EkeraParams,
+                            seed: int, idx0: int = 0, known_order: Optional[int] = None,
+                            device: int = 0) -> np.ndarray:
+    """ekera_postprocess for every row of j (shot idx0 + row, its RngStream
+    (seed, shot, 1, postprocess) as run_problem builds it), on the device."""
+    j = np.ascontiguousarray(j, dtype=np.uint64).reshape(-1, 2)
+    out = np.zeros(len(j), dtype=EKERA_DTYPE)
+    prm = shs_ekera_params(params.B, params.c, params.k, params.varsigma, params.m, params.ell)
+    _raise(L.load().shs_ekera_postprocess(j.ctypes.data_as(C.POINTER(C.c_uint64)), len(j), t, N,
+                                          a, C.byref(prm), seed, idx0, known_order or 0,
+                                          0 if known_order is None else 1, device,
+                                          out.ctypes.data))
+    return out
+
+
+@dataclass
+class EkeraOutcome(PostProcessOutcome):
+    recovered_order: Optional[int] = None
+    candidate_offset: Optional[int] = None
+
+
+def ekera_outcome_from_record(rec) -> EkeraOutcome:
+    om = int(rec["order_match"])
+    return EkeraOutcome(
+        classification=Classification(int(rec["classification"])),
+        convergent=(int(rec["k"][0]) | (int(rec["k"][1]) << 64),
+                    int(rec["r"][0]) | (int(rec["r"][1]) << 64)),
+        order_match=None if om == 2 else bool(om),
+        factors=[int(x) for x in rec["factors"][:int(rec["n_factors"])]],
+        recovered_order=int(rec["recovered_order"]) if rec["has_recovered_order"] else None,
+        candidate_offset=int(rec["candidate_offset"]) if rec["has_offset"] else None)
+
+
+def ekera_postprocess(j: int, t: int, N: int, a: int, params: EkeraParams, seed: int, idx: int,
+                      known_order: Optional[int] = None, device: int = 0) -> EkeraOutcome:
+    """postprocess.cpp:138-171 for one bit string (on the device)."""
+    arr = np.array([[j & (2**64 - 1), j >> 64]], dtype=np.uint64)
+    return ekera_outcome_from_record(
+        ekera_postprocess_array(arr, t, N, a, params, seed, idx, known_order, device)[0])
 
 
 def outcome_from_record(rec) -> PostProcessOutcome:
@@ -218,11 +289,15 @@ def tally(result: ProblemResult, outcomes: np.ndarray) -> ProblemResult:
 
 def run_problem(problem: FactoringProblem, M: int, error: Optional[ErrorConfig] = None,
                 options: Optional[SimulatorOptions] = None,
-                engine: Optional[IterativeShorEngine] = None) -> ProblemResult:
-    """run_problem (harness.cpp:109-148; simulator backend, Shor mode): shots
-    m = 0 .. M-1 are engine.run(problem.seed, m) — whole runs on the device for
-    small problems — then shor_standard_procedure with the known order on the
-    device, tallied in shot order."""
+                engine: Optional[IterativeShorEngine] = None,
+                post_mode: str = "shor") -> ProblemResult:
+    """run_problem (harness.cpp:109-148; simulator backend): shots m = 0 .. M-1
+    are engine.run(problem.seed, m) — whole runs on the device for small
+    problems — then shor_standard_procedure ("shor") or ekera_postprocess with
+    EkeraParams.for_problem(L, t) and RngStream(seed, m, 1, postprocess)
+    ("ekera"), with the known order, on the device, tallied in shot order."""
+    if post_mode not in ("shor", "ekera"):
+        raise ValueError(f"post_mode must be shor or ekera, not {post_mode!r}")
     if not problem.p or not problem.q:
         raise ValueError("campaign problems need known factors for verification labels")
     res = ProblemResult(problem=problem, M=M)
@@ -235,7 +310,12 @@ def run_problem(problem: FactoringProblem, M: int, error: Optional[ErrorConfig] 
     try:
         j = engine.run_batch_array(problem.seed, 0, M)
         dev = (options or SimulatorOptions()).device
-        outcomes = shor_postprocess_array(j, problem.t, problem.N, problem.a, res.order, dev)
+        if post_mode == "shor":
+            outcomes = shor_postprocess_array(j, problem.t, problem.N, problem.a, res.order, dev)
+        else:
+            outcomes = ekera_postprocess_array(j, problem.t, problem.N, problem.a,
+                                               EkeraParams.for_problem(problem.L, problem.t),
+                                               problem.seed, 0, res.order, dev)
     finally:
         if own:
             engine.close()

@@ -93,3 +93,55 @@ def test_run_problem_with_error_model(cuda_ok, reference):
                                 make_error("classical_measure", 0.05))
     assert (got.success, got.lucky_ne, got.lucky_no, got.lucky_oo, got.fail) == \
         (ref["success"], ref["lucky_ne"], ref["lucky_no"], ref["lucky_oo"], ref["fail"])
+
+
+# ------------------------------------------------------------------ Ekerå
+def ekera_fields(o):
+    return {"classification": int(o.classification),
+            "order_match": 2 if o.order_match is None else int(o.order_match),
+            "recovered_order": o.recovered_order, "candidate_offset": o.candidate_offset,
+            "k": o.convergent[0], "r": o.convergent[1], "factors": o.factors}
+
+
+EKERA_CASES = [(15, 7, 8, (3, 5)), (21, 2, 9, (3, 7)), (35, 3, 11, (5, 7)),
+               (4087, 1001, 24, (61, 67)), (16777207, 2, 48, (4093, 4099)),
+               (4294967213, 5, 64, (57139, 75167))]
+
+
+@pytest.mark.parametrize("N,a,t,pq", EKERA_CASES)
+def test_ekera_matches_reference(cuda_ok, reference, N, a, t, pq):
+    """ekera_postprocess (postprocess.cpp:138-171) with the shot's RngStream:
+    classification, recovered order, winning offset, convergent, factors and
+    order_match identical to the reference for peak, near-peak and random
+    bit strings (for_problem parameters: B = L sweeps +-L around j)."""
+    import paper_2308_05047_b200 as shs
+    from paper_2308_05047_b200.postprocess import ekera_outcome_from_record
+    rng = random.Random(7 * N + t)
+    L = N.bit_length()
+    prm = shs.EkeraParams.for_problem(L, t)
+    order = shs.multiplicative_order(a, N, pq)
+    js = [0, 1, (1 << t) - 1]
+    js += [(k * (1 << t)) // order + d for k in rng.sample(range(order), min(order, 12))
+           for d in (0, 3, -L - 1)]
+    js += [rng.getrandbits(t) for _ in range(24)]
+    js = [j % (1 << t) for j in js]
+    arr = np.array([[j & (2**64 - 1), j >> 64] for j in js], dtype=np.uint64)
+    seed = 4242
+    for ko in (order, None):
+        out = shs.ekera_postprocess_array(arr, t, N, a, prm, seed, 100, ko)
+        for i, (j, rec) in enumerate(zip(js, out)):
+            ref = reference.ekera_postprocess(j, t, N, a, (prm.B, prm.c, prm.k, prm.varsigma,
+                                                            prm.m, prm.ell), seed, 100 + i, ko)
+            assert ekera_fields(ekera_outcome_from_record(rec)) == ref, (j, ko)
+
+
+@pytest.mark.parametrize("N,pq", [(21, (3, 7)), (35, (5, 7))])
+def test_run_problem_ekera_matches_reference(cuda_ok, reference, N, pq):
+    import paper_2308_05047_b200 as shs
+    for i, a in enumerate(_all_bases(N)[:8]):
+        prob = shs.FactoringProblem.make(N, a, p=pq[0], q=pq[1], seed=500 + i)
+        got = shs.run_problem(prob, 256, post_mode="ekera")
+        ref = reference.run_problem(N, a, pq[0], pq[1], prob.L, prob.t, prob.seed, 256,
+                                    post_mode="ekera")
+        assert (got.success, got.fail, got.first_factor_index, got.first_order_index) == \
+            (ref["success"], ref["fail"], ref["first_factor_index"], ref["first_order_index"]), a
