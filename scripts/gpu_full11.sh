@@ -1,0 +1,5 @@
+python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc $?"; tail -3 gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/v11_bench_c4.json 2> gpurun_out/v11_bench_c4.err; echo "bench rc $?"; tail -2 gpurun_out/v11_bench_c4.err
+python scripts/summarize_bench.py gpurun_out/v11_bench_c4.json | cut -c1-500
+python -c "import json;d=json.loads(open('gpurun_out/v11_bench_c4.json').read().strip().splitlines()[-1]);print(json.dumps(d['batched_small_n']['config2_N21_N35'].get('statistics')))"
