@@ -127,9 +127,8 @@ struct shs_engine {
     uint64_t* sZ[2] = {nullptr, nullptr};
     double2* sV[2] = {nullptr, nullptr};
     uint64_t* sKeys = nullptr;
-    uint32_t* sIdx = nullptr;
-    uint32_t* sIdx2 = nullptr;
-    double* sNrm = nullptr;
+    double2* sNrm = nullptr;       // norm pairs in orbit order (sort input)
+    double2* sNrm2 = nullptr;      // ... sorted by z
     void* sTemp = nullptr;
     size_t sTempBytes = 0;
 };
@@ -390,8 +389,8 @@ uint32_t plan_sparse_prefix(const shs_engine* e) {
 
 // Sparse buffers inside the current Y (free until the first dense collapse of a
 // run; carved again at every run start since X / Y swap): Z0 Z1 (u64), V0 V1
-// (double2), sorted keys (u64), idx idx2 (u32), nrm (2 doubles) per support
-// element, then the radix sort's scratch.
+// (double2), sorted keys (u64), norm pairs and their sorted copy (double2) per
+// support element, then the radix sort's scratch.
 int carve_sparse(shs_engine* e) {
     const uint64_t K = uint64_t(1) << e->sparse_n;
     char* p = reinterpret_cast<char*>(e->Y);
@@ -405,12 +404,11 @@ int carve_sparse(shs_engine* e) {
     e->sV[0] = reinterpret_cast<double2*>(take(16 * K));
     e->sV[1] = reinterpret_cast<double2*>(take(16 * K));
     e->sKeys = reinterpret_cast<uint64_t*>(take(8 * K));
-    e->sIdx = reinterpret_cast<uint32_t*>(take(4 * K));
-    e->sIdx2 = reinterpret_cast<uint32_t*>(take(4 * K));
-    e->sNrm = reinterpret_cast<double*>(take(16 * K));
+    e->sNrm = reinterpret_cast<double2*>(take(16 * K));
+    e->sNrm2 = reinterpret_cast<double2*>(take(16 * K));
     if (!e->sTempBytes) {
         SHS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, e->sTempBytes, e->sZ[0], e->sKeys,
-                                                 e->sIdx, e->sIdx2, static_cast<int>(K), 0, 64,
+                                                 e->sNrm, e->sNrm2, static_cast<int>(K), 0, 64,
                                                  e->stream));
     }
     e->sTemp = take(e->sTempBytes);
@@ -618,7 +616,6 @@ SparseParams sparse_params(shs_engine* e, uint32_t s, const DevStage* dev) {
     p.dev = dev;
     p.Zn = e->sZ[(s + 1) & 1];
     p.Vn = e->sV[(s + 1) & 1];
-    p.idx = e->sIdx;
     p.nrm = e->sNrm;
     return p;
 }
@@ -639,11 +636,10 @@ int launch_sparse_probs(shs_engine* e, uint32_t s, const DevStage* dev, int* npa
         if (s == 0) k_sparse_init<<<1, 1, 0, e->stream>>>(e->sZ[0], e->sV[0]);
         k_sparse_expand<<<sparse_grid(e, p.Ko), kSparseThreads, 0, e->stream>>>(p);
         size_t bytes = e->sTempBytes;
-        sort_err = cub::DeviceRadixSort::SortPairs(e->sTemp, bytes, p.Zn, e->sKeys, e->sIdx,
-                                                   e->sIdx2, static_cast<int>(Kn), 0, end_bit,
+        sort_err = cub::DeviceRadixSort::SortPairs(e->sTemp, bytes, p.Zn, e->sKeys, e->sNrm,
+                                                   e->sNrm2, static_cast<int>(Kn), 0, end_bit,
                                                    e->stream);
-        k_sparse_fold<<<gf, kSparseThreads, 0, e->stream>>>(e->sKeys, e->sIdx2, e->sNrm, Kn,
-                                                           e->partials);
+        k_sparse_fold<<<gf, kSparseThreads, 0, e->stream>>>(e->sKeys, e->sNrm2, Kn, e->partials);
     });
     if (rc) return rc;
     if (sort_err != cudaSuccess)

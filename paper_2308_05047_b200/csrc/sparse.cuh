@@ -38,8 +38,7 @@ struct SparseParams {
     const DevStage* dev;  // ... or the device slot (later stages)
     uint64_t* Zn;         // [2 Ko] support after the stage (orbit order)
     double2* Vn;          // [2 Ko] collapse output
-    uint32_t* idx;        // [2 Ko] 0 .. 2 Ko - 1 (sort payload)
-    double* nrm;          // [2][2 Ko] |h0|^2, |h1|^2 per new index
+    double2* nrm;         // [2 Ko] (|h0|^2, |h1|^2) per new index (the sort payload)
 };
 
 __device__ __forceinline__ StageScalars sparse_scalars(const SparseParams& p) {
@@ -55,30 +54,26 @@ static __global__ void k_sparse_init(uint64_t* Z, double2* V) {
 // probs side: the new support (orbit order), the sort payload and both norms
 static __global__ void __launch_bounds__(kSparseThreads) k_sparse_expand(SparseParams p) {
     const StageScalars sc = sparse_scalars(p);
-    const uint64_t Kn = 2 * p.Ko;
     for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < p.Ko;
          k += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t z0 = p.Zo[k];
         const double2 v = p.Vo[k], zero = make_double2(0.0, 0.0);
         double h0r, h0i, h1r, h1i;
         stage_pair(sc, v, zero, h0r, h0i, h1r, h1i);  // z0: direct term only
-        p.nrm[2 * k] = cnorm(h0r, h0i);
-        p.nrm[Kn + 2 * k] = cnorm(h1r, h1i);
+        p.nrm[2 * k] = make_double2(cnorm(h0r, h0i), cnorm(h1r, h1i));
         stage_pair(sc, zero, v, h0r, h0i, h1r, h1i);  // A z0: gathered term only
-        p.nrm[2 * k + 1] = cnorm(h0r, h0i);
-        p.nrm[Kn + 2 * k + 1] = cnorm(h1r, h1i);
+        p.nrm[2 * k + 1] = make_double2(cnorm(h0r, h0i), cnorm(h1r, h1i));
         p.Zn[2 * k] = z0;
         p.Zn[2 * k + 1] = mulmod_shoup(z0, p.A, p.A_sh, p.N);
-        p.idx[2 * k] = static_cast<uint32_t>(2 * k);
-        p.idx[2 * k + 1] = static_cast<uint32_t>(2 * k + 1);
     }
 }
 
-// Block partials over the z-sorted support: the first element of every
-// 256-block run folds the run in order (0.0 + x + ...); exact per-CTA digits.
+// Block partials over the z-sorted support (norm pairs sorted along): the
+// first element of every 256-block run folds the run in order (0.0 + x + ...);
+// exact per-CTA digits.
 static __global__ void __launch_bounds__(kSparseThreads)
-    k_sparse_fold(const uint64_t* __restrict__ zs, const uint32_t* __restrict__ order,
-                  const double* __restrict__ nrm, uint64_t Kn, unsigned long long* partials) {
+    k_sparse_fold(const uint64_t* __restrict__ zs, const double2* __restrict__ nrm, uint64_t Kn,
+                  unsigned long long* partials) {
     __shared__ unsigned long long digits[2][kDigits];
     const int tid = threadIdx.x;
     for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&digits[0][0])[i] = 0ull;
@@ -92,9 +87,9 @@ static __global__ void __launch_bounds__(kSparseThreads)
         if (i > 0 && (zs[i - 1] >> 8) == b) continue;  // not the first of its block
         double s0 = 0.0, s1 = 0.0;
         for (uint64_t j = i; j < Kn && (zs[j] >> 8) == b; ++j) {
-            const uint32_t q = order[j];
-            s0 = __dadd_rn(s0, nrm[q]);
-            s1 = __dadd_rn(s1, nrm[Kn + q]);
+            const double2 n = nrm[j];
+            s0 = __dadd_rn(s0, n.x);
+            s1 = __dadd_rn(s1, n.y);
         }
         window_add(w0, s0, digits[0]);
         window_add(w1, s1, digits[1]);
