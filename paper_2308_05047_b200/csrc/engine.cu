@@ -496,6 +496,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
             }
             k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
+        e->launches++;  // k_tiled + k_tile_fixup: two kernels in one launch group
         *nparts = g1 + g2;
     } else if (e->e1) {
         // stage 0 from the implicit e_1: two live amplitudes (k_stage_probs_e1)
