@@ -124,14 +124,17 @@ int shs_engine_run(shs_engine* engine, uint64_t seed, uint64_t bitstring_index, 
 
 /* count consecutive runs idx0 .. idx0+count-1; j receives 2*count words. Small
  * problems (N <= 4096, t <= 20: configs 1-2) run whole runs on the device, one
- * CTA per run (batch.cuh); larger ones run stage by stage. Identical results. */
+ * CTA per run (batch.cuh); mid-size ones (N <= 2^22) advance the shots stage by
+ * stage together (lockstep.cuh); larger ones run one after another. Identical
+ * results. */
 int shs_engine_run_batch(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
                          uint64_t* j);
 /* as run_batch, with optional per-run outputs (NULL to skip): j_sampled [2*count],
  * p1 [count*t], bits [count*t*4] = sampled, observed, classical_flip, error_branch */
 int shs_engine_run_many(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,
                         uint64_t* j, uint64_t* j_sampled, double* p1, int32_t* bits);
-/* 1 when run_batch / run_many use the whole-run device kernel for this problem */
+/* 1 when run_batch / run_many use the whole-run device kernel for this problem,
+ * 2 when they advance the shots in lockstep, 0 otherwise */
 int shs_engine_batched(const shs_engine* engine);
 /* the same runs forced through the per-stage path (for comparisons) */
 int shs_engine_run_sequential(shs_engine* engine, uint64_t seed, uint64_t idx0, uint32_t count,

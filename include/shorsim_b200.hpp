@@ -83,7 +83,8 @@ public:
         a_pows_.resize(t_);
         throw_status(shs_engine_stage_multipliers(h_, a_pows_.data()));
         trace_.resize(t_);
-        batched_ = shs_engine_batched(h_) != 0;
+        batch_mode_ = shs_engine_batched(h_);
+        batched_ = batch_mode_ != 0;
     }
     ~IterativeShorEngine() {
         if (h_) shs_engine_destroy(h_);
@@ -92,15 +93,18 @@ public:
     IterativeShorEngine& operator=(const IterativeShorEngine&) = delete;
     IterativeShorEngine(IterativeShorEngine&& o) noexcept
         : h_(std::exchange(o.h_, nullptr)), t_(o.t_), a_pows_(std::move(o.a_pows_)),
-          trace_(std::move(o.trace_)), batched_(o.batched_), cache_seed_(o.cache_seed_),
+          trace_(std::move(o.trace_)), batched_(o.batched_), batch_mode_(o.batch_mode_),
+          next_fetch_(o.next_fetch_), cache_seed_(o.cache_seed_),
           cache_lo_(o.cache_lo_), cache_n_(o.cache_n_), c_j_(std::move(o.c_j_)),
           c_js_(std::move(o.c_js_)), c_p1_(std::move(o.c_p1_)), c_bits_(std::move(o.c_bits_)) {}
 
     // IterativeShorEngine::run, statevector.cpp:323-412. A run is a pure function
-    // of (seed, bitstring_index), so for problems the whole-run device kernel
-    // covers (shs_engine_batched) a miss fetches the next kPrefetch indices in
-    // one launch — the reference's shot loops (run_problem, simulate_to_jsonl)
-    // call run(seed, m) for consecutive m — and later calls are served from it.
+    // of (seed, bitstring_index), so for problems the batched paths cover
+    // (shs_engine_batched: 1 = whole runs per CTA, N <= 4096; 2 = lockstep
+    // shots, mid-size N) a miss fetches the next indices in one call — the
+    // reference's shot loops (run_problem, simulate_to_jsonl) call run(seed, m)
+    // for consecutive m — and later calls are served from it. Lockstep fetches
+    // start at 256 shots (a campaign's M) and double on consecutive misses.
     RunResult run(u64 seed, u64 bitstring_index) {
         if (batched_) {
             bool hit = cache_seed_ == seed && bitstring_index >= cache_lo_ &&
@@ -134,19 +138,27 @@ public:
     shs_engine* handle() const { return h_; }
 
 private:
-    static constexpr std::uint32_t kPrefetch = 4096;
+    static constexpr std::uint32_t kPrefetch = 4096;      // whole-run batches
+    static constexpr std::uint32_t kLockFirst = 256;      // lockstep: first fetch ...
+    static constexpr std::uint32_t kLockMax = 4096;       // ... doubling up to this
 
     void prefetch(u64 seed, u64 idx0) {
-        c_j_.resize(2 * kPrefetch);
-        c_js_.resize(2 * kPrefetch);
-        c_p1_.resize(std::size_t(kPrefetch) * t_);
-        c_bits_.resize(std::size_t(kPrefetch) * t_ * 4);
+        std::uint32_t n = kPrefetch;
+        if (batch_mode_ == 2) {
+            const bool next = cache_n_ && cache_seed_ == seed && idx0 == cache_lo_ + cache_n_;
+            next_fetch_ = next ? std::min(2 * next_fetch_, kLockMax) : kLockFirst;
+            n = next_fetch_;
+        }
+        c_j_.resize(2 * std::size_t(n));
+        c_js_.resize(2 * std::size_t(n));
+        c_p1_.resize(std::size_t(n) * t_);
+        c_bits_.resize(std::size_t(n) * t_ * 4);
         cache_n_ = 0;
-        throw_status(shs_engine_run_many(h_, seed, idx0, kPrefetch, c_j_.data(), c_js_.data(),
+        throw_status(shs_engine_run_many(h_, seed, idx0, n, c_j_.data(), c_js_.data(),
                                          c_p1_.data(), c_bits_.data()));
         cache_seed_ = seed;
         cache_lo_ = idx0;
-        cache_n_ = kPrefetch;
+        cache_n_ = n;
     }
 
     RunResult unpack(u64 k) const {
@@ -167,6 +179,8 @@ private:
     std::vector<u64> a_pows_;
     std::vector<shs_stage_trace> trace_;
     bool batched_ = false;
+    int batch_mode_ = 0;
+    std::uint32_t next_fetch_ = 0;
     u64 cache_seed_ = 0, cache_lo_ = 0, cache_n_ = 0;
     std::vector<std::uint64_t> c_j_, c_js_;
     std::vector<double> c_p1_;

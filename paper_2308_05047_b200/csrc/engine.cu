@@ -39,6 +39,7 @@
 #include "tiled.cuh"
 #include "batch.cuh"
 #include "sparse.cuh"
+#include "lockstep.cuh"
 
 using namespace shs;
 
@@ -120,6 +121,7 @@ struct shs_engine {
     StageRec* d_rec = nullptr;     // its device alias
     cudaEvent_t meas_ev[2] = {nullptr, nullptr};
     bool host_measure = false;     // SHS_HOST_MEASURE=1: the host-driven loop (A/B)
+    bool lockstep = true;          // SHS_LOCKSTEP=0: run_many runs shot by shot (A/B)
     // sparse prefix of device-resident runs (sparse.cuh): stages 0 .. sparse_n-1
     // on the support, carved out of Y (unused until the first dense stage)
     uint32_t sparse_n = 0;
@@ -876,6 +878,190 @@ int ensure_batch_tables(shs_engine* e) {
 }
 
 // `count` whole runs idx0 .. idx0+count-1 in one launch (one CTA per run).
+// Lockstep multi-shot runs (lockstep.cuh) for mid-size N: up to `cap` shots at
+// a time advance stage by stage together; the host stays one stage behind,
+// computing both candidate phases of every shot's next stage with glibc.
+constexpr uint64_t kLockMaxN = uint64_t(1) << 22;           // beyond: engine_run per shot
+constexpr uint64_t kLockBudget = uint64_t(16) << 30;         // HBM for the batch's states
+
+bool lockstep_ok(const shs_engine* e, uint32_t count) {
+    return count >= 2 && !batchable(e) && e->N <= kLockMaxN;
+}
+
+int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_t* j,
+                      uint64_t* js, double* p1, int32_t* bits) {
+    const uint64_t N = e->N, nb = e->nb, t = e->t;
+    const uint64_t per_shot = 2 * sizeof(double2) * N + 2 * sizeof(double) * nb;
+    const uint32_t B = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(count, kLockBudget / per_shot)));
+    const int G = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(e->nchunks, (4 * uint64_t(e->num_sms) + B - 1) / B)));
+    double2 *X = nullptr, *Y = nullptr;
+    double* S = nullptr;
+    unsigned long long* parts = nullptr;
+    DevStage* slots = nullptr;
+    NextPhase* d_nph = nullptr;
+    NextPhase* h_nph = nullptr;
+    StageRec* h_rec = nullptr;
+    StageRec* d_rec = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    auto cleanup = [&] {
+        cudaStreamSynchronize(e->stream);
+        cudaFree(X);
+        cudaFree(Y);
+        cudaFree(S);
+        cudaFree(parts);
+        cudaFree(slots);
+        cudaFree(d_nph);
+        if (h_nph) cudaFreeHost(h_nph);
+        if (h_rec) cudaFreeHost(h_rec);
+        for (auto v : ev)
+            if (v) cudaEventDestroy(v);
+    };
+    auto cuda_fail = [&](cudaError_t ce, const char* what) {
+        cleanup();
+        return set_error(SHS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(ce));
+    };
+    cudaError_t ce;
+    if ((ce = cudaMalloc(&X, sizeof(double2) * N * B)) != cudaSuccess ||
+        (ce = cudaMalloc(&Y, sizeof(double2) * N * B)) != cudaSuccess ||
+        (ce = cudaMalloc(&S, sizeof(double) * 2 * nb * B)) != cudaSuccess ||
+        (ce = cudaMalloc(&parts, sizeof(unsigned long long) * 2 * kDigits * G * B)) != cudaSuccess ||
+        (ce = cudaMalloc(&slots, sizeof(DevStage) * 2 * B)) != cudaSuccess ||
+        (ce = cudaMalloc(&d_nph, sizeof(NextPhase) * 2 * B)) != cudaSuccess ||
+        (ce = cudaHostAlloc(&h_nph, sizeof(NextPhase) * 2 * B, cudaHostAllocDefault)) != cudaSuccess ||
+        (ce = cudaHostAlloc(&h_rec, sizeof(StageRec) * t * B, cudaHostAllocMapped)) != cudaSuccess ||
+        (ce = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_rec), h_rec, 0)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(ce, "lockstep buffers");
+    std::vector<u128> observed(B), sampled(B);
+    for (uint32_t b0 = 0; b0 < count; b0 += B) {
+        const uint32_t nbat = std::min<uint32_t>(B, count - b0);
+        std::memset(h_rec, 0, sizeof(StageRec) * t * B);
+        std::fill(observed.begin(), observed.end(), u128{0});
+        std::fill(sampled.begin(), sampled.end(), u128{0});
+        LockParams lp{};
+        lp.X = X;
+        lp.Y = Y;
+        lp.N = N;
+        lp.nb = nb;
+        lp.nchunks = e->nchunks;
+        lp.sc0 = host_scalars(e, 0, 0, 1.0);
+        lp.slots = slots;
+        lp.S = S;
+        lp.partials = parts;
+        const dim3 grid(G, nbat);
+        // stage r's records, then every shot's candidates for stage r + 2
+        auto absorb = [&](uint32_t r) -> int {
+            if ((ce = cudaEventSynchronize(ev[r & 1])) != cudaSuccess)
+                return set_error(SHS_CUDA_ERROR, std::string("event sync: ") + cudaGetErrorString(ce));
+            for (uint32_t i = 0; i < nbat; ++i) {
+                StageRec rec;
+                std::memcpy(&rec, h_rec + uint64_t(i) * t + r, sizeof(rec));
+                if (!rec.done) return set_error(SHS_CUDA_ERROR, "stage record missing");
+                if (rec.status == SHS_ERROR)
+                    return set_error(SHS_ERROR, "statevector norm drifted beyond 1e-9 at stage " +
+                                                    std::to_string(r));
+                if (rec.status == SHS_DEGENERATE_BRANCH)
+                    return set_error(SHS_DEGENERATE_BRANCH,
+                                     "impossible measurement branch at stage " + std::to_string(r));
+                observed[i] |= u128{static_cast<unsigned>(rec.obit)} << r;
+                sampled[i] |= u128{static_cast<unsigned>(rec.sbit)} << r;
+            }
+            return SHS_OK;
+        };
+        int rc = SHS_OK;
+        for (uint32_t s = 0; s < t && rc == SHS_OK; ++s) {
+            const bool gather = e->a_pows[s] != 1;
+            lp.m = e->a_invs[s];
+            lp.m_sh = gather ? shoup(lp.m, N) : 0;
+            lp.m_step = gather ? mulmod(lp.m, kBlock, N) : 0;
+            lp.gather = gather ? 1 : 0;
+            lp.e1 = s == 0 ? 1 : 0;
+            lp.cur = static_cast<int>(s & 1);
+            rc = launch(e, 0, [&] { k_lock_probs<<<grid, kThreads, 0, e->stream>>>(lp); });
+            if (rc) break;
+            if (s > 0 && (rc = absorb(s - 1))) break;
+            NextPhase* hn = h_nph + (s & 1) * B;
+            if (s + 1 < t) {
+                for (uint32_t i = 0; i < nbat; ++i)
+                    for (int bit = 0; bit < 2; ++bit) {
+                        const StageScalars c = host_scalars(
+                            e, s + 1, observed[i] | (u128{static_cast<unsigned>(bit)} << s), 0.0);
+                        hn[i].phr[bit] = c.phr;
+                        hn[i].phi[bit] = c.phi;
+                        hn[i].phase_mul[bit] = c.phase_mul;
+                    }
+            }
+            NextPhase* dn = d_nph + (s & 1) * B;
+            if ((ce = cudaMemcpyAsync(dn, hn, sizeof(NextPhase) * nbat, cudaMemcpyHostToDevice,
+                                      e->stream)) != cudaSuccess) {
+                rc = set_error(SHS_CUDA_ERROR, std::string("candidates: ") + cudaGetErrorString(ce));
+                break;
+            }
+            LockMeasure q{};
+            q.seed = seed;
+            q.idx0 = idx0 + b0;
+            q.kind = e->err.kind;
+            q.delta = e->err.delta;
+            q.px = e->err.px;
+            q.py = e->err.py;
+            q.check_norms = e->opt.check_norms;
+            q.s = s;
+            q.t = static_cast<uint32_t>(t);
+            q.collapse = s + 1 < t ? 1 : 0;
+            q.kahan = e->kahan ? 1 : 0;
+            q.nparts = G;
+            q.nph = dn;
+            q.rec = d_rec;
+            rc = launch(e, 1, [&] { k_lock_measure<<<nbat, kFinalizeThreads, 0, e->stream>>>(lp, q); });
+            if (rc) break;
+            if ((ce = cudaEventRecord(ev[s & 1], e->stream)) != cudaSuccess) {
+                rc = set_error(SHS_CUDA_ERROR, "event record");
+                break;
+            }
+            if (s + 1 < t) {
+                rc = launch(e, 2, [&] { k_lock_collapse<<<grid, kThreads, 0, e->stream>>>(lp); });
+                std::swap(lp.X, lp.Y);
+            }
+        }
+        if (rc == SHS_OK) rc = absorb(static_cast<uint32_t>(t - 1));
+        if (rc) {
+            cleanup();
+            return rc;
+        }
+        for (uint32_t i = 0; i < nbat; ++i) {
+            const uint64_t o = b0 + i;
+            u128 jj = observed[i];
+            if (e->err.kind == SHS_ERR_BITFLIP)
+                jj = bitflip_bitstring(jj, static_cast<unsigned>(t), e->err.delta, seed,
+                                       static_cast<u32>(idx0 + o));
+            j[2 * o] = static_cast<uint64_t>(jj);
+            j[2 * o + 1] = static_cast<uint64_t>(jj >> 64);
+            if (js) {
+                js[2 * o] = static_cast<uint64_t>(sampled[i]);
+                js[2 * o + 1] = static_cast<uint64_t>(sampled[i] >> 64);
+            }
+            for (uint64_t s = 0; s < t; ++s) {
+                const StageRec& rec = h_rec[uint64_t(i) * t + s];
+                if (p1) p1[o * t + s] = rec.p1;
+                if (bits) {
+                    int32_t* b = bits + (o * t + s) * 4;
+                    b[0] = rec.sbit;
+                    b[1] = rec.obit;
+                    b[2] = rec.flip;
+                    b[3] = rec.ebranch;
+                }
+            }
+        }
+    }
+    cleanup();
+    if (e->timing) resolve_marks(e);
+    state_init(e);  // the engine's own buffers were not touched
+    return SHS_OK;
+}
+
 int run_many_batched(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_t* j,
                      uint64_t* js, double* p1, int32_t* bits) {
     int rc = ensure_batch_tables(e);
@@ -1083,6 +1269,8 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     {
         const char* hm = std::getenv("SHS_HOST_MEASURE");
         e->host_measure = hm && hm[0] == '1';
+        const char* ls = std::getenv("SHS_LOCKSTEP");
+        e->lockstep = !(ls && ls[0] == '0');
     }
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");
@@ -1148,6 +1336,8 @@ int shs_engine_run_many(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t co
         if (!j) return set_error(SHS_INVALID_ARGUMENT, "null output");
         if (count == 0) return SHS_OK;
         if (batchable(e)) return run_many_batched(e, seed, idx0, count, j, j_sampled, p1, bits);
+        if (lockstep_ok(e, count) && e->lockstep)
+            return run_many_lockstep(e, seed, idx0, count, j, j_sampled, p1, bits);
         std::vector<shs_stage_trace> tr(e->t);
         for (uint32_t i = 0; i < count; ++i) {
             u128 jj = 0, js = 0;
@@ -1174,7 +1364,11 @@ int shs_engine_run_many(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t co
     });
 }
 
-int shs_engine_batched(const shs_engine* e) { return e && batchable(e) ? 1 : 0; }
+int shs_engine_batched(const shs_engine* e) {
+    if (!e) return 0;
+    if (batchable(e)) return 1;
+    return lockstep_ok(e, 2) && e->lockstep ? 2 : 0;
+}
 
 int shs_engine_run_batch(shs_engine* e, uint64_t seed, uint64_t idx0, uint32_t count,
                          uint64_t* j) {

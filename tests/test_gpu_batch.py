@@ -75,3 +75,40 @@ def test_acceptance_c2_statistics_batched(cuda_ok):
     chi2 = sum((counts.get(j, 0) - 25000) ** 2 / 25000 for j in (0, 64, 128, 192))
     assert chi2 < 16.27  # p > 1e-3, 3 dof
     print(f"100000 batched runs of N=15: {dt * 1e3:.1f} ms ({dt / 1e5 * 1e9:.0f} ns/run)")
+
+
+# ------------------------------------------------------ lockstep (mid-size N)
+LOCK_ERRS = [E(), E("classical_measure", 0.05), E("amplitude_init", 0.1), E("phase_init", 0.1),
+             E("bitflip", 0.02), E("quantum_measure", 0.02, 0.01, 0.01, 0.0)]
+
+
+def _trace(r):
+    return [(x.p1, x.sampled_bit, x.observed_bit, x.event) for x in r.trace]
+
+
+@pytest.mark.parametrize("N,a,t", [(4087, 1001, 24), (262139, 4242, 16), (1048351, 12345, 12),
+                                   (4194301, 1234567, 10)])
+@pytest.mark.parametrize("ei", range(len(LOCK_ERRS)))
+def test_lockstep_runs_equal_single_runs(cuda_ok, N, a, t, ei):
+    """Shots of a mid-size problem advanced stage by stage together (lockstep.cuh):
+    every shot's bit string, sampled bits and p1 trace equal engine.run for it."""
+    eng = engine(N, a, t, LOCK_ERRS[ei])
+    many = eng.run_many(9, 5, 7)
+    for i, r in enumerate(many):
+        q = eng.run(9, 5 + i)
+        assert r.bits.j == q.bits.j and r.j_sampled == q.j_sampled, i
+        assert _trace(r) == _trace(q), i
+
+
+def test_lockstep_run_problem_matches_reference(cuda_ok, reference):
+    """run_problem at L = 12 (N = 4087: t = 24 > the shared-memory batch's 20)
+    through the lockstep engine equals the reference's statistics."""
+    import paper_2308_05047_b200 as shs
+    for i, a in enumerate([1001, 5, 17]):
+        prob = shs.FactoringProblem.make(4087, a, p=61, q=67, seed=900 + i)
+        got = shs.run_problem(prob, 96)
+        ref = reference.run_problem(4087, a, 61, 67, prob.L, prob.t, prob.seed, 96)
+        assert (got.success, got.lucky_ne, got.lucky_no, got.lucky_oo, got.fail) == \
+            (ref["success"], ref["lucky_ne"], ref["lucky_no"], ref["lucky_oo"], ref["fail"]), a
+        assert (got.first_factor_index, got.first_order_index) == \
+            (ref["first_factor_index"], ref["first_order_index"])
