@@ -883,6 +883,7 @@ int ensure_batch_tables(shs_engine* e) {
 // computing both candidate phases of every shot's next stage with glibc.
 constexpr uint64_t kLockMaxN = uint64_t(1) << 22;           // beyond: engine_run per shot
 constexpr uint64_t kLockBudget = uint64_t(16) << 30;         // HBM for the batch's states
+constexpr uint64_t kLockMinShots = 64;
 
 bool lockstep_ok(const shs_engine* e, uint32_t count) {
     return count >= 2 && !batchable(e) && e->N <= kLockMaxN;
@@ -892,8 +893,13 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
                       uint64_t* js, double* p1, int32_t* bits) {
     const uint64_t N = e->N, nb = e->nb, t = e->t;
     const uint64_t per_shot = 2 * sizeof(double2) * N + 2 * sizeof(double) * nb;
-    const uint32_t B = static_cast<uint32_t>(
-        std::max<uint64_t>(1, std::min<uint64_t>(count, kLockBudget / per_shot)));
+    // shots per batch: 2^24 / N (all of a campaign problem's M shots while N is
+    // small), at least 64 (measured at N = 2^18: 8 / 16 / 32 / 64 / 256 shots per
+    // batch -> 205 / 129 / 155 / 116 / 146 ms for 256 shots), at most kLockBudget
+    uint64_t want = std::max<uint64_t>(kLockMinShots, (uint64_t(1) << 24) / N);
+    if (const char* v = std::getenv("SHS_LOCK_BATCH")) want = std::max(1ull, std::strtoull(v, nullptr, 10));
+    const uint32_t B = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>({uint64_t(count), want, kLockBudget / per_shot})));
     const int G = static_cast<int>(std::max<uint64_t>(
         1, std::min<uint64_t>(e->nchunks, (4 * uint64_t(e->num_sms) + B - 1) / B)));
     double2 *X = nullptr, *Y = nullptr;
