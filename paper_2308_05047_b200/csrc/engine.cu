@@ -900,8 +900,11 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
     if (const char* v = std::getenv("SHS_LOCK_BATCH")) want = std::max(1ull, std::strtoull(v, nullptr, 10));
     const uint32_t B = static_cast<uint32_t>(std::max<uint64_t>(
         1, std::min<uint64_t>({uint64_t(count), want, kLockBudget / per_shot})));
-    const int G = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>(e->nchunks, (4 * uint64_t(e->num_sms) + B - 1) / B)));
+    // one chunk per CTA: the grid runs shot-major (blockIdx.x fastest), so only
+    // the ~(resident CTAs / nchunks) shots in flight share the L2 and their
+    // gathered reads hit it (N = 2^18: a shot is 4.2 MB; 64 shots at once at
+    // ~10 CTAs each thrashed it, probs + collapse at 1.6 / 2.4 TB/s)
+    const int G = static_cast<int>(std::max<uint64_t>(1, e->nchunks));
     double2 *X = nullptr, *Y = nullptr;
     double* S = nullptr;
     unsigned long long* parts = nullptr;

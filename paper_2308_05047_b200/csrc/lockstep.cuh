@@ -111,26 +111,7 @@ static __global__ void __launch_bounds__(kFinalizeThreads) k_lock_measure(LockPa
     const uint32_t shot = blockIdx.x;
     const double* S = p.S + uint64_t(shot) * 2 * p.nb;
     if (q.kahan) {
-        if (threadIdx.x == 0) {  // combine_blocks, statevector.cpp:32-40
-            double s0 = 0, c0 = 0, s1 = 0, c1 = 0;
-            for (uint64_t b = 0; b < p.nb; ++b) {
-                const double x0 = S[b], x1 = S[p.nb + b];
-                if (x0 != 0.0) {
-                    double y = __dsub_rn(x0, c0);
-                    double t = __dadd_rn(s0, y);
-                    c0 = __dsub_rn(__dsub_rn(t, s0), y);
-                    s0 = t;
-                }
-                if (x1 != 0.0) {
-                    double y = __dsub_rn(x1, c1);
-                    double t = __dadd_rn(s1, y);
-                    c1 = __dsub_rn(__dsub_rn(t, s1), y);
-                    s1 = t;
-                }
-            }
-            pp[0] = s0;
-            pp[1] = s1;
-        }
+        kahan_combine(S, p.nb, pp);  // combine_blocks, statevector.cpp:32-40
     } else {
         sum_slots(p.partials + uint64_t(shot) * q.nparts * 2 * kDigits, q.nparts, acc);
         if (threadIdx.x < 2) pp[threadIdx.x] = digits_to_double(acc[threadIdx.x]);

@@ -281,31 +281,69 @@ __device__ __forceinline__ void sum_slots(const unsigned long long* __restrict__
     __syncthreads();
 }
 
+// combine_blocks (statevector.cpp:32-40) for both groups: sequential Kahan over
+// the non-zero block partials in block order, bit-identical to the reference.
+// Called by every thread of the CTA (>= 3 warps). Warps 2.. stage tiles of S
+// into shared memory (coalesced, one tile ahead); lane 0 of warp g folds group
+// g's chain from shared memory, so the two 4-DADD chains run side by side and
+// no fold waits on a global load. pp[0] = p0, pp[1] = p1 on return (synced).
+constexpr int kKahanTile = 512;
+__device__ __forceinline__ void kahan_combine(const double* __restrict__ S, uint64_t nb,
+                                              double* pp) {
+    __shared__ double tile[2][2][kKahanTile];  // [buffer][group][block]
+    const int g = threadIdx.x >> 5;
+    const bool folder = g < 2 && (threadIdx.x & 31) == 0;
+    const uint64_t ntiles = (nb + kKahanTile - 1) / kKahanTile;
+    auto load = [&](uint64_t k) {
+        if (threadIdx.x < 64) return;
+        const uint64_t b0 = k * kKahanTile;
+        for (int i = threadIdx.x - 64; i < 2 * kKahanTile; i += blockDim.x - 64) {
+            const int gg = i / kKahanTile, j = i % kKahanTile;
+            tile[k & 1][gg][j] = b0 + j < nb ? S[gg * nb + b0 + j] : 0.0;
+        }
+    };
+    double s = 0.0, c = 0.0;
+    load(0);
+    __syncthreads();
+    for (uint64_t k = 0; k < ntiles; ++k) {
+        if (k + 1 < ntiles) load(k + 1);
+        if (folder) {
+            const double2* x = reinterpret_cast<const double2*>(tile[k & 1][g]);
+            double2 cur[4], nxt[4];  // 8 partials in registers, the next 8 in flight
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[u] = x[u];
+#pragma unroll 1
+            for (int i = 0; i < kKahanTile / 2; i += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nxt[u] = x[(i + 4 + u) % (kKahanTile / 2)];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double v = (u & 1) ? cur[u >> 1].y : cur[u >> 1].x;
+                    if (v != 0.0) {  // zero partials skipped (tile padding included)
+                        const double y = __dsub_rn(v, c);
+                        const double t = __dadd_rn(s, y);
+                        c = __dsub_rn(__dsub_rn(t, s), y);
+                        s = t;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+            }
+        }
+        __syncthreads();
+    }
+    if (folder) pp[g] = s;
+    __syncthreads();
+}
+
 static __global__ void __launch_bounds__(kFinalizeThreads) k_finalize(const unsigned long long* __restrict__ partials, int nparts,
                            const double* __restrict__ S, uint64_t nb, int kahan,
                            double* __restrict__ out) {
     __shared__ unsigned long long acc[2][kDigits];
     if (kahan) {
-        if (threadIdx.x == 0) {
-            double s0 = 0, c0 = 0, s1 = 0, c1 = 0;
-            for (uint64_t b = 0; b < nb; ++b) {
-                const double x0 = S[b], x1 = S[nb + b];
-                if (x0 != 0.0) {
-                    double y = __dsub_rn(x0, c0);
-                    double t = __dadd_rn(s0, y);
-                    c0 = __dsub_rn(__dsub_rn(t, s0), y);
-                    s0 = t;
-                }
-                if (x1 != 0.0) {
-                    double y = __dsub_rn(x1, c1);
-                    double t = __dadd_rn(s1, y);
-                    c1 = __dsub_rn(__dsub_rn(t, s1), y);
-                    s1 = t;
-                }
-            }
-            out[0] = s0;
-            out[1] = s1;
-        }
+        __shared__ double pp[2];
+        kahan_combine(S, nb, pp);
+        if (threadIdx.x < 2) out[threadIdx.x] = pp[threadIdx.x];
         return;
     }
     sum_slots(partials, nparts, acc);
@@ -338,26 +376,7 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
     __shared__ unsigned long long acc[2][kDigits];
     __shared__ double pp[2];
     if (kahan) {
-        if (threadIdx.x == 0) {
-            double s0 = 0, c0 = 0, s1 = 0, c1 = 0;
-            for (uint64_t b = 0; b < nb; ++b) {
-                const double x0 = S[b], x1 = S[nb + b];
-                if (x0 != 0.0) {
-                    double y = __dsub_rn(x0, c0);
-                    double t = __dadd_rn(s0, y);
-                    c0 = __dsub_rn(__dsub_rn(t, s0), y);
-                    s0 = t;
-                }
-                if (x1 != 0.0) {
-                    double y = __dsub_rn(x1, c1);
-                    double t = __dadd_rn(s1, y);
-                    c1 = __dsub_rn(__dsub_rn(t, s1), y);
-                    s1 = t;
-                }
-            }
-            pp[0] = s0;
-            pp[1] = s1;
-        }
+        kahan_combine(S, nb, pp);
     } else {
         sum_slots(partials, nparts, acc);
         if (threadIdx.x < 2) pp[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
