@@ -407,7 +407,38 @@ def small_n_throughput(shs):
         out[name] = entry
         for e in engines:
             e.close()
+    out["campaign_L18_lockstep"] = lockstep_throughput(shs, ref)
     return out
+
+
+def lockstep_throughput(shs, ref):
+    """The largest problems of the reference's headline campaign (acceptance
+    criteria 4-5: L = 9..18, M = 256 shots per problem): one L = 18 problem's
+    256 shots through run_batch_array, served by the lockstep multi-shot path
+    (DESIGN.md §6b), beside the reference engine's per-run time on one host core
+    (its campaign runs one problem per worker thread)."""
+    import numpy as np
+    N, a, shots = 262139, 4242, 256
+    e = shs.IterativeShorEngine(shs.FactoringProblem.make(N, a), shs.ErrorConfig(),
+                                shs.SimulatorOptions(qubit_ceiling=64))
+    buf = np.empty((shots, 2), dtype=np.uint64)
+    e.run_batch_array(3, 0, shots, buf)  # warm
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        e.run_batch_array(3, 0, shots, buf)
+    dt = (time.perf_counter() - t0) / reps
+    t = e.problem.t
+    e.close()
+    entry = {"N": N, "a": a, "t": t, "shots": shots, "seconds": dt, "runs_per_s": shots / dt,
+             "amp_updates_per_s": shots * N * t / dt}
+    if ref is not None:
+        re = ref.engine(N, a, N.bit_length(), t, qubit_ceiling=33)
+        k = 8
+        sec = re.time_runs(3, 0, k)
+        entry["reference_cpu_runs_per_s_1core"] = k / sec
+        entry["reference_sample"] = f"{k} IterativeShorEngine::run calls of N={N}, a={a}, 1 thread"
+    return entry
 
 
 def config2_statistics(shs, engines, problems, ref):

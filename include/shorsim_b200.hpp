@@ -103,8 +103,9 @@ public:
     // (shs_engine_batched: 1 = whole runs per CTA, N <= 4096; 2 = lockstep
     // shots, mid-size N) a miss fetches the next indices in one call — the
     // reference's shot loops (run_problem, simulate_to_jsonl) call run(seed, m)
-    // for consecutive m — and later calls are served from it. Lockstep fetches
-    // start at 256 shots (a campaign's M) and double on consecutive misses.
+    // for consecutive m — and later calls are served from it. Fetches start at
+    // 256 runs (a campaign's M: a larger first fetch is work the campaign never
+    // reads) and double on consecutive misses, up to 4096 runs.
     RunResult run(u64 seed, u64 bitstring_index) {
         if (batched_) {
             bool hit = cache_seed_ == seed && bitstring_index >= cache_lo_ &&
@@ -138,17 +139,13 @@ public:
     shs_engine* handle() const { return h_; }
 
 private:
-    static constexpr std::uint32_t kPrefetch = 4096;      // whole-run batches
-    static constexpr std::uint32_t kLockFirst = 256;      // lockstep: first fetch ...
-    static constexpr std::uint32_t kLockMax = 4096;       // ... doubling up to this
+    static constexpr std::uint32_t kFetchFirst = 256;     // first fetch ...
+    static constexpr std::uint32_t kFetchMax = 4096;      // ... doubling up to this
 
     void prefetch(u64 seed, u64 idx0) {
-        std::uint32_t n = kPrefetch;
-        if (batch_mode_ == 2) {
-            const bool next = cache_n_ && cache_seed_ == seed && idx0 == cache_lo_ + cache_n_;
-            next_fetch_ = next ? std::min(2 * next_fetch_, kLockMax) : kLockFirst;
-            n = next_fetch_;
-        }
+        const bool next = cache_n_ && cache_seed_ == seed && idx0 == cache_lo_ + cache_n_;
+        next_fetch_ = next ? std::min(2 * next_fetch_, kFetchMax) : kFetchFirst;
+        const std::uint32_t n = next_fetch_;
         c_j_.resize(2 * std::size_t(n));
         c_js_.resize(2 * std::size_t(n));
         c_p1_.resize(std::size_t(n) * t_);

@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -298,6 +299,110 @@ template <bool G, bool E1>
 void launch_collapse(shs_engine* e, const StageParams& p) {
     if (p.dev) launch_collapse_v<G, E1, true>(e, p);
     else launch_collapse_v<G, E1, false>(e, p);
+}
+
+// Lockstep multi-shot buffers (lockstep.cuh), pooled per process: the campaign
+// harness creates one engine per problem, and cudaMalloc/cudaFree of a batch's
+// states plus the pinned host records cost as much as the batch's kernels at
+// N = 2^18 (and more after large allocations). A call checks a set out (any
+// engine, same device, large enough), returns it after; the pool keeps at most
+// kLockPoolBytes of device memory. Engines on different threads take different sets.
+struct LockBufs {
+    int dev = -1;
+    size_t state_bytes = 0, s_bytes = 0, parts_bytes = 0, shots = 0, rec_bytes = 0;
+    double2* X = nullptr;
+    double2* Y = nullptr;
+    double* S = nullptr;
+    unsigned long long* parts = nullptr;
+    DevStage* slots = nullptr;
+    NextPhase* d_nph = nullptr;
+    NextPhase* h_nph = nullptr;
+    StageRec* h_rec = nullptr;
+    StageRec* d_rec = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    size_t device_bytes() const { return 2 * state_bytes + s_bytes + parts_bytes; }
+};
+
+void free_lock_buffers(LockBufs& L) {
+    cudaFree(L.X);
+    cudaFree(L.Y);
+    cudaFree(L.S);
+    cudaFree(L.parts);
+    cudaFree(L.slots);
+    cudaFree(L.d_nph);
+    if (L.h_nph) cudaFreeHost(L.h_nph);
+    if (L.h_rec) cudaFreeHost(L.h_rec);
+    for (auto v : L.ev)
+        if (v) cudaEventDestroy(v);
+    L = LockBufs{};
+}
+
+constexpr size_t kLockPoolBytes = size_t(4) << 30;
+std::mutex g_lock_pool_mu;
+std::vector<LockBufs> g_lock_pool;  // never freed at exit (CUDA may be torn down first)
+
+// A set with at least the given sizes on `dev`: from the pool, else allocated.
+cudaError_t lock_checkout(int dev, size_t state_bytes, size_t s_bytes, size_t parts_bytes,
+                          size_t shots, size_t rec_bytes, LockBufs& out) {
+    {
+        std::lock_guard<std::mutex> g(g_lock_pool_mu);
+        for (size_t i = 0; i < g_lock_pool.size(); ++i) {
+            const LockBufs& c = g_lock_pool[i];
+            if (c.dev == dev && c.state_bytes >= state_bytes && c.s_bytes >= s_bytes &&
+                c.parts_bytes >= parts_bytes && c.shots >= shots && c.rec_bytes >= rec_bytes) {
+                out = c;
+                g_lock_pool.erase(g_lock_pool.begin() + static_cast<std::ptrdiff_t>(i));
+                return cudaSuccess;
+            }
+        }
+    }
+    LockBufs L;
+    L.dev = dev;
+    L.state_bytes = state_bytes;
+    L.s_bytes = s_bytes;
+    L.parts_bytes = parts_bytes;
+    L.shots = shots;
+    L.rec_bytes = rec_bytes;
+    cudaError_t ce;
+    if ((ce = cudaMalloc(&L.X, state_bytes)) != cudaSuccess ||
+        (ce = cudaMalloc(&L.Y, state_bytes)) != cudaSuccess ||
+        (ce = cudaMalloc(&L.S, s_bytes)) != cudaSuccess ||
+        (ce = cudaMalloc(&L.parts, parts_bytes)) != cudaSuccess ||
+        (ce = cudaMalloc(&L.slots, sizeof(DevStage) * 2 * shots)) != cudaSuccess ||
+        (ce = cudaMalloc(&L.d_nph, sizeof(NextPhase) * 2 * shots)) != cudaSuccess ||
+        (ce = cudaHostAlloc(&L.h_nph, sizeof(NextPhase) * 2 * shots, cudaHostAllocDefault)) != cudaSuccess ||
+        (ce = cudaHostAlloc(&L.h_rec, rec_bytes, cudaHostAllocMapped)) != cudaSuccess ||
+        (ce = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L.d_rec), L.h_rec, 0)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&L.ev[0], cudaEventDisableTiming)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&L.ev[1], cudaEventDisableTiming)) != cudaSuccess) {
+        free_lock_buffers(L);
+        return ce;
+    }
+    out = L;
+    return cudaSuccess;
+}
+
+// Back to the pool (its work on the caller's stream already synchronised);
+// sets that would push the pool past kLockPoolBytes evict the oldest first.
+void lock_return(LockBufs& L) {
+    if (L.device_bytes() > kLockPoolBytes) {
+        free_lock_buffers(L);
+        return;
+    }
+    std::vector<LockBufs> evicted;
+    {
+        std::lock_guard<std::mutex> g(g_lock_pool_mu);
+        size_t total = L.device_bytes();
+        for (const auto& c : g_lock_pool) total += c.device_bytes();
+        while (total > kLockPoolBytes && !g_lock_pool.empty()) {
+            total -= g_lock_pool.front().device_bytes();
+            evicted.push_back(g_lock_pool.front());
+            g_lock_pool.erase(g_lock_pool.begin());
+        }
+        g_lock_pool.push_back(L);
+    }
+    for (auto& c : evicted) free_lock_buffers(c);
+    L = LockBufs{};
 }
 
 void release(shs_engine* e) {
@@ -905,45 +1010,25 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
     // gathered reads hit it (N = 2^18: a shot is 4.2 MB; 64 shots at once at
     // ~10 CTAs each thrashed it, probs + collapse at 1.6 / 2.4 TB/s)
     const int G = static_cast<int>(std::max<uint64_t>(1, e->nchunks));
-    double2 *X = nullptr, *Y = nullptr;
-    double* S = nullptr;
-    unsigned long long* parts = nullptr;
-    DevStage* slots = nullptr;
-    NextPhase* d_nph = nullptr;
-    NextPhase* h_nph = nullptr;
-    StageRec* h_rec = nullptr;
-    StageRec* d_rec = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    LockBufs L;
     auto cleanup = [&] {
         cudaStreamSynchronize(e->stream);
-        cudaFree(X);
-        cudaFree(Y);
-        cudaFree(S);
-        cudaFree(parts);
-        cudaFree(slots);
-        cudaFree(d_nph);
-        if (h_nph) cudaFreeHost(h_nph);
-        if (h_rec) cudaFreeHost(h_rec);
-        for (auto v : ev)
-            if (v) cudaEventDestroy(v);
+        lock_return(L);
     };
-    auto cuda_fail = [&](cudaError_t ce, const char* what) {
-        cleanup();
-        return set_error(SHS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(ce));
-    };
-    cudaError_t ce;
-    if ((ce = cudaMalloc(&X, sizeof(double2) * N * B)) != cudaSuccess ||
-        (ce = cudaMalloc(&Y, sizeof(double2) * N * B)) != cudaSuccess ||
-        (ce = cudaMalloc(&S, sizeof(double) * 2 * nb * B)) != cudaSuccess ||
-        (ce = cudaMalloc(&parts, sizeof(unsigned long long) * 2 * kDigits * G * B)) != cudaSuccess ||
-        (ce = cudaMalloc(&slots, sizeof(DevStage) * 2 * B)) != cudaSuccess ||
-        (ce = cudaMalloc(&d_nph, sizeof(NextPhase) * 2 * B)) != cudaSuccess ||
-        (ce = cudaHostAlloc(&h_nph, sizeof(NextPhase) * 2 * B, cudaHostAllocDefault)) != cudaSuccess ||
-        (ce = cudaHostAlloc(&h_rec, sizeof(StageRec) * t * B, cudaHostAllocMapped)) != cudaSuccess ||
-        (ce = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_rec), h_rec, 0)) != cudaSuccess ||
-        (ce = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming)) != cudaSuccess ||
-        (ce = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming)) != cudaSuccess)
-        return cuda_fail(ce, "lockstep buffers");
+    cudaError_t ce = lock_checkout(
+        e->dev, sizeof(double2) * N * B, sizeof(double) * 2 * nb * B,
+        sizeof(unsigned long long) * 2 * kDigits * G * B, B, sizeof(StageRec) * t * B, L);
+    if (ce != cudaSuccess)
+        return set_error(SHS_CUDA_ERROR, std::string("lockstep buffers: ") + cudaGetErrorString(ce));
+    double2 *X = L.X, *Y = L.Y;
+    double* S = L.S;
+    unsigned long long* parts = L.parts;
+    DevStage* slots = L.slots;
+    NextPhase* d_nph = L.d_nph;
+    NextPhase* h_nph = L.h_nph;
+    StageRec* h_rec = L.h_rec;
+    StageRec* d_rec = L.d_rec;
+    cudaEvent_t* ev = L.ev;
     std::vector<u128> observed(B), sampled(B);
     for (uint32_t b0 = 0; b0 < count; b0 += B) {
         const uint32_t nbat = std::min<uint32_t>(B, count - b0);
@@ -1225,14 +1310,17 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     };
     cudaError_t ce = cudaSetDevice(e->dev);
     if (ce != cudaSuccess) return fail(ce, "cudaSetDevice");
-    cudaDeviceProp prop;
-    ce = cudaGetDeviceProperties(&prop, e->dev);
-    if (ce != cudaSuccess) return fail(ce, "cudaGetDeviceProperties");
-    if (prop.major < 10) {
+    // two attributes, not cudaGetDeviceProperties (which queries every field:
+    // milliseconds per engine, and the campaign harness creates one per problem)
+    int major = 0, sms = 0;
+    if ((ce = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, e->dev)) != cudaSuccess ||
+        (ce = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->dev)) != cudaSuccess)
+        return fail(ce, "cudaDeviceGetAttribute");
+    if (major < 10) {
         release(e);
         return set_error(SHS_CUDA_ERROR, "device is not sm_100-class (B200 required)");
     }
-    e->num_sms = prop.multiProcessorCount;
+    e->num_sms = sms;
     e->tiled_cap = e->num_sms;
     e->max_rows = 0;
     // test hook: SHS_TILE_SPLIT=0 / 1 forces the tiled kernels' work-split variant

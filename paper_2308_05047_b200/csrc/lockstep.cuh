@@ -37,6 +37,36 @@ __device__ __forceinline__ StageScalars lock_scalars(const LockParams& p, uint32
     return p.e1 ? p.sc0 : p.slots[2 * shot + p.cur].sc;
 }
 
+// (sel[z], sel[src z]) of the thread's kPer elements zg + e*kBlock, all 2 kPer
+// loads issued before any is used (one round trip per chunk instead of kPer:
+// collapse 128 -> 122 us per N = 2^18 stage of 64 shots; the probs pass keeps
+// its per-element loads — batched, its 120 registers cost occupancy and it ran
+// 168 -> 182-199 us). Stage 0 synthesises e_1. Zero beyond N.
+__device__ __forceinline__ void lock_load(const LockParams& p, const double2* __restrict__ X,
+                                          uint64_t zg, double2 (&xa)[kPer], double2 (&xs)[kPer]) {
+    uint64_t src[kPer];
+    src[0] = p.gather ? mulmod_shoup(zg, p.m, p.m_sh, p.N) : zg;
+#pragma unroll
+    for (int e = 1; e < kPer; ++e)
+        src[e] = p.gather ? addmod(src[e - 1], p.m_step, p.N) : src[e - 1] + kBlock;
+    if (p.e1) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const uint64_t z = zg + uint64_t(e) * kBlock;
+            xa[e] = make_double2(z < p.N && z == 1 ? 1.0 : 0.0, 0.0);
+            xs[e] = make_double2(z < p.N && src[e] == 1 ? 1.0 : 0.0, 0.0);
+        }
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        const uint64_t z = zg + uint64_t(e) * kBlock;
+        const bool in = z < p.N;
+        xa[e] = in ? __ldg(X + z) : make_double2(0.0, 0.0);
+        xs[e] = in ? __ldg(X + src[e]) : make_double2(0.0, 0.0);
+    }
+}
+
 static __global__ void __launch_bounds__(kThreads) k_lock_probs(LockParams p) {
     __shared__ double nrm[2 * kPer][kBlock + 1];
     __shared__ unsigned long long digits[2][kDigits];
@@ -154,25 +184,16 @@ static __global__ void __launch_bounds__(kThreads) k_lock_collapse(LockParams p)
     const int sel = cur->sel;
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = c * kChunk + threadIdx.x;
-        uint64_t src = p.gather ? mulmod_shoup(zg, p.m, p.m_sh, p.N) : zg;
+        double2 xa[kPer], xs[kPer];
+        lock_load(p, X, zg, xa, xs);
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const uint64_t z = zg + uint64_t(e) * kBlock;
             if (z < p.N) {
-                double2 xa, xs;
-                if (p.e1) {
-                    xa = make_double2(z == 1 ? 1.0 : 0.0, 0.0);
-                    xs = make_double2(src == 1 ? 1.0 : 0.0, 0.0);
-                } else {
-                    xa = X[z];
-                    xs = X[src];
-                }
                 double h0r, h0i, h1r, h1i;
-                stage_pair(sc, xa, xs, h0r, h0i, h1r, h1i);
+                stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
                 Y[z] = sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
             }
-            if (p.gather) src = addmod(src, p.m_step, p.N);
-            else src += kBlock;
         }
     }
 }
