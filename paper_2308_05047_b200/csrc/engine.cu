@@ -89,6 +89,7 @@ struct shs_engine {
     unsigned long long* band_ctr = nullptr;  // k_tiled<., false> dynamic band counter
     uint64_t band_issued = 0;                // its value before the next launch
     bool kahan = false;      // resolved combine mode
+    bool lock_ws = true;     // lockstep probs: warp-specialized k_lock_probs_ws
     // state
     bool e1 = true;
     double inv = 1.0;
@@ -1010,6 +1011,8 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
     // gathered reads hit it (N = 2^18: a shot is 4.2 MB; 64 shots at once at
     // ~10 CTAs each thrashed it, probs + collapse at 1.6 / 2.4 TB/s)
     const int G = static_cast<int>(std::max<uint64_t>(1, e->nchunks));
+    // the warp-specialized probs pass walks kLockWsChunks chunks per CTA
+    const int Gp = e->lock_ws ? static_cast<int>((e->nchunks + kLockWsChunks - 1) / kLockWsChunks) : G;
     LockBufs L;
     auto cleanup = [&] {
         cudaStreamSynchronize(e->stream);
@@ -1074,7 +1077,12 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
             lp.gather = gather ? 1 : 0;
             lp.e1 = s == 0 ? 1 : 0;
             lp.cur = static_cast<int>(s & 1);
-            rc = launch(e, 0, [&] { k_lock_probs<<<grid, kThreads, 0, e->stream>>>(lp); });
+            if (e->lock_ws)
+                rc = launch(e, 0, [&] {
+                    k_lock_probs_ws<<<dim3(Gp, nbat), kLockWsThreads, kLockWsSmem, e->stream>>>(lp);
+                });
+            else
+                rc = launch(e, 0, [&] { k_lock_probs<<<grid, kThreads, 0, e->stream>>>(lp); });
             if (rc) break;
             if (s > 0 && (rc = absorb(s - 1))) break;
             NextPhase* hn = h_nph + (s & 1) * B;
@@ -1106,7 +1114,7 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
             q.t = static_cast<uint32_t>(t);
             q.collapse = s + 1 < t ? 1 : 0;
             q.kahan = e->kahan ? 1 : 0;
-            q.nparts = G;
+            q.nparts = Gp;
             q.nph = dn;
             q.rec = d_rec;
             rc = launch(e, 1, [&] { k_lock_measure<<<nbat, kFinalizeThreads, 0, e->stream>>>(lp, q); });
@@ -1362,12 +1370,17 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     ce = cudaFuncSetAttribute(k_tile_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(kFixSmem));
     if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tile_fixup)");
+    ce = cudaFuncSetAttribute(k_lock_probs_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kLockWsSmem));
+    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_lock_probs_ws)");
     e->fixup_cap = 3 * e->num_sms;  // 3 x 68 KB of transposed head slabs per SM
     {
         const char* hm = std::getenv("SHS_HOST_MEASURE");
         e->host_measure = hm && hm[0] == '1';
         const char* ls = std::getenv("SHS_LOCKSTEP");
         e->lockstep = !(ls && ls[0] == '0');
+        const char* lw = std::getenv("SHS_LOCK_WS");  // A/B: 0 = k_lock_probs
+        e->lock_ws = !(lw && lw[0] == '0');
     }
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");

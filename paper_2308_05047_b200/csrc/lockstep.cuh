@@ -122,6 +122,95 @@ static __global__ void __launch_bounds__(kThreads) k_lock_probs(LockParams p) {
                      p.partials + (uint64_t(shot) * gridDim.x + blockIdx.x) * 2 * kDigits, tid);
 }
 
+// k_lock_probs, warp-specialized: 8 load warps produce a chunk's |h|^2 into one
+// of two norm buffers while the chain warp folds the previous chunk's 16
+// in-order block sums (the 256 dependent DADDs per block no longer stall the
+// loads; in k_lock_probs every warp waits for them at the CTA barrier). Same
+// arithmetic and fold order, so S and the digits are identical. Each CTA walks
+// kLockWsChunks chunks of one shot (blockIdx.x + k gridDim.x), so the grid stays
+// shot-major. Dynamic shared memory: kLockWsSmem.
+constexpr int kLockWsLoadThreads = kThreads;                  // 8 load warps
+constexpr int kLockWsThreads = kLockWsLoadThreads + 32;       // + the chain warp
+constexpr int kLockWsChunks = 4;                              // chunks per CTA
+constexpr size_t kLockWsSmem = sizeof(double) * 2 * (2 * kPer) * (kBlock + 1);
+constexpr int kLockFull0 = 1, kLockEmpty0 = 3;                // named barriers (+ buffer)
+
+__device__ __forceinline__ void lock_bar_sync(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kLockWsThreads) : "memory");
+}
+__device__ __forceinline__ void lock_bar_arrive(int id) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kLockWsThreads) : "memory");
+}
+
+static __global__ void __launch_bounds__(kLockWsThreads, 2) k_lock_probs_ws(LockParams p) {
+    extern __shared__ double lock_nrm[];  // [2][2 kPer][kBlock + 1]
+    __shared__ unsigned long long digits[2][kDigits];
+    const uint32_t shot = blockIdx.y;
+    const int tid = threadIdx.x;
+    const double2* X = p.X + uint64_t(shot) * p.N;
+    for (int i = tid; i < 2 * kDigits; i += kLockWsThreads) (&digits[0][0])[i] = 0ull;
+    __syncthreads();
+    constexpr int kRow = kBlock + 1, kBuf = 2 * kPer * kRow;
+    if (tid < kLockWsLoadThreads) {
+        const StageScalars sc = lock_scalars(p, shot);
+        int i = 0;
+        for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x, ++i) {
+            const int buf = i & 1;
+            double* nrm = lock_nrm + buf * kBuf;
+            const uint64_t zg = c * kChunk + tid;
+            double n0[kPer], n1[kPer];
+            {
+                double2 xa[kPer], xs[kPer];
+                lock_load(p, X, zg, xa, xs);
+#pragma unroll
+                for (int e = 0; e < kPer; ++e) {
+                    const uint64_t z = zg + uint64_t(e) * kBlock;
+                    double h0r, h0i, h1r, h1i;
+                    stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
+                    n0[e] = z < p.N ? cnorm(h0r, h0i) : 0.0;
+                    n1[e] = z < p.N ? cnorm(h1r, h1i) : 0.0;
+                }
+            }
+            if (i >= 2) lock_bar_sync(kLockEmpty0 + buf);  // the chain warp is done with it
+#pragma unroll
+            for (int e = 0; e < kPer; ++e) {
+                nrm[e * kRow + tid] = n0[e];
+                nrm[(kPer + e) * kRow + tid] = n1[e];
+            }
+            lock_bar_arrive(kLockFull0 + buf);
+        }
+    } else {
+        const int lane = tid - kLockWsLoadThreads;
+        double* S = p.S + uint64_t(shot) * 2 * p.nb;
+        DigitWindow win;
+        window_reset(win);
+        int i = 0;
+        for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x, ++i) {
+            const int buf = i & 1;
+            lock_bar_sync(kLockFull0 + buf);
+            if (lane < 2 * kPer) {  // one lane per (block, group): in-order block sum
+                const double* row = lock_nrm + buf * kBuf + lane * kRow;
+                double s = 0.0;
+#pragma unroll 16
+                for (int k = 0; k < kBlock; ++k) s = __dadd_rn(s, row[k]);
+                const uint64_t b = c * kPer + (lane & (kPer - 1));
+                const int g = lane / kPer;
+                if (b < p.nb) {
+                    S[g * p.nb + b] = s;
+                    window_add(win, s, digits[g]);
+                }
+            }
+            __syncwarp();
+            // release the buffer only if the load warps will wait for it
+            if (c + 2 * uint64_t(gridDim.x) < p.nchunks) lock_bar_arrive(kLockEmpty0 + buf);
+        }
+        if (lane < 2 * kPer) window_flush(win, digits[lane / kPer]);
+    }
+    __syncthreads();
+    write_cta_digits(digits,
+                     p.partials + (uint64_t(shot) * gridDim.x + blockIdx.x) * 2 * kDigits, tid);
+}
+
 struct LockMeasure {
     uint64_t seed, idx0;
     int kind;
