@@ -220,7 +220,7 @@ def run_ours(args):
         eng.stage_collapse(b, p1 if b else p0)
         state["prefix"] = (state["prefix"] | (b << s)) & ((1 << t) - 1)
         state["s"] = s + 1 if s + 1 < t else 1
-        return s
+        return s, b
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -235,8 +235,11 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     wall0 = time.perf_counter()
+    timed_bits = []
     for _ in range(args.steps):
-        timed_stages.append(step())
+        s_, b_ = step()
+        timed_stages.append(s_)
+        timed_bits.append(b_)
     ev1.record(stream)
     ev1.synchronize()
     wall = time.perf_counter() - wall0
@@ -260,7 +263,17 @@ def run_ours(args):
     kt = eng.kernel_times()
     eng.set_timing(False)
     hbm_peak, peak_src = peaks()
-    per_amp = {"probs": 32, "combine": 0, "collapse": 48}  # algorithmic B/amplitude
+    # algorithmic B/amplitude: a tiled probs pass that is not the
+    # run's last also writes h0 (speculative group-0 write, +16 B); the collapse
+    # (48 B) then runs only when group 1 is kept
+    spec_on = os.environ.get("SHS_SPEC", "1") != "0"
+
+    def spec_at(s):
+        return spec_on and eng.tile_plan(s)["tiled"] and s + 1 < t
+    per_amp = {"probs": 48 if spec_at(timed_stages[-1]) else 32, "combine": 0, "collapse": 48}
+    step_bytes = [N * ((48 if spec_at(s) else 32) + (0 if spec_at(s) and b == 0 else 48))
+                  for s, b in zip(timed_stages, timed_bits)]
+    step_bpa = sum(step_bytes) / len(step_bytes) / N  # average algorithmic B/amp per timed stage
     kernels = {}
     for k, (tot, n) in kt.items():
         avg = tot / max(n, 1)
@@ -324,8 +337,13 @@ def run_ours(args):
         "s_per_run": run_s,
         "s_per_run_dense": run_s_dense,
         "sparse_prefix_stages": sparse_stages,
-        "stage_hbm_gbs": 80 * N / (ms_per_step * 1e-3) / 1e9,
-        "stage_frac_of_hbm": 80 * N / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
+        "stage_hbm_gbs": step_bpa * N / (ms_per_step * 1e-3) / 1e9,
+        "stage_frac_of_hbm": step_bpa * N / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
+        "stage_bytes_per_amp": step_bpa,
+        "speculative_group0": {"on": spec_on, "timed_bits_1": sum(timed_bits),
+                               "timed_steps": len(timed_bits),
+                               "collapse_skipped": sum(1 for s, b in zip(timed_stages, timed_bits)
+                                                       if spec_at(s) and b == 0)},
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "device_ms_per_stage_kernels": stage_dev_ms,
         "roofline": roofline, "kernels": kernels,

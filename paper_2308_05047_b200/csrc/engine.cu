@@ -88,6 +88,8 @@ struct shs_engine {
     uint2* split = nullptr;  // [t][tiled_cap + 1] CTA range starts of the tiled stages
     unsigned long long* band_ctr = nullptr;  // k_tiled<., false> dynamic band counter
     uint64_t band_issued = 0;                // its value before the next launch
+    bool spec_on = true;                     // speculative group-0 writes (SHS_SPEC=0: off)
+    int64_t spec_stage = -1;                 // Y holds h0 of this stage's tiled probs pass
     bool kahan = false;      // resolved combine mode
     bool lock_ws = true;     // lockstep probs: warp-specialized k_lock_probs_ws
     // state
@@ -552,6 +554,7 @@ int ensure_buffers(shs_engine* e) {
 }
 
 int state_init(shs_engine* e) {
+    e->spec_stage = -1;
     e->e1 = true;  // sel = e_1 implicitly: no memset of the N-amplitude buffer
     e->inv = 1.0;
     e->pending = false;
@@ -590,6 +593,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
     if (e->plans[s].tiled && !e->e1) {
         TileParams tp = tile_params_for(e, s);
         tp.dev = dev;
+        tp.spec = e->spec_on && s + 1 < e->t ? 1 : 0;
         const TilePlanHost& pl = e->plans[s];
         const int g1 = pl.split_tail ? pl.grid
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
@@ -606,7 +610,9 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         });
         e->launches++;  // k_tiled + k_tile_fixup: two kernels in one launch group
         *nparts = g1 + g2;
+        e->spec_stage = tp.spec ? static_cast<int64_t>(s) : -1;
     } else if (e->e1) {
+        e->spec_stage = -1;
         // stage 0 from the implicit e_1: two live amplitudes (k_stage_probs_e1)
         StageParams p = params_for(e, s);
         rc = launch(e, 0, [&] {
@@ -615,6 +621,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         });
         *nparts = 1;
     } else {
+        e->spec_stage = -1;
         StageParams p = params_for(e, s);
         p.dev = dev;
         rc = launch(e, 0, [&] {
@@ -633,9 +640,17 @@ int launch_collapse_pass(shs_engine* e, uint32_t s, int src_group, const DevStag
         TileParams tp = tile_params_for(e, s);
         tp.sel = src_group;
         tp.dev = dev;
+        tp.spec = e->spec_stage == static_cast<int64_t>(s) ? 1 : 0;
         const TilePlanHost& pl = e->plans[s];
         const int g1 = pl.split_tail ? pl.grid
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
+        const bool skip = tp.spec && !dev && src_group == 0;  // Y already holds h0
+        if (skip) {
+            e->spec_stage = -1;
+            std::swap(e->X, e->Y);
+            e->e1 = false;
+            return SHS_OK;
+        }
         rc = launch(e, 2, [&] {
             if (pl.split_tail) {
                 k_tiled<false, true><<<g1, tile_threads<false, true>(), tile_smem_bytes<false>(), e->stream>>>(tp);
@@ -659,6 +674,7 @@ int launch_collapse_pass(shs_engine* e, uint32_t s, int src_group, const DevStag
         });
     }
     if (rc) return rc;
+    e->spec_stage = -1;
     std::swap(e->X, e->Y);
     e->e1 = false;
     return SHS_OK;
@@ -1381,6 +1397,8 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         e->lockstep = !(ls && ls[0] == '0');
         const char* lw = std::getenv("SHS_LOCK_WS");  // A/B: 0 = k_lock_probs
         e->lock_ws = !(lw && lw[0] == '0');
+        const char* sp = std::getenv("SHS_SPEC");  // A/B: 0 = every collapse runs
+        e->spec_on = !(sp && sp[0] == '0');
     }
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");

@@ -117,6 +117,10 @@ struct TileParams {
     double* head;       // [H][2][256] head norms of each row (before its first boundary)
     double* tail;       // [H][2]      predecessor's tail partial, indexed by successor row
     int sel;            // collapse: group kept
+    // speculative group-0 write: the probs pass also stores h0 into Y (the
+    // collapse of group 0 would write exactly those values), and the collapse
+    // of a stage whose probs pass did so returns at once when group 0 is kept
+    int spec;
     const DevStage* dev;  // device-resident run: sc / sel from this slot instead
 };
 
@@ -449,6 +453,13 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
     (void)kConsumers;
     const StageScalars sc = p.dev ? p.dev->sc : p.sc;
     const int sel = p.dev ? p.dev->sel : p.sel;
+    if (!kProbs && p.spec && sel == 0) {
+        // Y already holds h0 (raw, like every collapse output); the dynamic band
+        // counter still advances by the ntiles fetches a full launch makes
+        if (!kSplit && blockIdx.x == 0 && tid == 0) atomicAdd(p.band_ctr, p.ntiles);
+        return;
+    }
+    const bool spec = kProbs && p.spec;
 #ifdef SHS_CTA_TRACE
     uint64_t trace_t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
@@ -550,6 +561,13 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
         // starts at an odd index stores its segment shifted by one element (the last
         // one is carried into the next chunk) so every store covers whole 32 B sectors
         constexpr bool kSectorShift = !kProbs && kCols == 32;
+        // speculative h0 stores: plain (the sector-shifted stores measured 2% slower
+        // per config-4 stage, profiles/r01/README.md v15); -DSHS_SPEC_SHIFT for A/B
+#ifdef SHS_SPEC_SHIFT
+        constexpr bool kSpecShift = kProbs && kCols == 32;
+#else
+        constexpr bool kSpecShift = false;
+#endif
         double2 carry[kRowsPerConsumer];
 #pragma unroll
         for (int q = 0; q < kRowsPerConsumer; ++q) carry[q] = make_double2(0.0, 0.0);
@@ -569,11 +587,11 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
                 const bool live = pos - rlo < rn;
                 double h0r, h0i, h1r, h1i;
                 stage_pair(sc, st.dst[r][c], st.src[c][r], h0r, h0i, h1r, h1i);
-                if (kProbs) {
-                    sm.nrm[b][0][r][c] = live ? cnorm(h0r, h0i) : 0.0;
-                    sm.nrm[b][1][r][c] = live ? cnorm(h1r, h1i) : 0.0;
-                } else if (kSectorShift) {
-                    const double2 hv = sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);
+                // row segment store of this warp's 32 columns (collapse output, or
+                // the probs pass's speculative h0): a row that starts at an odd
+                // index stores shifted by one element so every store covers whole
+                // 32 B sectors (the last element is carried into the next chunk)
+                auto store_seg = [&](const double2 hv) {
                     const uint64_t rz = st.row_z[r];
                     if ((rz & 1) == 0) {
                         if (live) p.Y[rz + pos] = hv;
@@ -593,6 +611,16 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
                         if (c == kCols - 1 && live && pos + 1 == rlo + rn) p.Y[rz + pos] = hv;
                         carry[q] = last;
                     }
+                };
+                if (kProbs) {
+                    sm.nrm[b][0][r][c] = live ? cnorm(h0r, h0i) : 0.0;
+                    sm.nrm[b][1][r][c] = live ? cnorm(h1r, h1i) : 0.0;
+                    if (spec) {
+                        if (kSpecShift) store_seg(make_double2(h0r, h0i));
+                        else if (live) p.Y[st.row_z[r] + pos] = make_double2(h0r, h0i);
+                    }
+                } else if (kSectorShift) {
+                    store_seg(sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i));
                 } else if (live) {
                     p.Y[st.row_z[r] + pos] =
                         sel ? make_double2(h1r, h1i) : make_double2(h0r, h0i);

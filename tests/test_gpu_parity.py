@@ -303,6 +303,45 @@ def test_tiled_work_split_vs_direct(cuda_ok, monkeypatch, N, a, split):
         prefix |= b << s
 
 
+@pytest.mark.parametrize("N,a,split", [(16777207, 1234567, ""), (268435247, 3, "0")])
+def test_speculative_group0_write(cuda_ok, monkeypatch, N, a, split):
+    """Tiled probs passes also store h0 into the successor buffer, so a stage
+    that keeps group 0 skips its collapse: identical block sums, states and
+    seeded runs to the engine with every collapse launched (SHS_SPEC=0), for
+    both work-split variants, forced branches of both kinds and device-resident
+    runs (where the collapse kernel returns at once on group 0)."""
+    if split:
+        monkeypatch.setenv("SHS_TILE_SPLIT", split)
+    spec = engine(N, a, 8)
+    monkeypatch.setenv("SHS_SPEC", "0")
+    full = engine(N, a, 8)
+    monkeypatch.delenv("SHS_SPEC", raising=False)
+    monkeypatch.delenv("SHS_TILE_SPLIT", raising=False)
+    assert sum(spec.tile_plan(s)["tiled"] for s in range(8)) >= 4
+    rng = np.random.default_rng(N + 1)
+    spec.state_init()
+    full.state_init()
+    prefix = 0
+    for s in range(8):
+        p = spec.stage_probs(s, prefix)
+        assert p == full.stage_probs(s, prefix), s
+        if s + 1 == 8:
+            break
+        b = s & 1 if s < 4 else int(rng.integers(2))
+        if min(p) <= 1e-300:
+            b = int(p[1] > p[0])
+        spec.stage_collapse(b, p[b])
+        full.stage_collapse(b, p[b])
+        for first in [0, N - 4096] + [int(x) for x in rng.integers(0, N - 4096, 4)]:
+            for x in (0, 1):
+                assert np.array_equal(arr(spec.state_read(x, first, 4096)),
+                                      arr(full.state_read(x, first, 4096))), (s, first)
+        prefix |= b << s
+    for idx in range(3):
+        r, q = spec.run(11, idx), full.run(11, idx)
+        assert r.bits.j == q.bits.j and [x.p1 for x in r.trace] == [x.p1 for x in q.trace], idx
+
+
 @pytest.mark.parametrize("N,a", [(16777207, 2), (268435247, 3), (4194301, 7), (268435247, 5)])
 def test_small_multiplier_streams_vs_gather(cuda_ok, N, a):
     """The last stages (multipliers a, a^2, a^4 ... <= 1024) stage their A
