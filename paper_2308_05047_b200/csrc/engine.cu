@@ -1093,6 +1093,7 @@ int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_
             lp.gather = gather ? 1 : 0;
             lp.e1 = s == 0 ? 1 : 0;
             lp.cur = static_cast<int>(s & 1);
+            lp.spec = e->lock_ws && e->spec_on && s + 1 < t ? 1 : 0;  // probs and collapse of stage s
             if (e->lock_ws)
                 rc = launch(e, 0, [&] {
                     k_lock_probs_ws<<<dim3(Gp, nbat), kLockWsThreads, kLockWsSmem, e->stream>>>(lp);

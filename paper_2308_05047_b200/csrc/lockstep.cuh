@@ -31,6 +31,8 @@ struct LockParams {
     int cur;             // slot s & 1
     double* S;           // [B][2][nb] block partials
     unsigned long long* partials;  // [B][gridDim.x][2][kDigits]
+    int spec;            // k_lock_probs_ws also stores h0 into Y; the collapse of a
+                         // shot that keeps group 0 then has nothing to write
 };
 
 __device__ __forceinline__ StageScalars lock_scalars(const LockParams& p, uint32_t shot) {
@@ -148,6 +150,7 @@ static __global__ void __launch_bounds__(kLockWsThreads, 2) k_lock_probs_ws(Lock
     const uint32_t shot = blockIdx.y;
     const int tid = threadIdx.x;
     const double2* X = p.X + uint64_t(shot) * p.N;
+    double2* Ys = p.Y + uint64_t(shot) * p.N;
     for (int i = tid; i < 2 * kDigits; i += kLockWsThreads) (&digits[0][0])[i] = 0ull;
     __syncthreads();
     constexpr int kRow = kBlock + 1, kBuf = 2 * kPer * kRow;
@@ -169,6 +172,7 @@ static __global__ void __launch_bounds__(kLockWsThreads, 2) k_lock_probs_ws(Lock
                     stage_pair(sc, xa[e], xs[e], h0r, h0i, h1r, h1i);
                     n0[e] = z < p.N ? cnorm(h0r, h0i) : 0.0;
                     n1[e] = z < p.N ? cnorm(h1r, h1i) : 0.0;
+                    if (p.spec && z < p.N) Ys[z] = make_double2(h0r, h0i);
                 }
             }
             if (i >= 2) lock_bar_sync(kLockEmpty0 + buf);  // the chain warp is done with it
@@ -271,6 +275,7 @@ static __global__ void __launch_bounds__(kThreads) k_lock_collapse(LockParams p)
     const DevStage* cur = p.slots + 2 * shot + p.cur;
     const StageScalars sc = cur->sc;  // stage 0: k_lock_measure stored sc0 there
     const int sel = cur->sel;
+    if (p.spec && sel == 0) return;  // Y already holds this shot's h0
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = c * kChunk + threadIdx.x;
         double2 xa[kPer], xs[kPer];
