@@ -263,13 +263,13 @@ def run_ours(args):
     kt = eng.kernel_times()
     eng.set_timing(False)
     hbm_peak, peak_src = peaks()
-    # algorithmic B/amplitude: a tiled probs pass that is not the
-    # run's last also writes h0 (speculative group-0 write, +16 B); the collapse
-    # (48 B) then runs only when group 1 is kept
+    # algorithmic B/amplitude: a probs pass that is not the run's
+    # last also writes h0 (speculative group-0 write, +16 B); the collapse (48 B)
+    # then runs only when group 1 is kept
     spec_on = os.environ.get("SHS_SPEC", "1") != "0"
 
     def spec_at(s):
-        return spec_on and eng.tile_plan(s)["tiled"] and s + 1 < t
+        return spec_on and s + 1 < t
     per_amp = {"probs": 48 if spec_at(timed_stages[-1]) else 32, "combine": 0, "collapse": 48}
     step_bytes = [N * ((48 if spec_at(s) else 32) + (0 if spec_at(s) and b == 0 else 48))
                   for s, b in zip(timed_stages, timed_bits)]

@@ -621,9 +621,10 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         });
         *nparts = 1;
     } else {
-        e->spec_stage = -1;
         StageParams p = params_for(e, s);
         p.dev = dev;
+        p.spec = e->spec_on && s + 1 < e->t ? 1 : 0;
+        e->spec_stage = p.spec ? static_cast<int64_t>(s) : -1;
         rc = launch(e, 0, [&] {
             if (gather) launch_probs<true, false>(e, p);
             else launch_probs<false, false>(e, p);
@@ -663,6 +664,13 @@ int launch_collapse_pass(shs_engine* e, uint32_t s, int src_group, const DevStag
         StageParams p = params_for(e, s);
         p.sel = src_group;
         p.dev = dev;
+        p.spec = e->spec_stage == static_cast<int64_t>(s) ? 1 : 0;
+        if (p.spec && !dev && src_group == 0) {  // Y already holds h0
+            e->spec_stage = -1;
+            std::swap(e->X, e->Y);
+            e->e1 = false;
+            return SHS_OK;
+        }
         rc = launch(e, 2, [&] {
             if (gather) {
                 if (e->e1) launch_collapse<true, true>(e, p);

@@ -46,6 +46,8 @@ struct StageParams {
     uint32_t A, W;
     float invA, invW;
     const DevStage* dev;  // device-resident run: sc / sel from this slot instead
+    int spec;             // single engine: the probs pass also stores h0 into Y, and
+                          // the collapse that keeps group 0 has nothing to write
 };
 
 // floor(d / D) for d < 2^20, D <= 2^11, from a float reciprocal and one correction
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_probs(StageParams p) {
             const bool live = zg + uint64_t(e) * kBlock < p.zend;
             nrm[e][tid] = live ? cnorm(h0r, h0i) : 0.0;
             nrm[kPer + e][tid] = live ? cnorm(h1r, h1i) : 0.0;
+            if (p.spec && live) p.Y[zg + uint64_t(e) * kBlock - p.z0] = make_double2(h0r, h0i);
         }
         __syncthreads();
         if (tid < 2 * kPer) {
@@ -434,6 +437,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_collapse(StageParams p) {
     if (kDev) __syncthreads();
     const volatile StageScalars& dsc = s_sc;
     const int sel = kDev ? s_sel : p.sel;
+    if (p.spec && sel == 0) return;  // Y already holds h0 (speculative probs pass)
     for (uint64_t c = blockIdx.x; c < p.nchunks; c += gridDim.x) {
         const uint64_t zg = p.z0 + c * kChunk + tid;
         double2 xa[kPer], xs[kPer];

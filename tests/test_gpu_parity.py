@@ -303,21 +303,27 @@ def test_tiled_work_split_vs_direct(cuda_ok, monkeypatch, N, a, split):
         prefix |= b << s
 
 
-@pytest.mark.parametrize("N,a,split", [(16777207, 1234567, ""), (268435247, 3, "0")])
-def test_speculative_group0_write(cuda_ok, monkeypatch, N, a, split):
+@pytest.mark.parametrize("N,a,split,tiling", [(16777207, 1234567, "", "auto"),
+                                              (268435247, 3, "0", "auto"),
+                                              (1048351, 12345, "", "off"),
+                                              (16777207, 5, "", "off")])
+def test_speculative_group0_write(cuda_ok, monkeypatch, N, a, split, tiling):
     """Tiled probs passes also store h0 into the successor buffer, so a stage
     that keeps group 0 skips its collapse: identical block sums, states and
     seeded runs to the engine with every collapse launched (SHS_SPEC=0), for
     both work-split variants, forced branches of both kinds and device-resident
-    runs (where the collapse kernel returns at once on group 0)."""
+    runs (where the collapse kernel returns at once on group 0); tiled and
+    direct kernels (gather; a = 5: the staged-stream small multipliers)."""
     if split:
         monkeypatch.setenv("SHS_TILE_SPLIT", split)
-    spec = engine(N, a, 8)
+    opt = {} if tiling == "auto" else {"tiling": tiling}
+    spec = engine(N, a, 8, **opt)
     monkeypatch.setenv("SHS_SPEC", "0")
-    full = engine(N, a, 8)
+    full = engine(N, a, 8, **opt)
     monkeypatch.delenv("SHS_SPEC", raising=False)
     monkeypatch.delenv("SHS_TILE_SPLIT", raising=False)
-    assert sum(spec.tile_plan(s)["tiled"] for s in range(8)) >= 4
+    n_tiled = sum(spec.tile_plan(s)["tiled"] for s in range(8))
+    assert n_tiled >= 4 if tiling == "auto" else n_tiled == 0
     rng = np.random.default_rng(N + 1)
     spec.state_init()
     full.state_init()
