@@ -292,7 +292,7 @@ def run_ours(args):
             ks = json.load(f)["kernels"][kname]
         traffic = ks["dram_bytes_per_amp"] * N
         traffic_src = f"profiles/r01/ncu_summary.json {kname} ({ks['version']}): " \
-                      f"{ks['dram_bytes_per_amp']} DRAM B/amp at n29 x N"
+                      f"{ks['dram_bytes_per_amp']} DRAM B/amp at N={ks.get('N', 'n29')} x this N"
     except (OSError, KeyError, ValueError):
         pass
     roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
