@@ -95,6 +95,14 @@ typedef struct {
     int32_t device;         /* CUDA device ordinal */
     int32_t combine;        /* SHS_COMBINE_* */
     int32_t tiling;         /* SHS_TILING_*: sorted-residue tiles for the permutation */
+    /* Multi-GPU: 0 = one device (`device`); >= 2 = the state is
+     * block-sharded over devices[0..n_devices) (NULL: device, device+1, ...; a
+     * device may repeat: virtual shards); < 0 = AUTO: one device while the state
+     * (32 B per amplitude) fits it, else as many as needed (the SHS_DEVICES
+     * environment variable, e.g. "0,1,2,3", overrides AUTO). `combine` applies
+     * to the global block partials exactly as on one device. */
+    int32_t n_devices;
+    const int32_t* devices;
 } shs_options;
 
 /* StageTrace, proj/include/shorsim/statevector.hpp:135-141 */
@@ -109,7 +117,7 @@ typedef struct {
 
 typedef struct shs_engine shs_engine;
 
-/* Library defaults (SimulatorOptions{4, 1, 26, true} on device 0, AUTO, AUTO). */
+/* Library defaults (SimulatorOptions{4, 1, 26, true} on device 0, AUTO, AUTO, one device). */
 void shs_default_options(shs_options* out);
 
 /* IterativeShorEngine::IterativeShorEngine, statevector.cpp:285-321. */
@@ -170,6 +178,10 @@ int shs_stage_read(shs_engine* engine, int32_t x, uint64_t first, uint64_t count
 /* current (post-init / post-reset) amplitudes g_x[y], interleaved (re, im) */
 int shs_state_read(shs_engine* engine, int32_t x, uint64_t first, uint64_t count,
                    double* interleaved);
+/* shs_state_read at arbitrary y: out[i] = g_x[idx[i]] (0 for idx[i] >= N); the
+ * ShardedState::amp_xy(x, y) accessor, statevector.hpp:44, batched */
+int shs_state_gather(shs_engine* engine, int32_t x, const uint64_t* idx, uint64_t count,
+                     double* interleaved);
 /* 256-amplitude block partials of the pending stage: out[0..nb) S0, out[nb..2nb) S1 */
 int shs_stage_block_sums(shs_engine* engine, double* out);
 uint64_t shs_num_blocks(const shs_engine* engine);
@@ -204,6 +216,9 @@ void* shs_engine_stream(const shs_engine* engine);
 uint64_t shs_engine_launch_count(const shs_engine* engine);
 /* bytes of device memory the engine holds */
 uint64_t shs_engine_device_bytes(const shs_engine* engine);
+/* devices the engine's state lives on (several when sharded): writes up to max
+ * ordinals, returns their count */
+int shs_engine_devices(const shs_engine* engine, int32_t* out, int32_t max);
 
 /* ---- sharded engine (one shard of the state per GPU; §8e) ----------------
  * Shard q of G owns global amplitude indices [q*S, min(N, (q+1)*S)), S a
@@ -221,6 +236,7 @@ uint64_t shs_engine_device_bytes(const shs_engine* engine);
 typedef struct shs_shard shs_shard;
 #define SHS_MAX_SHARDS 16
 #define SHS_DIGITS 80 /* 2 groups x 40 x 32-bit digits (in uint64 words) */
+#define SHS_SHARD_IPC_BYTES 640 /* shs_shard_ipc_handles blob */
 
 int shs_shard_create(const shs_problem* problem, const shs_error* error,
                      const shs_options* options, uint32_t rank, uint32_t nshards,
@@ -230,10 +246,27 @@ void shs_shard_destroy(shs_shard* shard);
 int shs_shard_range(const shs_shard* shard, uint64_t out[3]);
 /* this shard's two device buffers (allocated at create) */
 int shs_shard_buffers(const shs_shard* shard, void* out[2]);
-/* CUDA IPC handles of the two buffers: out receives 2 x 64 bytes */
+/* CUDA IPC handles of this shard's buffers, stage digits and ordering events:
+ * out receives SHS_SHARD_IPC_BYTES; a peer process passes them to
+ * shs_shard_attach_ipc */
 int shs_shard_ipc_handles(const shs_shard* shard, void* out);
+/* peer buffers only (enough for the per-stage driver); cross-device pointers
+ * get peer access enabled, or an error when the devices cannot reach each other */
 int shs_shard_attach(shs_shard* shard, uint32_t peer, void* const bufs[2]);
 int shs_shard_attach_ipc(shs_shard* shard, uint32_t peer, const void* handles);
+/* a peer shard object of this process (buffers, digits, events) */
+int shs_shard_attach_local(shs_shard* shard, shs_shard* peer);
+/* host barrier of a one-process-per-GPU run: a POSIX shared-memory segment
+ * name ("/..."), the same on every rank of the run (all ranks on one node) */
+int shs_shard_set_barrier(shs_shard* shard, const char* shm_name);
+/* IterativeShorEngine::run over the shards, device-resident (collective: the
+ * shards of this process; with count < G every process calls it with its own
+ * shards and the barrier set). Per stage: exchange, probs, the exact digit sum
+ * and the measurement on every device (no host round trip), collapse; stage
+ * ordering across shards by (IPC) events. trace: t entries or NULL. */
+int shs_shards_run(shs_shard* const* shards, uint32_t count, uint64_t seed, uint64_t idx,
+                   uint64_t j[2], uint64_t j_sampled[2], shs_stage_trace* trace);
+uint64_t shs_shard_device_bytes(const shs_shard* shard);
 int shs_shard_init(shs_shard* shard);
 int shs_shard_needs_exchange(const shs_shard* shard, uint32_t s);
 int shs_shard_exchange(shs_shard* shard, uint32_t s);

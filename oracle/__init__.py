@@ -148,6 +148,16 @@ class Oracle:
         L.so_stage_block_sums.argtypes = [C.c_void_p, C.POINTER(dbl)]
         L.so_num_blocks.restype = u64
         L.so_num_blocks.argtypes = [C.c_void_p]
+        L.so_sparse_create.argtypes = [u64, u64, C.c_uint, C.c_uint, C.POINTER(so_error), C.c_int,
+                                       C.POINTER(C.c_void_p)]
+        L.so_sparse_destroy.argtypes = [C.c_void_p]
+        L.so_sparse_init.argtypes = [C.c_void_p]
+        L.so_sparse_stage_probs.argtypes = [C.c_void_p, C.c_uint, u64, u64, C.c_int,
+                                            C.POINTER(dbl), C.POINTER(dbl)]
+        L.so_sparse_stage_collapse.argtypes = [C.c_void_p, C.c_int, dbl]
+        L.so_sparse_size.restype = u64
+        L.so_sparse_size.argtypes = [C.c_void_p]
+        L.so_sparse_state.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
 
     # scalar helpers
     def philox(self, key, ctr):
@@ -180,9 +190,49 @@ class Oracle:
         arr = (dbl * len(values))(*values)
         return self.lib.so_combine_blocks(arr, len(values))
 
+    def sparse(self, N, a, L, t, err=None, check_norms=True):
+        return SparseOracle(self, N, a, L, t, err, check_norms)
+
     def engine(self, N, a, L, t, err=None, shard_count=4, qubit_ceiling=64, check_norms=True):
         return OracleEngine(self, N, a, L, t, err or make_error(), shard_count, qubit_ceiling,
                             check_norms)
+
+
+class SparseOracle:
+    """so_sparse: the stage recipe on the support of the state (config-4 sizes)."""
+
+    def __init__(self, o, N, a, L, t, err=None, check_norms=True):
+        self.o, self.t, self.N = o, t, N
+        h = C.c_void_p()
+        _check(o.lib.so_sparse_create(N, a, L, t, C.byref(err or make_error()),
+                                      1 if check_norms else 0, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.lib.so_sparse_destroy(self.h)
+            self.h = None
+
+    def state_init(self):
+        _check(self.o.lib.so_sparse_init(self.h))
+
+    def stage_probs(self, s, prefix=0, combine_mode=0):
+        p0, p1 = dbl(), dbl()
+        _check(self.o.lib.so_sparse_stage_probs(self.h, s, prefix & (2**64 - 1), prefix >> 64,
+                                                combine_mode, C.byref(p0), C.byref(p1)))
+        return p0.value, p1.value
+
+    def collapse(self, src_group, p_src):
+        _check(self.o.lib.so_sparse_stage_collapse(self.h, src_group, p_src))
+
+    def state(self, x):
+        """(sorted support as uint64 array, g_x there as interleaved float64 array)"""
+        import numpy as np
+        n = self.o.lib.so_sparse_size(self.h)
+        z = np.empty(n, dtype=np.uint64)
+        v = np.empty(2 * n, dtype=np.float64)
+        _check(self.o.lib.so_sparse_state(self.h, x, z.ctypes.data, v.ctypes.data))
+        return z, v
 
 
 class OracleEngine:

@@ -4,8 +4,17 @@
 #include "shor_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
+
+struct par_job_hdr { void (*fn)(void*, uint64_t, uint64_t); void* ctx; uint64_t lo, hi; };
+static void* par_trampoline(void* p) {
+    struct par_job_hdr* j = (struct par_job_hdr*)p;
+    j->fn(j->ctx, j->lo, j->hi);
+    return NULL;
+}
 
 typedef unsigned __int128 u128;
 typedef __int128 i128;
@@ -354,6 +363,58 @@ static inline void stage_pair(const so_engine* g, uint64_t z, uint64_t src, doub
     h[3] = (ui - vi) * kInvSqrt2;
 }
 
+/* Host-thread fan-out over independent index ranges (block partials are each a
+ * sequential in-order sum, collapse is elementwise: results do not depend on
+ * the thread count). SO_THREADS overrides the online core count. */
+static void par_for(uint64_t n, void (*fn)(void*, uint64_t, uint64_t), void* ctx) {
+    long nt = sysconf(_SC_NPROCESSORS_ONLN);
+    const char* env = getenv("SO_THREADS");
+    if (env) nt = atol(env);
+    if (nt < 1) nt = 1;
+    if (nt > 64) nt = 64;
+    if (n < 65536 || nt == 1) { fn(ctx, 0, n); return; }
+    pthread_t th[64];
+    struct par_job { void (*fn)(void*, uint64_t, uint64_t); void* ctx; uint64_t lo, hi; } jobs[64];
+    uint64_t per = (n + (uint64_t)nt - 1) / (uint64_t)nt;
+    for (long i = 0; i < nt; ++i) {
+        uint64_t lo = per * (uint64_t)i, hi = lo + per < n ? lo + per : n;
+        jobs[i].fn = fn; jobs[i].ctx = ctx; jobs[i].lo = lo < n ? lo : n; jobs[i].hi = hi;
+    }
+    for (long i = 1; i < nt; ++i) pthread_create(&th[i], NULL, par_trampoline, &jobs[i]);
+    fn(ctx, jobs[0].lo, jobs[0].hi);
+    for (long i = 1; i < nt; ++i) pthread_join(th[i], NULL);
+}
+
+struct probs_ctx { const so_engine* g; int gather; uint64_t m; double* b0; double* b1; };
+static void probs_range(void* vc, uint64_t lo, uint64_t hi) {
+    struct probs_ctx* c = (struct probs_ctx*)vc;
+    const uint64_t N = c->g->N;
+    for (uint64_t b = lo; b < hi; ++b) { /* statevector.cpp:353-371 */
+        uint64_t z = b * BLOCK, ze = z + BLOCK < N ? z + BLOCK : N;
+        double s0 = 0, s1 = 0, h[4];
+        for (; z < ze; ++z) {
+            uint64_t src = c->gather ? so_mulmod(c->m, z, N) : z;
+            stage_pair(c->g, z, src, h);
+            s0 += h[0] * h[0] + h[1] * h[1]; /* std::norm */
+            s1 += h[2] * h[2] + h[3] * h[3];
+        }
+        c->b0[b] = s0;
+        c->b1[b] = s1;
+    }
+}
+
+struct collapse_ctx { so_engine* g; int gather; uint64_t m; int src_group; };
+static void collapse_range(void* vc, uint64_t lo, uint64_t hi) {
+    struct collapse_ctx* c = (struct collapse_ctx*)vc;
+    so_engine* g = c->g;
+    for (uint64_t z = lo; z < hi; ++z) {
+        double h[4];
+        stage_pair(g, z, c->gather ? so_mulmod(c->m, z, g->N) : z, h);
+        g->nxt[2 * z] = h[2 * c->src_group];
+        g->nxt[2 * z + 1] = h[2 * c->src_group + 1];
+    }
+}
+
 int so_stage_probs(so_engine* g, unsigned s, uint64_t lo, uint64_t hi, int combine_mode,
                    double* p0, double* p1) {
     if (s >= g->t) return SO_INVALID;
@@ -366,18 +427,9 @@ int so_stage_probs(so_engine* g, unsigned s, uint64_t lo, uint64_t hi, int combi
     uint64_t N = g->N, m = g->a_invs[s];
     double* b0 = g->bsum;
     double* b1 = g->bsum + g->nblocks;
-    for (uint64_t b = 0; b < g->nblocks; ++b) { /* statevector.cpp:353-371 */
-        uint64_t z = b * BLOCK, ze = z + BLOCK < N ? z + BLOCK : N;
-        double s0 = 0, s1 = 0, h[4];
-        for (; z < ze; ++z) {
-            uint64_t src = gather ? so_mulmod(m, z, N) : z;
-            stage_pair(g, z, src, h);
-            s0 += h[0] * h[0] + h[1] * h[1]; /* std::norm */
-            s1 += h[2] * h[2] + h[3] * h[3];
-        }
-        b0[b] = s0;
-        b1[b] = s1;
-    }
+    /* blocks are independent (each a sequential in-order sum): threads over blocks */
+    struct probs_ctx c = {g, gather, m, b0, b1};
+    par_for(g->nblocks, probs_range, &c);
     if (combine_mode == 0) {
         g->p0 = so_combine_blocks(b0, g->nblocks);
         g->p1 = so_combine_blocks(b1, g->nblocks);
@@ -418,12 +470,8 @@ int so_stage_collapse(so_engine* g, int src_group, double p_src) {
     if (p_src < kDegenerateMass) return SO_DEGENERATE;
     int gather = g->a_pows[g->ps] != 1;
     uint64_t N = g->N, m = g->a_invs[g->ps];
-    for (uint64_t z = 0; z < N; ++z) {
-        double h[4];
-        stage_pair(g, z, gather ? so_mulmod(m, z, N) : z, h);
-        g->nxt[2 * z] = h[2 * src_group];
-        g->nxt[2 * z + 1] = h[2 * src_group + 1];
-    }
+    struct collapse_ctx c = {g, gather, m, src_group};
+    par_for(N, collapse_range, &c);
     double* tmp = g->sel; g->sel = g->nxt; g->nxt = tmp;
     g->inv = 1.0 / sqrt(p_src);
     g->pending = 0;
@@ -475,5 +523,197 @@ int so_engine_run(so_engine* g, uint64_t seed, uint64_t idx, int combine_mode, u
     j[0] = (uint64_t)observed;
     j[1] = (uint64_t)(observed >> 64);
     if (g->err.kind == K_BITFLIP) so_bitflip(j, g->t, g->err.delta, seed, (uint32_t)idx);
+    return SO_OK;
+}
+
+/* ------------------------------------------------- sparse-support engine
+ * The same stage recipe (Appendix A; statevector.cpp:339-401) on the support
+ * of the state only, for N too large for the dense restatement (config 4,
+ * N ~ 2^32). From the run start e_1 (statevector.cpp:326-329), stage s can only
+ * make amplitudes at z and A_s * z nonzero (the gather of :345 reads sel[a_inv
+ * z]), so sel lives on a sorted set of indices. Every amplitude outside it is
+ * exactly zero: its |h|^2 is +0.0 and adding +0.0 leaves the reference's
+ * in-order 256-block sums (:354-370) unchanged, and all-zero blocks are
+ * skipped by combine_blocks (:32-40). Hence p0/p1 and every support amplitude
+ * equal the dense computation's; no assumption about the orbit is made (the
+ * candidate set is a sorted union, so wraps and collisions are handled). */
+struct so_sparse {
+    uint64_t N;
+    unsigned t;
+    so_error err;
+    int check_norms;
+    double w[4];
+    uint64_t* a_pows;
+    uint64_t* a_invs;
+    uint64_t n;       /* support size of sel */
+    uint64_t* z;      /* sorted support */
+    double* v;        /* sel values, interleaved */
+    double inv;
+    int pending;
+    unsigned ps;
+    double ph[2];
+    int phase_mul;
+    uint64_t nc;      /* pending stage: candidate indices (sorted) and h0, h1 */
+    uint64_t* cz;
+    double* ch;       /* 4 per candidate */
+    double p0, p1;
+};
+
+void so_sparse_destroy(so_sparse* g) {
+    if (!g) return;
+    free(g->a_pows); free(g->a_invs); free(g->z); free(g->v); free(g->cz); free(g->ch);
+    free(g);
+}
+
+int so_sparse_create(uint64_t N, uint64_t a, unsigned L, unsigned t, const so_error* e,
+                     int check_norms, so_sparse** out) {
+    int rc = engine_validate(N, L, t, e, 2, 127);
+    if (rc) return rc;
+    so_sparse* g = (so_sparse*)calloc(1, sizeof(so_sparse));
+    g->N = N; g->t = t; g->err = *e; g->check_norms = check_norms;
+    so_reinit_state(e, g->w);
+    g->a_pows = (uint64_t*)calloc(t, sizeof(uint64_t));
+    g->a_invs = (uint64_t*)calloc(t, sizeof(uint64_t));
+    g->a_pows[t - 1] = a % N; /* statevector.cpp:302-306 */
+    for (unsigned s = t - 1; s > 0; --s) g->a_pows[s - 1] = so_mulmod(g->a_pows[s], g->a_pows[s], N);
+    for (unsigned s = 0; s < t; ++s) {
+        if (g->a_pows[s] == 1) continue;
+        uint64_t gcd;
+        rc = so_mod_inverse(g->a_pows[s], N, &g->a_invs[s], &gcd);
+        if (rc) { so_sparse_destroy(g); return rc; }
+    }
+    so_sparse_init(g);
+    *out = g;
+    return SO_OK;
+}
+
+int so_sparse_init(so_sparse* g) {
+    free(g->z); free(g->v); free(g->cz); free(g->ch);
+    g->cz = NULL; g->ch = NULL; g->nc = 0;
+    g->n = 1;
+    g->z = (uint64_t*)malloc(sizeof(uint64_t));
+    g->v = (double*)malloc(2 * sizeof(double));
+    g->z[0] = 1; g->v[0] = 1.0; g->v[1] = 0.0; /* e_1, inv = 1 (see so_state_init) */
+    g->inv = 1.0;
+    g->pending = 0;
+    return SO_OK;
+}
+
+static int cmp_u64(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+/* index of z in the sorted support, or -1 */
+static int64_t sp_find(const so_sparse* g, uint64_t z) {
+    uint64_t lo = 0, hi = g->n;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if (g->z[mid] < z) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < g->n && g->z[lo] == z) ? (int64_t)lo : -1;
+}
+
+int so_sparse_stage_probs(so_sparse* g, unsigned s, uint64_t lo, uint64_t hi, int combine_mode,
+                          double* p0, double* p1) {
+    if (s >= g->t) return SO_INVALID;
+    double phi = so_stage_phase(s, lo, hi);
+    g->ph[0] = 1.0 * cos(phi); /* std::polar(1.0, phi), statevector.cpp:338 */
+    g->ph[1] = 1.0 * sin(phi);
+    int gather = g->a_pows[s] != 1;
+    g->phase_mul = gather || phi != 0.0;
+    g->ps = s;
+    uint64_t N = g->N, A = g->a_pows[s], m = g->a_invs[s];
+    /* candidates: support ∪ A * support (z with sel[z] or sel[a_inv z] nonzero) */
+    uint64_t nc = gather ? 2 * g->n : g->n;
+    free(g->cz); free(g->ch);
+    g->cz = (uint64_t*)malloc(sizeof(uint64_t) * nc);
+    memcpy(g->cz, g->z, sizeof(uint64_t) * g->n);
+    if (gather)
+        for (uint64_t i = 0; i < g->n; ++i) g->cz[g->n + i] = so_mulmod(A, g->z[i], N);
+    qsort(g->cz, nc, sizeof(uint64_t), cmp_u64);
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < nc; ++i)
+        if (k == 0 || g->cz[i] != g->cz[k - 1]) g->cz[k++] = g->cz[i];
+    nc = k;
+    g->nc = nc;
+    g->ch = (double*)malloc(sizeof(double) * 4 * (nc ? nc : 1));
+    /* block partials in z order over the candidate set (statevector.cpp:353-371) */
+    double* b0 = (double*)malloc(sizeof(double) * (nc ? nc : 1));
+    double* b1 = (double*)malloc(sizeof(double) * (nc ? nc : 1));
+    uint64_t nb = 0, cur = UINT64_MAX;
+    double s0 = 0, s1 = 0;
+    const double inv = g->inv;
+    for (uint64_t i = 0; i < nc; ++i) {
+        uint64_t z = g->cz[i];
+        if (z / BLOCK != cur) {
+            if (cur != UINT64_MAX) { b0[nb] = s0; b1[nb] = s1; ++nb; }
+            cur = z / BLOCK; s0 = 0; s1 = 0;
+        }
+        int64_t ix = sp_find(g, z);
+        int64_t is = sp_find(g, gather ? so_mulmod(m, z, N) : z);
+        double xr = ix >= 0 ? g->v[2 * ix] : 0.0, xi = ix >= 0 ? g->v[2 * ix + 1] : 0.0;
+        double sr = is >= 0 ? g->v[2 * is] : 0.0, si = is >= 0 ? g->v[2 * is + 1] : 0.0;
+        xr *= inv; xi *= inv; sr *= inv; si *= inv;
+        double ur, ui, vr, vi, *h = g->ch + 4 * i;
+        CMUL(g->w[0], g->w[1], xr, xi, ur, ui);   /* g0[z] = w0 * v      (reset, :397) */
+        CMUL(g->w[2], g->w[3], sr, si, vr, vi);   /* g1[src] = w1 * v    (reset, :398) */
+        if (g->phase_mul) CMUL(vr, vi, g->ph[0], g->ph[1], vr, vi); /* * ph  (:345 / :360) */
+        h[0] = (ur + vr) * kInvSqrt2;             /* h0 (:361) */
+        h[1] = (ui + vi) * kInvSqrt2;
+        h[2] = (ur - vr) * kInvSqrt2;             /* h1 (:362) */
+        h[3] = (ui - vi) * kInvSqrt2;
+        s0 += h[0] * h[0] + h[1] * h[1];          /* std::norm */
+        s1 += h[2] * h[2] + h[3] * h[3];
+    }
+    if (cur != UINT64_MAX) { b0[nb] = s0; b1[nb] = s1; ++nb; }
+    if (combine_mode == 0) {
+        g->p0 = so_combine_blocks(b0, nb);
+        g->p1 = so_combine_blocks(b1, nb);
+    } else {
+        g->p0 = so_exact_sum(b0, nb);
+        g->p1 = so_exact_sum(b1, nb);
+    }
+    free(b0); free(b1);
+    g->pending = 1;
+    *p0 = g->p0;
+    *p1 = g->p1;
+    if (g->check_norms && fabs(g->p0 + g->p1 - 1.0) > kNormTolerance) return SO_ERROR; /* :374 */
+    return SO_OK;
+}
+
+/* collapse/reset, statevector.cpp:384-401: sel = h_src on the candidates */
+int so_sparse_stage_collapse(so_sparse* g, int src_group, double p_src) {
+    if (!g->pending) return SO_INVALID;
+    if (p_src < kDegenerateMass) return SO_DEGENERATE;
+    free(g->z); free(g->v);
+    g->n = g->nc;
+    g->z = g->cz;
+    g->v = (double*)malloc(sizeof(double) * 2 * (g->n ? g->n : 1));
+    for (uint64_t i = 0; i < g->n; ++i) {
+        g->v[2 * i] = g->ch[4 * i + 2 * src_group];
+        g->v[2 * i + 1] = g->ch[4 * i + 2 * src_group + 1];
+    }
+    free(g->ch);
+    g->cz = NULL; g->ch = NULL; g->nc = 0;
+    g->inv = 1.0 / sqrt(p_src);
+    g->pending = 0;
+    return SO_OK;
+}
+
+uint64_t so_sparse_size(const so_sparse* g) { return g->n; }
+
+/* sorted support and the materialised g_x = w_x * (sel * inv) there */
+int so_sparse_state(const so_sparse* g, int x, uint64_t* z_out, double* out) {
+    for (uint64_t i = 0; i < g->n; ++i) {
+        if (z_out) z_out[i] = g->z[i];
+        if (out) {
+            double vr = g->v[2 * i] * g->inv, vi = g->v[2 * i + 1] * g->inv, r, im;
+            CMUL(g->w[2 * x], g->w[2 * x + 1], vr, vi, r, im);
+            out[2 * i] = r;
+            out[2 * i + 1] = im;
+        }
+    }
     return SO_OK;
 }

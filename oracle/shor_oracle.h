@@ -80,6 +80,21 @@ int so_state_read(so_engine* e, int x, uint64_t first, uint64_t count, double* o
 int so_stage_block_sums(so_engine* e, double* out);
 uint64_t so_num_blocks(const so_engine* e);
 
+/* sparse-support engine: the same recipe on the support of the state only
+ * (N beyond the dense restatement's reach, e.g. config 4). Bit-identical p0/p1
+ * (both combine modes) and amplitudes to so_engine on the same forced sequence. */
+typedef struct so_sparse so_sparse;
+int so_sparse_create(uint64_t N, uint64_t a, unsigned L, unsigned t, const so_error* e,
+                     int check_norms, so_sparse** out);
+void so_sparse_destroy(so_sparse* g);
+int so_sparse_init(so_sparse* g);
+int so_sparse_stage_probs(so_sparse* g, unsigned s, uint64_t prefix_lo, uint64_t prefix_hi,
+                          int combine_mode, double* p0, double* p1);
+int so_sparse_stage_collapse(so_sparse* g, int src_group, double p_src);
+uint64_t so_sparse_size(const so_sparse* g);
+/* z_out[size] = sorted support (may be NULL); out[2*size] = g_x there (may be NULL) */
+int so_sparse_state(const so_sparse* g, int x, uint64_t* z_out, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,7 @@ SHS_CUDA_ERROR = 8
 
 COMBINE = {"auto": 0, "kahan": 1, "exact": 2}
 SHS_DIGITS = 80
+SHS_SHARD_IPC_BYTES = 640
 MAX_SHARDS = 16
 TILING = {"auto": 0, "force": 1, "off": 2}
 
@@ -45,7 +46,8 @@ class shs_error(C.Structure):
 
 class shs_options(C.Structure):
     _fields_ = [("shard_count", u32), ("workers", u32), ("qubit_ceiling", u32),
-                ("check_norms", i32), ("device", i32), ("combine", i32), ("tiling", i32)]
+                ("check_norms", i32), ("device", i32), ("combine", i32), ("tiling", i32),
+                ("n_devices", i32), ("devices", C.POINTER(i32))]
 
 
 class shs_stage_trace(C.Structure):
@@ -73,6 +75,7 @@ SIGNATURES = [
     ("shs_stage_collapse", C.c_int, [vp, i32, dbl]),
     ("shs_stage_read", C.c_int, [vp, i32, u64, u64, C.POINTER(dbl)]),
     ("shs_state_read", C.c_int, [vp, i32, u64, u64, C.POINTER(dbl)]),
+    ("shs_state_gather", C.c_int, [vp, i32, C.POINTER(u64), u64, C.POINTER(dbl)]),
     ("shs_stage_block_sums", C.c_int, [vp, C.POINTER(dbl)]),
     ("shs_num_blocks", u64, [vp]),
     ("shs_index_map", C.c_int, [vp, u32, u64, u64, C.POINTER(u64)]),
@@ -85,6 +88,7 @@ SIGNATURES = [
     ("shs_engine_stream", vp, [vp]),
     ("shs_engine_launch_count", u64, [vp]),
     ("shs_engine_device_bytes", u64, [vp]),
+    ("shs_engine_devices", C.c_int, [vp, C.POINTER(i32), i32]),
     ("shs_shard_create", C.c_int, [C.POINTER(shs_problem), C.POINTER(shs_error),
                                    C.POINTER(shs_options), u32, u32, C.POINTER(vp)]),
     ("shs_shard_destroy", None, [vp]),
@@ -93,6 +97,11 @@ SIGNATURES = [
     ("shs_shard_ipc_handles", C.c_int, [vp, C.c_void_p]),
     ("shs_shard_attach", C.c_int, [vp, u32, C.POINTER(vp)]),
     ("shs_shard_attach_ipc", C.c_int, [vp, u32, C.c_void_p]),
+    ("shs_shard_attach_local", C.c_int, [vp, vp]),
+    ("shs_shard_set_barrier", C.c_int, [vp, C.c_char_p]),
+    ("shs_shards_run", C.c_int, [C.POINTER(vp), u32, u64, u64, C.POINTER(u64), C.POINTER(u64),
+                                 C.POINTER(shs_stage_trace)]),
+    ("shs_shard_device_bytes", u64, [vp]),
     ("shs_shard_init", C.c_int, [vp]),
     ("shs_shard_needs_exchange", C.c_int, [vp, u32]),
     ("shs_shard_exchange", C.c_int, [vp, u32]),

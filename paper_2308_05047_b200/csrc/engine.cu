@@ -41,6 +41,7 @@
 #include "batch.cuh"
 #include "sparse.cuh"
 #include "lockstep.cuh"
+#include "shard_group.hpp"
 
 using namespace shs;
 
@@ -137,6 +138,10 @@ struct shs_engine {
     double2* sNrm2 = nullptr;      // ... sorted by z
     void* sTemp = nullptr;
     size_t sTempBytes = 0;
+    // multi-device engine (options.n_devices): the state is block-sharded over a
+    // shard group driven by this engine (shard.cu); every run / step call below
+    // is forwarded to it
+    ShardGroup* group = nullptr;
 };
 
 namespace {
@@ -410,6 +415,8 @@ void lock_return(LockBufs& L) {
 
 void release(shs_engine* e) {
     if (!e) return;
+    group_destroy(e->group);
+    e->group = nullptr;
     cudaSetDevice(e->dev);
     if (e->stream) cudaStreamSynchronize(e->stream);
     for (auto& m : e->marks) {
@@ -527,8 +534,29 @@ int carve_sparse(shs_engine* e) {
     return SHS_OK;
 }
 
+// All-or-nothing: a failed allocation frees what this call allocated, so a
+// retry starts clean (and no kernel ever runs with a half-allocated engine).
+int ensure_buffers_once(shs_engine* e);
 int ensure_buffers(shs_engine* e) {
     if (e->X) return SHS_OK;
+    const uint64_t bytes0 = e->device_bytes;
+    int rc = ensure_buffers_once(e);
+    if (rc) {
+        for (void* p : {static_cast<void*>(e->X), static_cast<void*>(e->Y), static_cast<void*>(e->S),
+                        static_cast<void*>(e->head), static_cast<void*>(e->tail),
+                        static_cast<void*>(e->split)})
+            cudaFree(p);
+        e->X = e->Y = nullptr;
+        e->S = nullptr;
+        e->head = e->tail = nullptr;
+        e->split = nullptr;
+        e->device_bytes = bytes0;
+        cudaGetLastError();  // the failed cudaMalloc is reported through rc
+    }
+    return rc;
+}
+
+int ensure_buffers_once(shs_engine* e) {
     const size_t amp_bytes = sizeof(double2) * e->N;
     SHS_CUDA(cudaMalloc(&e->X, amp_bytes));
     SHS_CUDA(cudaMalloc(&e->Y, amp_bytes));
@@ -968,11 +996,14 @@ int engine_run_host(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
 
 int engine_run(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_out,
                shs_stage_trace* trace) {
+    if (e->group) return group_run(e->group, seed, idx, j_out, js_out, trace);
     return e->host_measure ? engine_run_host(e, seed, idx, j_out, js_out, trace)
                            : engine_run_device(e, seed, idx, j_out, js_out, trace);
 }
 
-bool batchable(const shs_engine* e) { return e->N <= kBatchMaxN && e->t <= kBatchMaxT; }
+bool batchable(const shs_engine* e) {
+    return !e->group && e->N <= kBatchMaxN && e->t <= kBatchMaxT;
+}
 
 // Device tables for whole-run batches: multipliers, inverses (+ Shoup) and the
 // phase table std::polar(1, stage_phase(s, p)) for every (s, prefix) computed
@@ -1016,7 +1047,7 @@ constexpr uint64_t kLockBudget = uint64_t(16) << 30;         // HBM for the batc
 constexpr uint64_t kLockMinShots = 64;
 
 bool lockstep_ok(const shs_engine* e, uint32_t count) {
-    return count >= 2 && !batchable(e) && e->N <= kLockMaxN;
+    return count >= 2 && !e->group && !batchable(e) && e->N <= kLockMaxN;
 }
 
 int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_t* j,
@@ -1274,6 +1305,8 @@ void shs_default_options(shs_options* o) {
     o->device = 0;
     o->combine = SHS_COMBINE_AUTO;
     o->tiling = SHS_TILING_AUTO;
+    o->n_devices = 0;
+    o->devices = nullptr;
 }
 
 const char* shs_last_error(void) { return last_error(); }
@@ -1425,6 +1458,28 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     e->device_bytes = part_bytes + 32;  // the N-amplitude buffers come with the first stage
     e->sparse_n = plan_sparse_prefix(e);
     state_init(e);
+    {  // multi-device: options.n_devices, AUTO by the state's size
+        std::vector<int> devs;
+        if (o.n_devices >= 2) {
+            if (o.n_devices > SHS_MAX_SHARDS) {
+                release(e);
+                return set_error(SHS_INVALID_ARGUMENT, "n_devices must be <= 16");
+            }
+            for (int q = 0; q < o.n_devices; ++q) devs.push_back(o.devices ? o.devices[q] : o.device + q);
+        } else if (o.n_devices < 0) {
+            if ((rc = plan_devices(e->N, o.device, &devs))) {
+                release(e);
+                return rc;
+            }
+        }
+        if (devs.size() >= 2) {
+            if ((rc = group_create(*problem, *error, o, devs, &e->group))) {
+                release(e);
+                return rc;
+            }
+            e->sparse_n = 0;  // the group runs every stage dense
+        }
+    }
     *out = e;
     return SHS_OK;
 }
@@ -1527,19 +1582,29 @@ int shs_engine_run_sequential(shs_engine* e, uint64_t seed, uint64_t idx0, uint3
 }
 
 int shs_state_init(shs_engine* e) {
-    return guarded(e, [&] { return state_init(e); });
+    return guarded(e, [&] { return e->group ? group_state_init(e->group) : state_init(e); });
 }
 
 int shs_stage_probs(shs_engine* e, uint32_t s, uint64_t lo, uint64_t hi, double* p0, double* p1) {
-    return guarded(e, [&] { return stage_probs(e, s, (u128{hi} << 64) | lo, p0, p1); });
+    return guarded(e, [&] {
+        if (e->group) {
+            if (s >= e->t) return set_error(SHS_INVALID_ARGUMENT, "stage index out of range");
+            return group_stage_probs(e->group, s, (u128{hi} << 64) | lo, p0, p1);
+        }
+        return stage_probs(e, s, (u128{hi} << 64) | lo, p0, p1);
+    });
 }
 
 int shs_stage_collapse(shs_engine* e, int32_t src_group, double p_source) {
-    return guarded(e, [&] { return stage_collapse(e, src_group, p_source, true); });
+    return guarded(e, [&] {
+        if (e->group) return group_stage_collapse(e->group, src_group, p_source);
+        return stage_collapse(e, src_group, p_source, true);
+    });
 }
 
 int shs_stage_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, double* host) {
     return guarded(e, [&]() -> int {
+        if (e->group) return group_stage_read(e->group, x, first, count, host);
         if (!e->pending) return set_error(SHS_INVALID_ARGUMENT, "no pending stage");
         if (count == 0) return SHS_OK;
         double2* d = nullptr;
@@ -1567,6 +1632,7 @@ int shs_stage_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
 int shs_state_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, double* host) {
     return guarded(e, [&]() -> int {
         if (x != 0 && x != 1) return set_error(SHS_INVALID_ARGUMENT, "group must be 0 or 1");
+        if (e->group) return group_state_read(e->group, x, first, count, host);
         if (!e->e1 && !e->X) return set_error(SHS_INVALID_ARGUMENT, "no state");
         if (count == 0) return SHS_OK;
         double2* d = nullptr;
@@ -1581,6 +1647,35 @@ int shs_state_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
         SHS_CUDA(cudaMemcpyAsync(host, d, sizeof(double2) * count, cudaMemcpyDeviceToHost,
                                  e->stream));
         SHS_CUDA(cudaFreeAsync(d, e->stream));
+        return sync(e);
+    });
+}
+
+int shs_state_gather(shs_engine* e, int32_t x, const uint64_t* idx, uint64_t count,
+                     double* host) {
+    return guarded(e, [&]() -> int {
+        if (x != 0 && x != 1) return set_error(SHS_INVALID_ARGUMENT, "group must be 0 or 1");
+        if (!e->e1 && !e->X) return set_error(SHS_INVALID_ARGUMENT, "no state");
+        if (count == 0) return SHS_OK;
+        if (!idx || !host) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+        if (e->group) return group_state_gather(e->group, x, idx, count, host);
+        uint64_t* di = nullptr;
+        double2* d = nullptr;
+        SHS_CUDA(cudaMallocAsync(&di, sizeof(uint64_t) * count, e->stream));
+        SHS_CUDA(cudaMallocAsync(&d, sizeof(double2) * count, e->stream));
+        SHS_CUDA(cudaMemcpyAsync(di, idx, sizeof(uint64_t) * count, cudaMemcpyHostToDevice,
+                                 e->stream));
+        const int grid = static_cast<int>(std::min<uint64_t>((count + 255) / 256, 4096));
+        const double wr = e->w[2 * x], wi = e->w[2 * x + 1];
+        int rc = launch(e, -1, [&] {
+            if (e->e1) k_state_gather<true><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, di, count, d);
+            else k_state_gather<false><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, di, count, d);
+        });
+        if (rc) return rc;
+        SHS_CUDA(cudaMemcpyAsync(host, d, sizeof(double2) * count, cudaMemcpyDeviceToHost,
+                                 e->stream));
+        SHS_CUDA(cudaFreeAsync(d, e->stream));
+        SHS_CUDA(cudaFreeAsync(di, e->stream));
         return sync(e);
     });
 }
@@ -1602,6 +1697,7 @@ int shs_stage_tile_plan(const shs_engine* e, uint32_t s, uint64_t out[6]) {
 
 int shs_stage_block_sums(shs_engine* e, double* out) {
     return guarded(e, [&]() -> int {
+        if (e->group) return set_error(SHS_INVALID_ARGUMENT, "block sums of a sharded engine live on its shards");
         if (!e->pending) return set_error(SHS_INVALID_ARGUMENT, "no pending stage");
         SHS_CUDA(cudaMemcpyAsync(out, e->S, sizeof(double) * 2 * e->nb, cudaMemcpyDeviceToHost,
                                  e->stream));
@@ -1680,8 +1776,23 @@ int shs_engine_kernel_times(const shs_engine* e, double ms[3], uint64_t launches
 
 void* shs_engine_stream(const shs_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
 
-uint64_t shs_engine_launch_count(const shs_engine* e) { return e ? e->launches : 0; }
+uint64_t shs_engine_launch_count(const shs_engine* e) {
+    return e ? e->launches + (e->group ? group_launches(e->group) : 0) : 0;
+}
 
-uint64_t shs_engine_device_bytes(const shs_engine* e) { return e ? e->device_bytes : 0; }
+uint64_t shs_engine_device_bytes(const shs_engine* e) {
+    return e ? e->device_bytes + (e->group ? group_device_bytes(e->group) : 0) : 0;
+}
+
+int shs_engine_devices(const shs_engine* e, int32_t* out, int32_t max) {
+    if (!e) return 0;
+    if (!e->group) {
+        if (out && max > 0) out[0] = e->dev;
+        return 1;
+    }
+    const int n = static_cast<int>(e->group->shards.size());
+    for (int q = 0; q < n && out && q < max; ++q) out[q] = shard_device(e->group->shards[q]);
+    return n;
+}
 
 }  // extern "C"

@@ -229,11 +229,12 @@ struct Enumerator {
 
 extern "C" int shs_exhaustive_distribution(const shs_problem* problem, const shs_error* error,
                                            uint64_t node_budget, int32_t device, double* out) {
-    if (!problem || !error || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    if (!problem || !error) return set_error(SHS_INVALID_ARGUMENT, "null argument");
     // statevector.cpp:536-538: the reference's limits come first
     if (problem->t > 14 || problem->L + 1 > 12)
         return set_error(SHS_BUDGET_EXCEEDED,
                          "exhaustive_joint_distribution: t <= 14 and n <= 12 required");
+    if (!out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
     std::string why;
     if (validate_error(*error, &why)) return set_error(SHS_CONFIG_ERROR, why);
     if (problem->N < 2 || problem->t < 1 || problem->N > (uint64_t(1) << problem->L))

@@ -11,9 +11,15 @@
 //   collapse  shard-local, in place over P, which becomes the next sel.
 // Identity stages and the first stage (implicit |1>) need no exchange.
 #include <cuda_runtime.h>
+#include <fcntl.h>
 #include <nvtx3/nvToolsExt.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -26,8 +32,63 @@
 #include "stage_kernels.cuh"
 #include "tile_plan.hpp"
 #include "tiled.cuh"
+#include "shard_group.hpp"
 
 using namespace shs;
+
+// Host barrier for one-process-per-GPU sharded runs: a sense-reversing counter
+// in a POSIX shared-memory segment (every rank of a run lives on one node: the
+// NVLink domain). It orders ENQUEUES, never GPU work: a rank records its event
+// for stage s before the barrier, its peers enqueue their waits on that event
+// after it (cudaStreamWaitEvent waits on the record enqueued before the call).
+struct ShmBarrier {
+    struct Seg {
+        std::atomic<uint32_t> count;
+        std::atomic<uint32_t> gen;
+    };
+    Seg* seg = nullptr;
+    std::string name;
+    uint32_t n = 1;
+    bool owner = false;
+    ~ShmBarrier() {
+        if (seg) munmap(seg, sizeof(Seg));
+        if (owner) shm_unlink(name.c_str());
+    }
+    int open(const char* nm, uint32_t parties, bool unlink_at_close) {
+        name = nm;
+        n = parties;
+        owner = unlink_at_close;
+        const int fd = shm_open(nm, O_CREAT | O_RDWR, 0600);
+        if (fd < 0) return set_error(SHS_INVALID_ARGUMENT, std::string("shm_open ") + nm);
+        if (ftruncate(fd, sizeof(Seg)) != 0) {  // zero-filled on first creation
+            ::close(fd);
+            return set_error(SHS_INVALID_ARGUMENT, std::string("ftruncate ") + nm);
+        }
+        void* p = mmap(nullptr, sizeof(Seg), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        ::close(fd);
+        if (p == MAP_FAILED) return set_error(SHS_INVALID_ARGUMENT, std::string("mmap ") + nm);
+        seg = static_cast<Seg*>(p);
+        return SHS_OK;
+    }
+    // every party calls arrive(); returns when all n have arrived
+    int arrive() {
+        const uint32_t g = seg->gen.load(std::memory_order_acquire);
+        if (seg->count.fetch_add(1, std::memory_order_acq_rel) + 1 == n) {
+            seg->count.store(0, std::memory_order_relaxed);
+            seg->gen.fetch_add(1, std::memory_order_acq_rel);
+            return SHS_OK;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        for (uint64_t k = 0; seg->gen.load(std::memory_order_acquire) == g; ++k) {
+            if (k > 1024) sched_yield();
+            if ((k & 0xffff) == 0 &&
+                std::chrono::steady_clock::now() - t0 > std::chrono::seconds(600))
+                return set_error(SHS_CUDA_ERROR, "sharded run: peer rank did not reach the barrier "
+                                                 "within 600 s");
+        }
+        return SHS_OK;
+    }
+};
 
 struct shs_shard {
     shs_problem prob{};
@@ -60,6 +121,31 @@ struct shs_shard {
     double kms[3] = {0, 0, 0};
     uint64_t klaunch[3] = {0, 0, 0};
     uint64_t launches = 0;
+    // device-resident runs (shard_run): stage slots and host-mapped records as
+    // the single engine's, this shard's exact digits per stage parity (read by
+    // every peer's finalize), and the cross-shard ordering events per parity:
+    // X = exchange pushes done, D = digits written, C = collapse done (all
+    // interprocess-capable), M = measurement record written (host only).
+    DevStage* d_slots = nullptr;
+    StageRec* h_rec = nullptr;
+    StageRec* d_rec = nullptr;
+    unsigned long long* d_dig2 = nullptr;  // [2 parities][2 groups][kDigits]
+    const unsigned long long* peer_dig[kMaxShards] = {};
+    bool peer_dig_ipc[kMaxShards] = {};
+    cudaEvent_t evx[2] = {}, evd[2] = {}, evc[2] = {}, evm[2] = {};
+    cudaEvent_t pevx[kMaxShards][2] = {}, pevd[kMaxShards][2] = {}, pevc[kMaxShards][2] = {};
+    bool peer_ev_ipc[kMaxShards] = {};
+    ShmBarrier* barrier = nullptr;
+    uint64_t device_bytes = 0;
+    // p0/p1 like the reference (sequential Kahan over the global block partials,
+    // statevector.cpp:32-40) for small N under AUTO, or always under KAHAN: then
+    // Sb holds two stage parities and every finalize gathers the G shards'
+    // partials through peer pointers; otherwise the exact digit sum.
+    bool kahan = false;
+    const double* peer_S[kMaxShards] = {};
+    bool peer_S_ipc[kMaxShards] = {};
+    double* Scat = nullptr;   // kahan: [2][nb_total] gathered partials
+    double* d_p = nullptr;    // kahan step API: p0, p1
 };
 
 namespace {
@@ -118,7 +204,7 @@ StageParams local_params(const shs_shard* sh, uint32_t s, bool use_p) {
     p.m_sh = sh->a_pows[s] != 1 ? shoup(p.m, sh->N) : 0;
     p.m_step = sh->a_pows[s] != 1 ? mulmod(p.m, kBlock, sh->N) : 0;
     p.sc = sh->sc;
-    p.S = sh->Sb;
+    p.S = sh->Sb;  // (a kahan run selects the stage parity: launch_run_probs)
     p.nb = sh->nb;
     p.partials = sh->partials;
     p.nchunks = sh->nchunks;
@@ -157,6 +243,28 @@ void release(shs_shard* sh) {
     if (sh->h_digits) cudaFreeHost(sh->h_digits);
     for (auto& e : sh->ev)
         if (e) cudaEventDestroy(e);
+    for (uint32_t q = 0; q < sh->G; ++q) {
+        if (sh->peer_dig_ipc[q] && sh->peer_dig[q])
+            cudaIpcCloseMemHandle(const_cast<unsigned long long*>(sh->peer_dig[q]));
+        if (sh->peer_ev_ipc[q])
+            for (int k = 0; k < 2; ++k) {  // opened IPC events are released like events
+                if (sh->pevx[q][k]) cudaEventDestroy(sh->pevx[q][k]);
+                if (sh->pevd[q][k]) cudaEventDestroy(sh->pevd[q][k]);
+                if (sh->pevc[q][k]) cudaEventDestroy(sh->pevc[q][k]);
+            }
+    }
+    for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t e : {sh->evx[k], sh->evd[k], sh->evc[k], sh->evm[k]})
+            if (e) cudaEventDestroy(e);
+    cudaFree(sh->d_slots);
+    if (sh->h_rec) cudaFreeHost(sh->h_rec);
+    cudaFree(sh->d_dig2);
+    cudaFree(sh->Scat);
+    cudaFree(sh->d_p);
+    for (uint32_t q = 0; q < sh->G; ++q)
+        if (sh->peer_S_ipc[q] && sh->peer_S[q])
+            cudaIpcCloseMemHandle(const_cast<double*>(sh->peer_S[q]));
+    delete sh->barrier;
     if (sh->stream) cudaStreamDestroy(sh->stream);
     delete sh;
 }
@@ -165,7 +273,502 @@ bool stage_needs_exchange(const shs_shard* sh, uint32_t s) {
     return !sh->e1 && sh->a_pows[s] != 1;
 }
 
+
+// The exchange of stage s (exchange.cuh): this rank's round-robin share of the
+// tiles, or the owner-addressed direct pull for stages without a tile plan.
+int launch_exchange(shs_shard* sh, uint32_t s) {
+    const ShardMap map = shard_map(sh);
+    const TilePlanHost& pl = sh->plans[s];
+    if (pl.tiled) {
+        TileParams tp{};
+        tp.N = sh->N;
+        tp.A = pl.A;
+        tp.A_sh = pl.A_sh;
+        tp.m = pl.m;
+        tp.m_sh = pl.m_sh;
+        tp.m_chunk = mulmod(pl.m, kCols, sh->N);
+        tp.H = pl.H;
+        tp.u = pl.u;
+        tp.v = pl.v;
+        tp.du = pl.du;
+        tp.dv = pl.dv;
+        tp.ntiles = pl.ntiles;
+        const uint64_t mine = (pl.ntiles + sh->G - 1 - sh->rank) / sh->G;
+        const int g = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(mine, 1), sh->num_sms));
+        return shard_launch(sh, 1, [&] {
+            k_exchange<<<g, kExchangeThreads, exchange_smem_bytes(), sh->stream>>>(tp, map, sh->rank,
+                                                                                  sh->G);
+        });
+    }
+    StageParams p = local_params(sh, s, false);
+    return shard_launch(sh, 1, [&] {
+        k_exchange_direct<<<grid(sh), kThreads, 0, sh->stream>>>(p, map, sh->buf[sh->parity ^ 1]);
+    });
+}
+
+// Host scalars of stage s for the observed prefix (statevector.cpp:338-349).
+StageScalars shard_scalars(const shs_shard* sh, uint32_t s, u128 prefix, double inv) {
+    const double phi = stage_phase(s, prefix);
+    StageScalars sc{};
+    sc.w0r = sh->w[0];
+    sc.w0i = sh->w[1];
+    sc.w1r = sh->w[2];
+    sc.w1i = sh->w[3];
+    sc.phr = 1.0 * std::cos(phi);  // std::polar(1.0, phi), statevector.cpp:338
+    sc.phi = 1.0 * std::sin(phi);
+    sc.inv = inv;
+    sc.phase_mul = (sh->a_pows[s] != 1 || phi != 0.0) ? 1 : 0;
+    return sc;
+}
+
+// probs(s) of a device-resident run: scalars from slot `dev` (stage 0: the
+// host's, run start e_1), then this shard's exact digits into parity s & 1.
+int launch_run_probs(shs_shard* sh, uint32_t s, const DevStage* dev) {
+    const bool ex = stage_needs_exchange(sh, s);
+    const bool gather = sh->a_pows[s] != 1;
+    StageParams p = local_params(sh, s, ex);
+    p.dev = dev;
+    if (sh->kahan) p.S = sh->Sb + (s & 1) * 2 * sh->nb;  // peers read it in their finalize
+    const int g = grid(sh);
+    unsigned long long* out = sh->d_dig2 + (s & 1) * 2 * kDigits;
+    return shard_launch(sh, 0, [&] {
+        if (sh->e1) {
+            if (gather) k_stage_probs<kSrcGather, true, false><<<g, kThreads, 0, sh->stream>>>(p);
+            else k_stage_probs<kSrcDirect, true, false><<<g, kThreads, 0, sh->stream>>>(p);
+        } else if (ex) {
+            k_stage_probs<kSrcBuffer, false, true><<<g, kThreads, 0, sh->stream>>>(p);
+        } else {
+            k_stage_probs<kSrcDirect, false, true><<<g, kThreads, 0, sh->stream>>>(p);
+        }
+        k_sum_partials<<<1, kFinalizeThreads, 0, sh->stream>>>(sh->partials, g, out);
+    });
+}
+
+// collapse(s) of a device-resident run: group and scalars from slot `dev`
+int launch_run_collapse(shs_shard* sh, uint32_t s, const DevStage* dev) {
+    const bool ex = stage_needs_exchange(sh, s);
+    const bool gather = sh->a_pows[s] != 1;
+    StageParams p = local_params(sh, s, ex);
+    p.dev = dev;
+    const int g = grid(sh);
+    int rc = shard_launch(sh, 2, [&] {
+        if (sh->e1) {
+            if (gather) k_stage_collapse<kSrcGather, true, true><<<g, kThreads, 0, sh->stream>>>(p);
+            else k_stage_collapse<kSrcDirect, true, true><<<g, kThreads, 0, sh->stream>>>(p);
+        } else if (ex) {  // in place over P
+            k_stage_collapse<kSrcBuffer, false, true><<<g, kThreads, 0, sh->stream>>>(p);
+        } else {
+            k_stage_collapse<kSrcDirect, false, true><<<g, kThreads, 0, sh->stream>>>(p);
+        }
+    });
+    if (rc) return rc;
+    sh->parity ^= 1;
+    sh->e1 = false;
+    return SHS_OK;
+}
+
+// the G shards' block partials of stage parity k (kahan combine)
+ShardPartials shard_partials(const shs_shard* sh, int k) {
+    ShardPartials sp{};
+    sp.G = static_cast<int>(sh->G);
+    uint64_t off = 0;
+    for (uint32_t q = 0; q < sh->G; ++q) {
+        const uint64_t lo = uint64_t(q) * sh->S, hi = std::min(sh->N, lo + sh->S);
+        const uint64_t nbq = (hi - lo + kBlock - 1) / kBlock;
+        sp.off[q] = off;
+        sp.S[q] = sh->peer_S[q] + k * 2 * nbq;
+        off += nbq;
+    }
+    sp.off[sh->G] = off;
+    return sp;
+}
+
+#define RUN_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return set_error(SHS_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Device-resident sharded run (IterativeShorEngine::run, statevector.cpp:323-412,
+// over G block shards). `L` = the shards THIS host thread drives: all G of them
+// (one process drives several devices, or virtual shards on one device), or
+// one (one process per GPU, `bar` = the node-local host barrier). Per stage s
+// every shard q enqueues, with no host wait on the GPU:
+//   [exchange stages] wait C_r[s-1] of every peer r (its collapse wrote the sel
+//       q pulls from, and freed the P q pushes into); k_exchange; record X_q[s]
+//   [barrier]  wait X_r[s] (every push into q's P landed)
+//   probs(s) -> k_sum_partials -> digits_q[s & 1]; record D_q[s]
+//   [barrier]  (host) read stage s-1's record: the observed prefix, from which
+//       both candidate phases of stage s+1 are computed with glibc
+//   wait D_r[s]; k_shard_finalize_measure: p0/p1 from the G digit arrays (exact,
+//       so identical on every shard), the measurement, the next scalars;
+//       record M_q[s]; collapse(s); record C_q[s]
+//   [barrier]
+// Barriers order enqueues only (a wait must be enqueued after the record it
+// waits on); events carry two parities, so a record for stage s+2 can never
+// overtake a peer's wait for stage s (the peer passed stage s+1's barriers).
+// Results equal the single engine with SHS_COMBINE_EXACT for every G.
+int shards_run(const std::vector<shs_shard*>& L, ShmBarrier* bar, u64 seed, u64 idx, u128* j_out,
+               u128* js_out, shs_stage_trace* trace) {
+    nvtxRangePushA("shs sharded run (device-resident)");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
+    shs_shard* s0 = L.front();
+    const uint32_t t = s0->t, G = s0->G;
+    for (shs_shard* q : L) {
+        for (uint32_t r = 0; r < G; ++r)
+            if (!q->peer[r][0] || !q->peer_dig[r] || !q->pevd[r][0])
+                return set_error(SHS_INVALID_ARGUMENT, "sharded run: shard " + std::to_string(r) +
+                                                           " not attached to " + std::to_string(q->rank));
+        RUN_CUDA(cudaSetDevice(q->dev));
+        shs_shard_init(q);
+        std::memset(q->h_rec, 0, sizeof(StageRec) * t);
+    }
+    auto barrier = [&]() -> int { return bar ? bar->arrive() : SHS_OK; };
+    auto wait_peers = [&](shs_shard* q, cudaEvent_t (*ev)[2], int k) -> int {
+        for (uint32_t r = 0; r < G; ++r)
+            if (r != q->rank) RUN_CUDA(cudaStreamWaitEvent(q->stream, ev[r][k], 0));
+        return SHS_OK;
+    };
+    MeasureCfg mc{seed, static_cast<u32>(idx), s0->err.kind, s0->err.delta, s0->err.px,
+                  s0->err.py, s0->opt.check_norms};
+    u128 observed = 0, sampled = 0;
+    double inv = 1.0;
+    StageScalars sc = shard_scalars(s0, 0, 0, 1.0);
+    int status = SHS_OK;
+    auto absorb = [&](uint32_t r) -> int {
+        RUN_CUDA(cudaSetDevice(s0->dev));
+        RUN_CUDA(cudaEventSynchronize(s0->evm[r & 1]));
+        StageRec rec;
+        std::memcpy(&rec, s0->h_rec + r, sizeof(rec));
+        if (!rec.done) return set_error(SHS_CUDA_ERROR, "stage record missing");
+        if (trace) {
+            trace[r].cbit = r;
+            trace[r].p1 = rec.p1;
+            trace[r].sampled_bit = rec.sbit;
+            trace[r].observed_bit = rec.obit;
+            trace[r].classical_flip = static_cast<uint8_t>(rec.flip);
+            trace[r].quantum_error_branch = static_cast<uint8_t>(rec.ebranch);
+        }
+        if (rec.status == SHS_ERROR)
+            return set_error(SHS_ERROR, "statevector norm drifted beyond 1e-9 at stage " +
+                                            std::to_string(r));
+        if (rec.status == SHS_DEGENERATE_BRANCH)
+            return set_error(SHS_DEGENERATE_BRANCH,
+                             "impossible measurement branch at stage " + std::to_string(r));
+        observed |= u128{static_cast<unsigned>(rec.obit)} << r;
+        sampled |= u128{static_cast<unsigned>(rec.sbit)} << r;
+        if (r + 1 < t) {
+            const int src_group = rec.ebranch ? 1 - rec.sbit : rec.sbit;
+            inv = 1.0 / std::sqrt(src_group == 1 ? rec.p1 : rec.p0);  // statevector.cpp:391
+            sc = shard_scalars(s0, r + 1, observed, inv);
+        }
+        return SHS_OK;
+    };
+    auto drain = [&](int code) {
+        for (shs_shard* q : L) {
+            cudaSetDevice(q->dev);
+            cudaStreamSynchronize(q->stream);  // queued stages fold zeros (inv = 0)
+            q->pending = false;
+        }
+        return code;
+    };
+    for (uint32_t s = 0; s < t; ++s) {
+        const int k = s & 1;
+        const bool ex = stage_needs_exchange(s0, s);
+        if (ex) {
+            for (shs_shard* q : L) {
+                RUN_CUDA(cudaSetDevice(q->dev));
+                if (s > 0 && (status = wait_peers(q, q->pevc, (s - 1) & 1))) return drain(status);
+                if ((status = launch_exchange(q, s))) return drain(status);
+                RUN_CUDA(cudaEventRecord(q->evx[k], q->stream));
+            }
+            if ((status = barrier())) return drain(status);
+            for (shs_shard* q : L) {
+                RUN_CUDA(cudaSetDevice(q->dev));
+                if ((status = wait_peers(q, q->pevx, k))) return drain(status);
+            }
+        }
+        for (shs_shard* q : L) {
+            RUN_CUDA(cudaSetDevice(q->dev));
+            q->sc = sc;  // stage 0's kernel arguments (later stages read the slot)
+            q->ps = s;
+            if ((status = launch_run_probs(q, s, s == 0 ? nullptr : q->d_slots + k)))
+                return drain(status);
+            RUN_CUDA(cudaEventRecord(q->evd[k], q->stream));
+        }
+        if ((status = barrier())) return drain(status);
+        if (s > 0 && (status = absorb(s - 1))) return drain(status);
+        MeasureStep ms{};
+        ms.cfg = mc;
+        ms.s = s;
+        ms.collapse = s + 1 < t ? 1 : 0;
+        ms.init_cur = s == 0 ? 1 : 0;
+        ms.sc0 = sc;
+        if (s + 1 < t)
+            for (int bit = 0; bit < 2; ++bit) {
+                const StageScalars c =
+                    shard_scalars(s0, s + 1, observed | (u128{static_cast<unsigned>(bit)} << s), 0.0);
+                ms.nph.phr[bit] = c.phr;
+                ms.nph.phi[bit] = c.phi;
+                ms.nph.phase_mul[bit] = c.phase_mul;
+            }
+        for (shs_shard* q : L) {
+            RUN_CUDA(cudaSetDevice(q->dev));
+            if ((status = wait_peers(q, q->pevd, k))) return drain(status);
+            ms.cur = q->d_slots + k;
+            ms.next = q->d_slots + (k ^ 1);
+            ms.rec = q->d_rec;
+            if (q->kahan) {  // the reference's sequential Kahan over all G shards' partials
+                const ShardPartials sp = shard_partials(q, k);
+                const uint64_t nbt = sp.off[G];
+                const int gg = static_cast<int>(std::min<uint64_t>((2 * nbt + 255) / 256, 1024));
+                k_shard_gather_partials<<<gg, 256, 0, q->stream>>>(sp, q->Scat);
+                k_finalize_measure<<<1, kFinalizeThreads, 0, q->stream>>>(nullptr, 0, q->Scat, nbt, 1, ms);
+                q->launches += 2;
+            } else {
+                ShardDigits sd{};
+                sd.G = static_cast<int>(G);
+                for (uint32_t r = 0; r < G; ++r) sd.d[r] = q->peer_dig[r] + k * 2 * kDigits;
+                k_shard_finalize_measure<<<1, 2 * kDigits, 0, q->stream>>>(sd, ms);
+                q->launches++;
+            }
+            RUN_CUDA(cudaGetLastError());
+            RUN_CUDA(cudaEventRecord(q->evm[k], q->stream));
+            if (s + 1 < t) {
+                if ((status = launch_run_collapse(q, s, q->d_slots + k))) return drain(status);
+                RUN_CUDA(cudaEventRecord(q->evc[k], q->stream));
+            }
+        }
+        if ((status = barrier())) return drain(status);
+    }
+    if ((status = absorb(t - 1))) return drain(status);
+    for (shs_shard* q : L) {
+        RUN_CUDA(cudaSetDevice(q->dev));
+        RUN_CUDA(cudaStreamSynchronize(q->stream));
+        // shard state as the host-driven loop leaves it: stage t-1 pending
+        q->ps = t - 1;
+        q->inv = inv;
+        q->sc = sc;
+        q->pending = true;
+        q->exchanged = stage_needs_exchange(q, t - 1) ? static_cast<int>(t - 1) : -1;
+    }
+    // the collapses advanced parity / e1; the pending stage t-1 read its sel from
+    // the parity before the last (absent) collapse, i.e. the current one
+    u128 j = observed;
+    if (s0->err.kind == SHS_ERR_BITFLIP)
+        j = bitflip_bitstring(j, t, s0->err.delta, seed, static_cast<u32>(idx));
+    *j_out = j;
+    if (js_out) *js_out = sampled;
+    return SHS_OK;
+}
+
+namespace {
+}  // namespace
+
+
+// ---------------------------------------------------------------------------
+// In-process groups (shard_group.hpp)
+
+int plan_devices(uint64_t N, int first_device, std::vector<int>* devices) {
+    devices->clear();
+    if (const char* env = std::getenv("SHS_DEVICES")) {  // e.g. "0,1" or "0,0" (virtual shards)
+        std::string v(env);
+        size_t pos = 0;
+        while (pos <= v.size()) {
+            size_t e = v.find(',', pos);
+            if (e == std::string::npos) e = v.size();
+            if (e > pos) devices->push_back(std::atoi(v.substr(pos, e - pos).c_str()));
+            pos = e + 1;
+        }
+        if (devices->empty()) return set_error(SHS_INVALID_ARGUMENT, "SHS_DEVICES is empty");
+        return SHS_OK;
+    }
+    const double need = 32.0 * static_cast<double>(N);  // sel + successor (or P) per amplitude
+    const double slack = 2.0e9;                         // partials, plans, scratch
+    if (need + slack <= 16.0e9) {  // fits any B200: no device query per engine
+        devices->push_back(first_device);
+        return SHS_OK;
+    }
+    int ndev = 0;
+    RUN_CUDA(cudaGetDeviceCount(&ndev));
+    size_t fr = 0, tot = 0;
+    RUN_CUDA(cudaSetDevice(first_device));
+    RUN_CUDA(cudaMemGetInfo(&fr, &tot));
+    if (need + slack <= static_cast<double>(fr)) {
+        devices->push_back(first_device);
+        return SHS_OK;
+    }
+    for (int G = 2; G <= std::min(ndev, kMaxShards); ++G)
+        if (need / G + slack <= static_cast<double>(fr)) {
+            for (int q = 0; q < G; ++q) devices->push_back((first_device + q) % ndev);
+            return SHS_OK;
+        }
+    return set_error(SHS_CUDA_ERROR, "the state (" + std::to_string(need / 1e9) +
+                                         " GB) does not fit the " + std::to_string(ndev) +
+                                         " visible device(s)");
+}
+
+void group_destroy(ShardGroup* g) {
+    if (!g) return;
+    for (shs_shard* q : g->shards) release(q);
+    delete g;
+}
+
+int group_create(const shs_problem& problem, const shs_error& error, const shs_options& options,
+                 const std::vector<int>& devices, ShardGroup** out) {
+    auto* g = new ShardGroup;
+    const uint32_t G = static_cast<uint32_t>(devices.size());
+    for (uint32_t q = 0; q < G; ++q) {
+        shs_options o = options;
+        o.device = devices[q];
+        o.n_devices = 0;
+        o.devices = nullptr;
+        shs_shard* sh = nullptr;
+        int rc = shs_shard_create(&problem, &error, &o, q, G, &sh);
+        if (rc) {
+            group_destroy(g);
+            return rc;
+        }
+        g->shards.push_back(sh);
+    }
+    for (shs_shard* a : g->shards)
+        for (shs_shard* b : g->shards)
+            if (a != b) {
+                int rc = shs_shard_attach_local(a, b);
+                if (rc) {
+                    group_destroy(g);
+                    return rc;
+                }
+            }
+    g->N = problem.N;
+    g->S = g->shards[0]->S;
+    g->t = problem.t;
+    *out = g;
+    return SHS_OK;
+}
+
+int group_run(ShardGroup* g, u64 seed, u64 idx, u128* j, u128* js, shs_stage_trace* trace) {
+    int rc = shards_run(g->shards, nullptr, seed, idx, j, js, trace);
+    g->pending = rc == SHS_OK;
+    return rc;
+}
+
+int group_state_init(ShardGroup* g) {
+    for (shs_shard* q : g->shards) shs_shard_init(q);
+    g->pending = false;
+    return SHS_OK;
+}
+
+// the per-gate path over the group: exchange on every shard, then probs and the
+// exact digit sum (what the device-resident run does on the device)
+int group_stage_probs(ShardGroup* g, uint32_t s, u128 prefix, double* p0, double* p1) {
+    int rc;
+    for (shs_shard* q : g->shards)
+        if ((rc = shs_shard_exchange(q, s))) return rc;
+    for (shs_shard* q : g->shards)
+        if ((rc = shs_shard_sync(q))) return rc;
+    uint64_t total[SHS_DIGITS] = {}, d[SHS_DIGITS];
+    for (shs_shard* q : g->shards) {
+        if ((rc = shs_shard_probs(q, s, static_cast<uint64_t>(prefix),
+                                  static_cast<uint64_t>(prefix >> 64), d)))
+            return rc;
+        for (int i = 0; i < SHS_DIGITS; ++i) total[i] += d[i];
+    }
+    shs_digits_to_probs(total, &g->p0, &g->p1);
+    if (g->shards[0]->kahan) {  // the reference's Kahan over every shard's partials (parity 0)
+        shs_shard* q = g->shards[0];
+        RUN_CUDA(cudaSetDevice(q->dev));
+        const ShardPartials sp = shard_partials(q, 0);
+        const uint64_t nbt = sp.off[q->G];
+        const int gg = static_cast<int>(std::min<uint64_t>((2 * nbt + 255) / 256, 1024));
+        k_shard_gather_partials<<<gg, 256, 0, q->stream>>>(sp, q->Scat);
+        k_finalize<<<1, kFinalizeThreads, 0, q->stream>>>(nullptr, 0, q->Scat, nbt, 1, q->d_p);
+        RUN_CUDA(cudaGetLastError());
+        double pp[2];
+        RUN_CUDA(cudaMemcpyAsync(pp, q->d_p, sizeof(pp), cudaMemcpyDeviceToHost, q->stream));
+        RUN_CUDA(cudaStreamSynchronize(q->stream));
+        g->p0 = pp[0];
+        g->p1 = pp[1];
+    }
+    *p0 = g->p0;
+    *p1 = g->p1;
+    g->pending = true;
+    if (g->shards[0]->opt.check_norms && std::fabs(g->p0 + g->p1 - 1.0) > kNormTolerance)
+        return set_error(SHS_ERROR, "statevector norm drifted beyond 1e-9 at stage " +
+                                        std::to_string(s));
+    return SHS_OK;
+}
+
+int group_stage_collapse(ShardGroup* g, int src_group, double p_src) {
+    int rc;
+    for (shs_shard* q : g->shards)
+        if ((rc = shs_shard_collapse(q, src_group, p_src))) return rc;
+    for (shs_shard* q : g->shards)
+        if ((rc = shs_shard_sync(q))) return rc;
+    g->pending = false;
+    return SHS_OK;
+}
+
+template <typename F>
+int group_read_ranges(ShardGroup* g, uint64_t first, uint64_t count, double* host, F&& read) {
+    std::fill(host, host + 2 * count, 0.0);
+    for (shs_shard* q : g->shards) {
+        const uint64_t a = std::max(first, q->lo), b = std::min(first + count, q->hi);
+        if (a >= b) continue;
+        int rc = read(q, a, b - a, host + 2 * (a - first));
+        if (rc) return rc;
+    }
+    return SHS_OK;
+}
+
+int group_state_read(ShardGroup* g, int x, uint64_t first, uint64_t count, double* host) {
+    return group_read_ranges(g, first, count, host, [&](shs_shard* q, uint64_t a, uint64_t n,
+                                                        double* out) {
+        return shs_shard_state_read(q, x, a, n, out);
+    });
+}
+
+int group_stage_read(ShardGroup* g, int x, uint64_t first, uint64_t count, double* host) {
+    return group_read_ranges(g, first, count, host, [&](shs_shard* q, uint64_t a, uint64_t n,
+                                                        double* out) {
+        return shs_shard_stage_read(q, x, a, n, out);
+    });
+}
+
+int group_state_gather(ShardGroup* g, int x, const uint64_t* idx, uint64_t count, double* host) {
+    // one contiguous read per index (the parity checks gather a few thousand points)
+    for (uint64_t i = 0; i < count; ++i) {
+        double v[2] = {0.0, 0.0};
+        if (idx[i] < g->N) {
+            shs_shard* q = g->shards[std::min<uint64_t>(idx[i] / g->S, g->shards.size() - 1)];
+            int rc = shs_shard_state_read(q, x, idx[i], 1, v);
+            if (rc) return rc;
+        }
+        host[2 * i] = v[0];
+        host[2 * i + 1] = v[1];
+    }
+    return SHS_OK;
+}
+
+uint64_t group_launches(const ShardGroup* g) {
+    uint64_t n = 0;
+    for (const shs_shard* q : g->shards) n += q->launches;
+    return n;
+}
+
+int shard_device(const shs_shard* sh) { return sh->dev; }
+
+uint64_t group_device_bytes(const ShardGroup* g) {
+    uint64_t n = 0;
+    for (const shs_shard* q : g->shards) n += q->device_bytes;
+    return n;
+}
 
 extern "C" {
 
@@ -256,8 +859,16 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
     for (int b = 0; b < 2; ++b)
         if ((ce = cudaMalloc(&sh->buf[b], sizeof(double2) * sh->nloc)) != cudaSuccess)
             return fail(ce, "cudaMalloc(shard buffer)");
-    if ((ce = cudaMalloc(&sh->Sb, sizeof(double) * 2 * sh->nb)) != cudaSuccess)
+    const uint64_t nb_total = (sh->N + kBlock - 1) / kBlock;
+    sh->kahan = o.combine == SHS_COMBINE_KAHAN ||
+                (o.combine == SHS_COMBINE_AUTO && nb_total <= kKahanMaxBlocks);
+    if ((ce = cudaMalloc(&sh->Sb, sizeof(double) * 2 * sh->nb * (sh->kahan ? 2 : 1))) != cudaSuccess)
         return fail(ce, "cudaMalloc(block sums)");
+    if (sh->kahan) {
+        if ((ce = cudaMalloc(&sh->Scat, sizeof(double) * 2 * nb_total)) != cudaSuccess ||
+            (ce = cudaMalloc(&sh->d_p, sizeof(double) * 2)) != cudaSuccess)
+            return fail(ce, "cudaMalloc(kahan scratch)");
+    }
     if ((ce = cudaMalloc(&sh->partials, sizeof(unsigned long long) * 2 * kDigits * sh->grid_cap)) !=
         cudaSuccess)
         return fail(ce, "cudaMalloc(partials)");
@@ -268,13 +879,85 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
         return fail(ce, "cudaHostAlloc");
     for (auto& e : sh->ev)
         if ((ce = cudaEventCreate(&e)) != cudaSuccess) return fail(ce, "cudaEventCreate");
+    // device-resident run state (shard_run)
+    if ((ce = cudaMalloc(&sh->d_slots, 2 * sizeof(DevStage))) != cudaSuccess)
+        return fail(ce, "cudaMalloc(slots)");
+    if ((ce = cudaHostAlloc(&sh->h_rec, sizeof(StageRec) * sh->t, cudaHostAllocMapped)) != cudaSuccess)
+        return fail(ce, "cudaHostAlloc(records)");
+    if ((ce = cudaHostGetDevicePointer(reinterpret_cast<void**>(&sh->d_rec), sh->h_rec, 0)) !=
+        cudaSuccess)
+        return fail(ce, "cudaHostGetDevicePointer");
+    if ((ce = cudaMalloc(&sh->d_dig2, sizeof(unsigned long long) * 4 * kDigits)) != cudaSuccess)
+        return fail(ce, "cudaMalloc(stage digits)");
+    if ((ce = cudaMemset(sh->d_dig2, 0, sizeof(unsigned long long) * 4 * kDigits)) != cudaSuccess)
+        return fail(ce, "cudaMemset");
+    for (int k = 0; k < 2; ++k) {
+        const unsigned ipc = cudaEventDisableTiming | cudaEventInterprocess;
+        if ((ce = cudaEventCreateWithFlags(&sh->evx[k], ipc)) != cudaSuccess ||
+            (ce = cudaEventCreateWithFlags(&sh->evd[k], ipc)) != cudaSuccess ||
+            (ce = cudaEventCreateWithFlags(&sh->evc[k], ipc)) != cudaSuccess ||
+            (ce = cudaEventCreateWithFlags(&sh->evm[k], cudaEventDisableTiming)) != cudaSuccess)
+            return fail(ce, "cudaEventCreate(run events)");
+        sh->pevx[rank][k] = sh->evx[k];
+        sh->pevd[rank][k] = sh->evd[k];
+        sh->pevc[rank][k] = sh->evc[k];
+    }
+    sh->peer_dig[rank] = sh->d_dig2;
+    sh->peer_S[rank] = sh->Sb;
     sh->peer[rank][0] = sh->buf[0];
     sh->peer[rank][1] = sh->buf[1];
+    sh->device_bytes = 2 * sizeof(double2) * sh->nloc + sizeof(double) * 2 * sh->nb +
+                       sizeof(unsigned long long) * (2 * kDigits * sh->grid_cap + 6 * kDigits);
     *out = sh;
     return SHS_OK;
 }
 
 void shs_shard_destroy(shs_shard* sh) { release(sh); }
+
+int shs_shard_attach_local(shs_shard* sh, shs_shard* peer) {
+    if (!sh || !peer || peer->G != sh->G || peer->rank >= sh->G)
+        return set_error(SHS_INVALID_ARGUMENT, "bad local attach");
+    if (peer == sh) return SHS_OK;
+    void* bufs[2] = {peer->buf[0], peer->buf[1]};
+    int rc = shs_shard_attach(sh, peer->rank, bufs);
+    if (rc) return rc;
+    sh->peer_dig[peer->rank] = peer->d_dig2;
+    sh->peer_S[peer->rank] = peer->Sb;
+    for (int k = 0; k < 2; ++k) {  // cross-device stream waits on events work in-process
+        sh->pevx[peer->rank][k] = peer->evx[k];
+        sh->pevd[peer->rank][k] = peer->evd[k];
+        sh->pevc[peer->rank][k] = peer->evc[k];
+    }
+    sh->peer_ev_ipc[peer->rank] = false;
+    return SHS_OK;
+}
+
+int shs_shards_run(shs_shard* const* shards, uint32_t count, uint64_t seed, uint64_t idx,
+                   uint64_t j[2], uint64_t j_sampled[2], shs_stage_trace* trace) {
+    if (!shards || count == 0 || !j) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    std::vector<shs_shard*> L(shards, shards + count);
+    const uint32_t G = L[0]->G;
+    ShmBarrier* bar = nullptr;
+    if (count < G) {
+        bar = L[0]->barrier;
+        if (!bar)
+            return set_error(SHS_INVALID_ARGUMENT,
+                             "sharded run over processes needs shs_shard_set_barrier");
+    }
+    u128 jj = 0, js = 0;
+    int rc = shards_run(L, bar, seed, idx, &jj, &js, trace);
+    if (rc) return rc;
+    j[0] = static_cast<uint64_t>(jj);
+    j[1] = static_cast<uint64_t>(jj >> 64);
+    if (j_sampled) {
+        j_sampled[0] = static_cast<uint64_t>(js);
+        j_sampled[1] = static_cast<uint64_t>(js >> 64);
+    }
+    return SHS_OK;
+}
+
+uint64_t shs_shard_device_bytes(const shs_shard* sh) { return sh ? sh->device_bytes : 0; }
+
 
 int shs_shard_range(const shs_shard* sh, uint64_t out[3]) {
     if (!sh || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
@@ -291,38 +974,108 @@ int shs_shard_buffers(const shs_shard* sh, void* out[2]) {
     return SHS_OK;
 }
 
+// What a peer process needs to reach this shard: its two state buffers, its
+// per-stage digits and its three ordering events per parity.
+struct ShardIpcBlob {
+    cudaIpcMemHandle_t buf[2];
+    cudaIpcMemHandle_t dig;
+    cudaIpcMemHandle_t sb;
+    cudaIpcEventHandle_t evx[2], evd[2], evc[2];
+};
+static_assert(sizeof(ShardIpcBlob) <= SHS_SHARD_IPC_BYTES, "SHS_SHARD_IPC_BYTES too small");
+
 int shs_shard_ipc_handles(const shs_shard* csh, void* out) {
     auto* sh = const_cast<shs_shard*>(csh);
     return shard_guard(sh, [&]() -> int {
-        cudaIpcMemHandle_t h[2];
-        for (int b = 0; b < 2; ++b) SHD_CUDA(cudaIpcGetMemHandle(&h[b], sh->buf[b]));
-        std::memcpy(out, h, sizeof(h));
+        if (!out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+        ShardIpcBlob b;
+        for (int k = 0; k < 2; ++k) SHD_CUDA(cudaIpcGetMemHandle(&b.buf[k], sh->buf[k]));
+        SHD_CUDA(cudaIpcGetMemHandle(&b.dig, sh->d_dig2));
+        SHD_CUDA(cudaIpcGetMemHandle(&b.sb, sh->Sb));
+        for (int k = 0; k < 2; ++k) {
+            SHD_CUDA(cudaIpcGetEventHandle(&b.evx[k], sh->evx[k]));
+            SHD_CUDA(cudaIpcGetEventHandle(&b.evd[k], sh->evd[k]));
+            SHD_CUDA(cudaIpcGetEventHandle(&b.evc[k], sh->evc[k]));
+        }
+        std::memset(out, 0, SHS_SHARD_IPC_BYTES);
+        std::memcpy(out, &b, sizeof(b));
         return SHS_OK;
     });
 }
 
+// Raw device pointers of a peer's buffers, valid in this process. A buffer on
+// another device is reached over NVLink: peer access is enabled here (an
+// explicit error when the devices cannot access each other).
 int shs_shard_attach(shs_shard* sh, uint32_t peer, void* const bufs[2]) {
-    if (!sh || !bufs || peer >= sh->G) return set_error(SHS_INVALID_ARGUMENT, "bad attach");
-    sh->peer[peer][0] = static_cast<double2*>(bufs[0]);
-    sh->peer[peer][1] = static_cast<double2*>(bufs[1]);
-    sh->peer_ipc[peer] = false;
-    return SHS_OK;
+    return shard_guard(sh, [&]() -> int {
+        if (!bufs || peer >= sh->G) return set_error(SHS_INVALID_ARGUMENT, "bad attach");
+        for (int b = 0; b < 2; ++b) {
+            cudaPointerAttributes at{};
+            SHD_CUDA(cudaPointerGetAttributes(&at, bufs[b]));
+            if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+                return set_error(SHS_INVALID_ARGUMENT, "attach: not a device pointer");
+            if (at.device != sh->dev) {
+                int can = 0;
+                SHD_CUDA(cudaDeviceCanAccessPeer(&can, sh->dev, at.device));
+                if (!can)
+                    return set_error(SHS_INVALID_ARGUMENT,
+                                     "attach: device " + std::to_string(sh->dev) +
+                                         " cannot access device " + std::to_string(at.device));
+                cudaError_t pe = cudaDeviceEnablePeerAccess(at.device, 0);
+                if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (pe != cudaSuccess)
+                    return set_error(SHS_CUDA_ERROR, std::string("cudaDeviceEnablePeerAccess: ") +
+                                                         cudaGetErrorString(pe));
+            }
+        }
+        sh->peer[peer][0] = static_cast<double2*>(bufs[0]);
+        sh->peer[peer][1] = static_cast<double2*>(bufs[1]);
+        sh->peer_ipc[peer] = false;
+        return SHS_OK;
+    });
 }
 
 int shs_shard_attach_ipc(shs_shard* sh, uint32_t peer, const void* handles) {
     return shard_guard(sh, [&]() -> int {
         if (!handles || peer >= sh->G) return set_error(SHS_INVALID_ARGUMENT, "bad attach");
         if (peer == sh->rank) return SHS_OK;
-        cudaIpcMemHandle_t h[2];
-        std::memcpy(h, handles, sizeof(h));
-        for (int b = 0; b < 2; ++b) {
+        ShardIpcBlob b;
+        std::memcpy(&b, handles, sizeof(b));
+        for (int k = 0; k < 2; ++k) {
             void* p = nullptr;
-            SHD_CUDA(cudaIpcOpenMemHandle(&p, h[b], cudaIpcMemLazyEnablePeerAccess));
-            sh->peer[peer][b] = static_cast<double2*>(p);
+            SHD_CUDA(cudaIpcOpenMemHandle(&p, b.buf[k], cudaIpcMemLazyEnablePeerAccess));
+            sh->peer[peer][k] = static_cast<double2*>(p);
         }
         sh->peer_ipc[peer] = true;
+        void* d = nullptr;
+        SHD_CUDA(cudaIpcOpenMemHandle(&d, b.dig, cudaIpcMemLazyEnablePeerAccess));
+        sh->peer_dig[peer] = static_cast<const unsigned long long*>(d);
+        sh->peer_dig_ipc[peer] = true;
+        void* sp = nullptr;
+        SHD_CUDA(cudaIpcOpenMemHandle(&sp, b.sb, cudaIpcMemLazyEnablePeerAccess));
+        sh->peer_S[peer] = static_cast<const double*>(sp);
+        sh->peer_S_ipc[peer] = true;
+        for (int k = 0; k < 2; ++k) {
+            SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevx[peer][k], b.evx[k]));
+            SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevd[peer][k], b.evd[k]));
+            SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevc[peer][k], b.evc[k]));
+        }
+        sh->peer_ev_ipc[peer] = true;
         return SHS_OK;
     });
+}
+
+int shs_shard_set_barrier(shs_shard* sh, const char* name) {
+    if (!sh || !name || name[0] != '/')
+        return set_error(SHS_INVALID_ARGUMENT, "barrier name must start with '/'");
+    delete sh->barrier;
+    sh->barrier = new ShmBarrier;
+    int rc = sh->barrier->open(name, sh->G, sh->rank == 0);
+    if (rc) {
+        delete sh->barrier;
+        sh->barrier = nullptr;
+    }
+    return rc;
 }
 
 int shs_shard_init(shs_shard* sh) {
@@ -350,36 +1103,7 @@ int shs_shard_exchange(shs_shard* sh, uint32_t s) {
         for (uint32_t q = 0; q < sh->G; ++q)
             if (!sh->peer[q][0] || !sh->peer[q][1])
                 return set_error(SHS_INVALID_ARGUMENT, "shard " + std::to_string(q) + " not attached");
-        const ShardMap map = shard_map(sh);
-        const TilePlanHost& pl = sh->plans[s];
-        int rc;
-        if (pl.tiled) {
-            TileParams tp{};
-            tp.N = sh->N;
-            tp.A = pl.A;
-            tp.A_sh = pl.A_sh;
-            tp.m = pl.m;
-            tp.m_sh = pl.m_sh;
-            tp.m_chunk = mulmod(pl.m, kCols, sh->N);
-            tp.H = pl.H;
-            tp.u = pl.u;
-            tp.v = pl.v;
-            tp.du = pl.du;
-            tp.dv = pl.dv;
-            tp.ntiles = pl.ntiles;
-            const uint64_t mine = (pl.ntiles + sh->G - 1 - sh->rank) / sh->G;
-            const int g = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(mine, 1), sh->num_sms));
-            rc = shard_launch(sh, 1, [&] {
-                k_exchange<<<g, kExchangeThreads, exchange_smem_bytes(), sh->stream>>>(
-                    tp, map, sh->rank, sh->G);
-            });
-        } else {
-            StageParams p = local_params(sh, s, false);
-            rc = shard_launch(sh, 1, [&] {
-                k_exchange_direct<<<grid(sh), kThreads, 0, sh->stream>>>(p, map,
-                                                                        sh->buf[sh->parity ^ 1]);
-            });
-        }
+        int rc = launch_exchange(sh, s);
         if (rc) return rc;
         sh->exchanged = static_cast<int>(s);
         return SHS_OK;

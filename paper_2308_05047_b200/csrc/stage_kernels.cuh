@@ -373,20 +373,8 @@ struct MeasureStep {
     StageRec* rec;       // [t], host-mapped
 };
 
-static __global__ void __launch_bounds__(kFinalizeThreads)
-    k_finalize_measure(const unsigned long long* __restrict__ partials, int nparts,
-                       const double* __restrict__ S, uint64_t nb, int kahan, MeasureStep ms) {
-    __shared__ unsigned long long acc[2][kDigits];
-    __shared__ double pp[2];
-    if (kahan) {
-        kahan_combine(S, nb, pp);
-    } else {
-        sum_slots(partials, nparts, acc);
-        if (threadIdx.x < 2) pp[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    const double p0 = pp[0], p1 = pp[1];
+// thread 0 of a finalize kernel, once p0/p1 are known
+__device__ __forceinline__ void measure_step(double p0, double p1, const MeasureStep& ms) {
     const DevMeasure mr = measure_dev(p0, p1, ms.cfg, ms.s, ms.collapse != 0);
     StageScalars n = ms.init_cur ? ms.sc0 : ms.cur->sc;
     if (ms.init_cur) ms.cur->sc = ms.sc0;
@@ -406,6 +394,64 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
     r.status = mr.status;
     r.done = 1;
     ms.rec[ms.s] = r;
+}
+
+static __global__ void __launch_bounds__(kFinalizeThreads)
+    k_finalize_measure(const unsigned long long* __restrict__ partials, int nparts,
+                       const double* __restrict__ S, uint64_t nb, int kahan, MeasureStep ms) {
+    __shared__ unsigned long long acc[2][kDigits];
+    __shared__ double pp[2];
+    if (kahan) {
+        kahan_combine(S, nb, pp);
+    } else {
+        sum_slots(partials, nparts, acc);
+        if (threadIdx.x < 2) pp[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) measure_step(pp[0], pp[1], ms);
+}
+
+// Stage s of a device-resident SHARDED run (shard.cu): every shard's finalize
+// sums the G shards' exact digit arrays (integers: order-independent, so every
+// shard computes the same p0/p1 and the same measurement) read through peer
+// pointers, then proceeds as k_finalize_measure for its own slots.
+struct ShardDigits {
+    const unsigned long long* d[16];  // shard q's carry-normalised digits [2][kDigits]
+    int G;
+};
+
+// The G shards' block partials (each [2][nb_q], in shard = block order) copied
+// into one [2][nb_total] array for the reference's sequential Kahan combine
+// (kahan_combine) when a sharded engine combines like the reference (small N).
+struct ShardPartials {
+    const double* S[16];
+    uint64_t off[17];  // first global block of shard q; off[G] = nb_total
+    int G;
+};
+
+static __global__ void k_shard_gather_partials(ShardPartials sp, double* __restrict__ out) {
+    const uint64_t nbt = sp.off[sp.G];
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < 2 * nbt;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t g = i / nbt, b = i - g * nbt;
+        int q = 0;
+        while (q + 1 < sp.G && sp.off[q + 1] <= b) ++q;
+        const uint64_t nbq = sp.off[q + 1] - sp.off[q];
+        out[i] = sp.S[q][g * nbq + (b - sp.off[q])];
+    }
+}
+
+static __global__ void __launch_bounds__(2 * kDigits)
+    k_shard_finalize_measure(ShardDigits sd, MeasureStep ms) {
+    __shared__ unsigned long long acc[2][kDigits];
+    __shared__ double pp[2];
+    unsigned long long s = 0;
+    for (int q = 0; q < sd.G; ++q) s += sd.d[q][threadIdx.x];
+    (&acc[0][0])[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < 2) pp[threadIdx.x] = digits_to_double(acc[threadIdx.x]);
+    __syncthreads();
+    if (threadIdx.x == 0) measure_step(pp[0], pp[1], ms);
 }
 
 // The exact digits of this engine's (or shard's) partial masses: sum of the
@@ -494,6 +540,27 @@ __global__ void k_state_read(const double2* __restrict__ X, uint64_t z0, uint64_
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
          i += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t z = first + i;
+        if (z >= zend || z < z0) {
+            out[i] = make_double2(0.0, 0.0);
+            continue;
+        }
+        double2 v = load_amp<kE1>(X, z, z0);
+        double r, im;
+        cmul(wr, wi, __dmul_rn(v.x, inv), __dmul_rn(v.y, inv), r, im);
+        out[i] = make_double2(r, im);
+    }
+}
+
+// k_state_read at arbitrary global indices idx[i] (the sparse-support parity
+// check reads the 2^(s+1) support points of a dense state this way).
+template <bool kE1>
+__global__ void k_state_gather(const double2* __restrict__ X, uint64_t z0, uint64_t zend,
+                               double wr, double wi, double inv,
+                               const uint64_t* __restrict__ idx, uint64_t count,
+                               double2* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t z = idx[i];
         if (z >= zend || z < z0) {
             out[i] = make_double2(0.0, 0.0);
             continue;

@@ -213,11 +213,23 @@ class SimulatorOptions:
     device: int = 0
     combine: str = "auto"  # "auto" | "kahan" | "exact" (see include/shorsim_b200.h)
     tiling: str = "auto"   # "auto" | "force" | "off"
+    # multi-GPU (include/shorsim_b200.h shs_options.n_devices): None = one device;
+    # a list of ordinals (repeats allowed: virtual shards) shards the state over
+    # them; "auto" = as many devices as the state needs
+    devices: Optional[object] = None
 
     def to_c(self) -> L.shs_options:
-        return L.shs_options(self.shard_count, self.workers, self.qubit_ceiling,
-                             1 if self.check_norms else 0, self.device, L.COMBINE[self.combine],
-                             L.TILING[self.tiling])
+        o = L.shs_options(self.shard_count, self.workers, self.qubit_ceiling,
+                          1 if self.check_norms else 0, self.device, L.COMBINE[self.combine],
+                          L.TILING[self.tiling], 0, None)
+        if self.devices == "auto":
+            o.n_devices = -1
+        elif self.devices is not None and len(self.devices) >= 2:
+            arr = (L.i32 * len(self.devices))(*[int(d) for d in self.devices])
+            o.n_devices = len(self.devices)
+            o.devices = C.cast(arr, C.POINTER(L.i32))
+            o.keep = arr  # the array lives as long as the struct
+        return o
 
 
 @dataclass
@@ -368,6 +380,15 @@ class IterativeShorEngine:
         _raise(self._lib.shs_state_read(self._h, x, first, count, out))
         return out
 
+    def state_gather(self, x: int, idx):
+        """g_x at arbitrary indices (uint64 array-like) -> interleaved (re, im) doubles."""
+        import numpy as np
+        ix = np.ascontiguousarray(idx, dtype=np.uint64)
+        out = np.empty(2 * ix.size, dtype=np.float64)
+        _raise(self._lib.shs_state_gather(self._h, x, ix.ctypes.data_as(C.POINTER(L.u64)),
+                                          ix.size, out.ctypes.data_as(C.POINTER(L.dbl))))
+        return out
+
     def block_sums(self):
         nb = self._lib.shs_num_blocks(self._h)
         out = (L.dbl * (2 * nb))()
@@ -410,6 +431,12 @@ class IterativeShorEngine:
 
     def device_bytes(self) -> int:
         return self._lib.shs_engine_device_bytes(self._h)
+
+    def devices(self) -> List[int]:
+        """CUDA ordinals the state lives on (several when the engine is sharded)."""
+        out = (L.i32 * L.MAX_SHARDS)()
+        n = self._lib.shs_engine_devices(self._h, out, L.MAX_SHARDS)
+        return list(out[:n])
 
 
 def run_iterative_shor(problem: FactoringProblem, error: ErrorConfig, seed: int,

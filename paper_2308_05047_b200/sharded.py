@@ -74,7 +74,7 @@ class Shard:
         return [out[0], out[1]]
 
     def ipc_handles(self) -> bytes:
-        buf = C.create_string_buffer(128)
+        buf = C.create_string_buffer(L.SHS_SHARD_IPC_BYTES)
         _raise(self._lib.shs_shard_ipc_handles(self._h, buf))
         return buf.raw
 
@@ -83,8 +83,15 @@ class Shard:
         _raise(self._lib.shs_shard_attach(self._h, peer, arr))
 
     def attach_ipc(self, peer: int, handles: bytes):
-        buf = C.create_string_buffer(handles, 128)
+        buf = C.create_string_buffer(handles, L.SHS_SHARD_IPC_BYTES)
         _raise(self._lib.shs_shard_attach_ipc(self._h, peer, buf))
+
+    def attach_local(self, peer: "Shard"):
+        """a peer shard of this process: buffers, stage digits and ordering events"""
+        _raise(self._lib.shs_shard_attach_local(self._h, peer._h))
+
+    def set_barrier(self, name: str):
+        _raise(self._lib.shs_shard_set_barrier(self._h, name.encode()))
 
     def init(self):
         _raise(self._lib.shs_shard_init(self._h))
@@ -140,7 +147,7 @@ class LocalGroup:
         for a in self.shards:
             for b in self.shards:
                 if a is not b:
-                    a.attach(b.rank, b.buffers())
+                    a.attach_local(b)
 
     def barrier(self):
         for sh in self.shards:
@@ -154,6 +161,7 @@ class DistGroup:
     """One shard per torch.distributed rank; peers attached through CUDA IPC."""
 
     def __init__(self, shard, attach_ipc: bool = True, device=None):
+        import os
         import torch
         import torch.distributed as dist
         self.dist, self.torch = dist, torch
@@ -165,6 +173,10 @@ class DistGroup:
             for q, h in enumerate(handles):
                 if q != shard.rank:
                     shard.attach_ipc(q, h)
+            # the node-local host barrier of device-resident runs (shs_shards_run)
+            name = [f"/shs_{os.getpid()}_{os.urandom(6).hex()}" if dist.get_rank() == 0 else None]
+            dist.broadcast_object_list(name, src=0)
+            shard.set_barrier(name[0])
             dist.barrier()
 
     def barrier(self):
@@ -238,7 +250,23 @@ class ShardedShorEngine:
         self.group.barrier()  # the next exchange reads every shard's new sel
 
     def run(self, seed: int, bitstring_index: int) -> RunResult:
-        """IterativeShorEngine::run, statevector.cpp:323-412, sharded."""
+        """IterativeShorEngine::run, statevector.cpp:323-412, sharded and
+        device-resident (shs_shards_run): per stage exchange, probs, the exact
+        digit sum and the measurement run on every device, ordered across
+        shards by (IPC) events; the host only enqueues. Collective over the
+        group's processes."""
+        arr = (L.vp * len(self.shards))(*[sh._h for sh in self.shards])
+        j, js = (L.u64 * 2)(), (L.u64 * 2)()
+        tr = (L.shs_stage_trace * self.t)()
+        _raise(L.load().shs_shards_run(arr, len(self.shards), seed, bitstring_index, j, js, tr))
+        trace = [StageTrace(x.cbit, x.p1, x.sampled_bit, x.observed_bit,
+                            ErrorEvent(bool(x.classical_flip), bool(x.quantum_error_branch)))
+                 for x in tr]
+        return RunResult(BitString(self.t, j[0] | (j[1] << 64)), js[0] | (js[1] << 64), trace)
+
+    def run_stepwise(self, seed: int, bitstring_index: int) -> RunResult:
+        """The same run sequenced from the host through the per-stage calls
+        (exchange / probs / digit allreduce / host sampling / collapse)."""
         self.state_init()
         observed = sampled = 0
         trace = []

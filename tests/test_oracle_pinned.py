@@ -172,3 +172,43 @@ def test_index_map_matches_reference_live(oracle, reference):
         n = N.bit_length() + 1
         plan = reference.plan(a, N, n, 2)
         assert oracle.index_map(a, N, 0, N) == plan["gather"]
+
+
+def _sparse_vs_dense(oracle, reference, N, a, t, err, seed, bits_rng):
+    """so_sparse (the config-4 checker) == so_engine (and the reference's per-gate
+    state) on a seeded forced sequence: p0/p1 in both combine modes, every support
+    amplitude, and zero off the support."""
+    import numpy as np
+    L = N.bit_length()
+    d = oracle.engine(N, a, L, t, err)
+    sp = oracle.sparse(N, a, L, t, err)
+    d.state_init()
+    sp.state_init()
+    prefix = 0
+    for s in range(t):
+        for mode in (1, 0):  # exact first: the Kahan call leaves the pending state the same
+            q = d.stage_probs(s, prefix, mode)
+            r = sp.stage_probs(s, prefix, mode)
+            assert q == r, (N, s, mode)
+        b = bits_rng.randrange(2) if min(q) > 1e-6 else int(q[1] > q[0])
+        d.collapse(b, q[b])
+        sp.collapse(b, r[b])
+        for x in (0, 1):
+            z, v = sp.state(x)
+            full = np.frombuffer(d.state_read(x, 0, N), dtype=np.float64).reshape(-1, 2)
+            assert np.array_equal(full[z.astype(np.int64)].ravel(), v), (N, s, x)
+            mask = np.ones(N, bool)
+            mask[z.astype(np.int64)] = False
+            assert not np.any(full[mask]), (N, s, x)
+        prefix |= b << s
+
+
+def test_sparse_support_oracle_equals_dense(oracle, reference):
+    from oracle import make_error
+    rng = random.Random(5)
+    cases = [(1048351, 12345, 14, make_error("phase_init", 0.1)),      # threaded dense path
+             (196597, 3, 16, make_error()),                            # orbit wraps early
+             (4087, 1001, 24, make_error("amplitude_init", 0.15)),     # support saturates
+             (15, 7, 8, make_error())]                                 # identity stages
+    for N, a, t, err in cases:
+        _sparse_vs_dense(oracle, reference, N, a, t, err, 3, rng)

@@ -89,7 +89,7 @@ def _run_cases(rank, world, dist, q):
                                         shs.DistGroup(shard, attach_ipc=False))
             ref = orc.engine(N, a, N.bit_length(), t, oe)
             for idx in range(2):
-                r = eng.run(17, idx)
+                r = eng.run_stepwise(17, idx)
                 o = ref.run(17, idx, 1)  # oracle with the exact combine
                 results.append((N, idx, r.bits.j == o["j"], [x.p1 for x in r.trace] == o["p1"],
                                 r.j_sampled == o["j_sampled"]))
