@@ -545,10 +545,16 @@ def config3_runs(shs):
 
 
 def run_sharded(args):
-    """N > 1 GPUs: one shard of the config-4 state per rank (strong scaling, the
-    same N), peers attached through CUDA IPC, barriers / digit allreduce over
-    NCCL. A step is one non-identity stage: exchange + probs + allreduce +
-    measurement + collapse."""
+    """N > 1 GPUs (one process per GPU under torchrun): one block shard of the
+    config-4 state per rank (strong scaling: the same N as at 1 GPU). Peers
+    attach through CUDA IPC (buffers, stage digits, ordering events).
+
+    step (value, ms_per_step): one non-identity stage through the per-stage
+    shard API, as at 1 GPU: exchange -> probs -> digit allreduce -> measurement
+    -> collapse, device time max over ranks.
+    e2e: full device-resident runs through ShardedShorEngine.run
+    (shs_shards_run: no host round trip per stage; stages ordered across ranks
+    by IPC events), wall time max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -556,7 +562,7 @@ def run_sharded(args):
 
     ws, rank, local = dist_env()
     # SHS_BENCH_BACKEND=gloo lets the multi-rank path run with ranks sharing a GPU
-    # (a functional check only: host-side barriers, no kernel waits on another rank)
+    # (functional check: the kernels never wait on another rank's kernels)
     backend = os.environ.get("SHS_BENCH_BACKEND", "nccl")
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
@@ -565,6 +571,13 @@ def run_sharded(args):
         dist.init_process_group("nccl", device_id=dev)
     else:
         dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else None
+
+    def max_over_ranks(x):
+        tt = torch.tensor([float(x)], device=cdev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
     w = WORKLOADS[args.workload]
     N, a = w["N"], w["a"]
     prob = shs.FactoringProblem.make(N, a)
@@ -572,7 +585,7 @@ def run_sharded(args):
     err = shs.ErrorConfig()
     opts = shs.SimulatorOptions(device=local, qubit_ceiling=64, combine="exact")
     shard = shs.Shard(prob, err, opts, rank, ws)
-    group = shs.DistGroup(shard, attach_ipc=True, device=dev if backend == "nccl" else None)
+    group = shs.DistGroup(shard, attach_ipc=True, device=cdev)
     eng = shs.ShardedShorEngine(prob, err, opts, [shard], group)
     stream = torch.cuda.ExternalStream(shard.stream_handle(), device=dev)
     seed = 2308
@@ -604,10 +617,7 @@ def run_sharded(args):
     ev1.synchronize()
     dist.barrier()
     clock_info = clocks.stop()
-    cdev = dev if backend == "nccl" else None
-    ms = torch.tensor([ev0.elapsed_time(ev1)], device=cdev, dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_per_step = float(ms.item()) / args.steps
+    ms_per_step = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
     launches = shard.launch_count() - launches0
 
     shard.set_timing(True)
@@ -615,22 +625,27 @@ def run_sharded(args):
         step()
     kt = shard.kernel_times()
     shard.set_timing(False)
-    kms = {k: v[0] / max(v[1], 1) for k, v in kt.items()}
-    tms = torch.tensor([kms["probs"], kms["exchange"], kms["collapse"]], device=cdev,
-                       dtype=torch.float64)
-    dist.all_reduce(tms, op=dist.ReduceOp.MAX)
-    kms = dict(zip(["probs", "exchange", "collapse"], tms.tolist()))
+    kms = {k: max_over_ranks(v[0] / max(v[1], 1)) for k, v in kt.items()}
     nloc = shard.hi - shard.lo
-    nvlink_bytes = 16 * nloc * (ws - 1) / ws  # per GPU per direction
-    nvlink_peak = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
+    # exchange (exchange.cuh): every rank executes a round-robin share of the
+    # tiles, pulling 512 B source runs from their owners and pushing 512 B row
+    # runs into the owners' P: per GPU and direction 2 x 16 B x (N/G)(G-1)/G
+    # cross the links (the all-to-all minimum is half that)
+    nvlink_bytes = 32 * nloc * (ws - 1) / ws
+    nvlink_min_bytes = 16 * nloc * (ws - 1) / ws
+    nvlink_peak = 900.0  # GB/s per direction per GPU (NVLink 5, north_star)
     hbm_peak, peak_src = peaks()
     ex_gbs = nvlink_bytes / (kms["exchange"] * 1e-3) / 1e9 if kms["exchange"] else None
+    local_ms = kms["probs"] + kms["collapse"]
+    local_gbs = 80 * nloc / (local_ms * 1e-3) / 1e9 if local_ms else None
 
+    res = eng.run(seed, 1000)  # warm the device-resident path
+    e2e_runs = max(1, args.e2e_runs)
+    dist.barrier()
     t0 = time.perf_counter()
-    res = eng.run(seed, 1000)
-    run_s = torch.tensor([time.perf_counter() - t0], device=cdev, dtype=torch.float64)
-    dist.all_reduce(run_s, op=dist.ReduceOp.MAX)
-    run_s = float(run_s.item())
+    for i in range(e2e_runs):
+        res = eng.run(seed, 1001 + i)
+    run_s = max_over_ranks((time.perf_counter() - t0) / e2e_runs)
 
     line = {
         "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": ws,
@@ -639,22 +654,27 @@ def run_sharded(args):
         "data": "synthetic: the deterministic iterative-Shor state from |1> (no dataset)",
         "config": {"workload": args.workload, "desc": w["desc"], "N": N, "a": a, "t": t,
                    "shard_amplitudes": nloc, "parallelism": f"{ws} shards (block-sharded state)",
+                   "backend": backend,
                    "l2": "state far larger than L2: no flush needed"},
         "s_per_run": run_s,
-        "s_per_run_dense": run_s_dense,
-        "sparse_prefix_stages": sparse_stages,
+        "s_per_run_dense": run_s,
+        "sparse_prefix_stages": 0,
         "kernels_max_over_ranks_ms": kms,
-        "roofline": {"kernel": "k_stage_probs/collapse (shard-local) + k_exchange", "bound": "hbm",
-                     "achieved": 96 * nloc / ((kms["probs"] + kms["collapse"] + kms["exchange"]) * 1e-3) / 1e9,
-                     "peak": hbm_peak, "unit": "GB/s", "peak_source": peak_src, "traffic": None,
-                     "frac": 96 * nloc / ((kms["probs"] + kms["collapse"] + kms["exchange"]) * 1e-3) / 1e9 / hbm_peak,
-                     "bytes_per_amp": 96},
+        "roofline": {"kernel": "k_stage_probs + k_stage_collapse <kSrcBuffer> (shard-local)",
+                     "bound": "hbm", "achieved": local_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": local_gbs / hbm_peak if local_gbs else None,
+                     "peak_source": peak_src, "traffic": None, "bytes_per_amp": 80},
         "nvlink": {"kernel": "k_exchange", "achieved": ex_gbs, "peak": nvlink_peak,
                    "unit": "GB/s per direction", "frac": ex_gbs / nvlink_peak if ex_gbs else None,
-                   "bytes_per_gpu_per_direction": nvlink_bytes},
+                   "bytes_per_gpu_per_direction": nvlink_bytes,
+                   "all_to_all_minimum_bytes": nvlink_min_bytes,
+                   "note": "one GPU per process; with ranks sharing a GPU (gloo) the exchange "
+                           "runs over local HBM and this is not an NVLink number"},
         "e2e": {"value": N * t / run_s, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 8 * 80, "last_j": str(res.bits.j),
-                "what": "ShardedShorEngine.run over the C ABI: exchange / probs / digit allreduce / collapse per stage"},
+                "d2h_bytes_per_step": 16, "last_j": str(res.bits.j),
+                "what": "ShardedShorEngine.run over the C ABI (shs_shards_run): exchange, probs, "
+                        "digit sum and measurement on every device, stages ordered across ranks "
+                        "by IPC events; bit string returned to the host"},
         "gpu_launches": launches, "clocks": clock_info,
     }
     if rank == 0:
@@ -662,6 +682,19 @@ def run_sharded(args):
     shard.close()
     dist.destroy_process_group()
     return 0
+
+
+def self_launch(args):
+    """--gpus N > 1 without torchrun: relaunch this script as N ranks."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -677,9 +710,15 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    ws = dist_env()[0]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if ws != args.gpus:
+        print(f"error: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference_arm(args)
-    if dist_env()[0] > 1:
+    if ws > 1:
         return run_sharded(args)
     return run_ours(args)
 

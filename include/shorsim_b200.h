@@ -279,6 +279,12 @@ int shs_shard_state_read(shs_shard* shard, int32_t x, uint64_t first, uint64_t c
                          double* interleaved);
 int shs_shard_stage_read(shs_shard* shard, int32_t x, uint64_t first, uint64_t count,
                          double* interleaved);
+/* 1 when the shards combine p0/p1 like the reference (sequential Kahan over the
+ * global block partials: combine = KAHAN, or AUTO with <= 1024 blocks); then,
+ * once every shard's probs of the stage is done, shs_shard_kahan_probs runs that
+ * combine on this shard's device over all shards' partials (peer pointers) */
+int shs_shard_kahan(const shs_shard* shard);
+int shs_shard_kahan_probs(shs_shard* shard, double* p0, double* p1);
 /* correctly rounded p0, p1 from summed exact digits (host-side, no device) */
 int shs_digits_to_probs(const uint64_t digits[SHS_DIGITS], double* p0, double* p1);
 /* per-kernel CUDA-event times like shs_engine_kernel_times: kind 0 probs,

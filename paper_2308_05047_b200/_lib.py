@@ -102,6 +102,8 @@ SIGNATURES = [
     ("shs_shards_run", C.c_int, [C.POINTER(vp), u32, u64, u64, C.POINTER(u64), C.POINTER(u64),
                                  C.POINTER(shs_stage_trace)]),
     ("shs_shard_device_bytes", u64, [vp]),
+    ("shs_shard_kahan", C.c_int, [vp]),
+    ("shs_shard_kahan_probs", C.c_int, [vp, C.POINTER(dbl), C.POINTER(dbl)]),
     ("shs_shard_init", C.c_int, [vp]),
     ("shs_shard_needs_exchange", C.c_int, [vp, u32]),
     ("shs_shard_exchange", C.c_int, [vp, u32]),

@@ -681,21 +681,8 @@ int group_stage_probs(ShardGroup* g, uint32_t s, u128 prefix, double* p0, double
         for (int i = 0; i < SHS_DIGITS; ++i) total[i] += d[i];
     }
     shs_digits_to_probs(total, &g->p0, &g->p1);
-    if (g->shards[0]->kahan) {  // the reference's Kahan over every shard's partials (parity 0)
-        shs_shard* q = g->shards[0];
-        RUN_CUDA(cudaSetDevice(q->dev));
-        const ShardPartials sp = shard_partials(q, 0);
-        const uint64_t nbt = sp.off[q->G];
-        const int gg = static_cast<int>(std::min<uint64_t>((2 * nbt + 255) / 256, 1024));
-        k_shard_gather_partials<<<gg, 256, 0, q->stream>>>(sp, q->Scat);
-        k_finalize<<<1, kFinalizeThreads, 0, q->stream>>>(nullptr, 0, q->Scat, nbt, 1, q->d_p);
-        RUN_CUDA(cudaGetLastError());
-        double pp[2];
-        RUN_CUDA(cudaMemcpyAsync(pp, q->d_p, sizeof(pp), cudaMemcpyDeviceToHost, q->stream));
-        RUN_CUDA(cudaStreamSynchronize(q->stream));
-        g->p0 = pp[0];
-        g->p1 = pp[1];
-    }
+    if (g->shards[0]->kahan && (rc = shs_shard_kahan_probs(g->shards[0], &g->p0, &g->p1)))
+        return rc;
     *p0 = g->p0;
     *p1 = g->p1;
     g->pending = true;
@@ -957,6 +944,31 @@ int shs_shards_run(shs_shard* const* shards, uint32_t count, uint64_t seed, uint
 }
 
 uint64_t shs_shard_device_bytes(const shs_shard* sh) { return sh ? sh->device_bytes : 0; }
+
+int shs_shard_kahan(const shs_shard* sh) { return sh && sh->kahan ? 1 : 0; }
+
+int shs_shard_kahan_probs(shs_shard* sh, double* p0, double* p1) {
+    return shard_guard(sh, [&]() -> int {
+        if (!sh->kahan) return set_error(SHS_INVALID_ARGUMENT, "shard combines exactly (digits)");
+        if (!p0 || !p1) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+        for (uint32_t r = 0; r < sh->G; ++r)
+            if (!sh->peer_S[r]) return set_error(SHS_INVALID_ARGUMENT, "peer partials not attached");
+        const ShardPartials sp = shard_partials(sh, 0);
+        const uint64_t nbt = sp.off[sh->G];
+        const int gg = static_cast<int>(std::min<uint64_t>((2 * nbt + 255) / 256, 1024));
+        k_shard_gather_partials<<<gg, 256, 0, sh->stream>>>(sp, sh->Scat);
+        k_finalize<<<1, kFinalizeThreads, 0, sh->stream>>>(nullptr, 0, sh->Scat, nbt, 1, sh->d_p);
+        sh->launches += 2;
+        SHD_CUDA(cudaGetLastError());
+        double pp[2];
+        SHD_CUDA(cudaMemcpyAsync(pp, sh->d_p, sizeof(pp), cudaMemcpyDeviceToHost, sh->stream));
+        SHD_CUDA(cudaStreamSynchronize(sh->stream));
+        *p0 = pp[0];
+        *p1 = pp[1];
+        return SHS_OK;
+    });
+}
+
 
 
 int shs_shard_range(const shs_shard* sh, uint64_t out[3]) {

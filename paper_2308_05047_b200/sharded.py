@@ -113,6 +113,15 @@ class Shard:
     def sync(self):
         _raise(self._lib.shs_shard_sync(self._h))
 
+    def kahan(self) -> bool:
+        """p0/p1 combined like the reference (sequential Kahan; small N under AUTO)"""
+        return bool(self._lib.shs_shard_kahan(self._h))
+
+    def kahan_probs(self):
+        p0, p1 = L.dbl(), L.dbl()
+        _raise(self._lib.shs_shard_kahan_probs(self._h, C.byref(p0), C.byref(p1)))
+        return p0.value, p1.value
+
     def state_read(self, x: int, first: int, count: int):
         out = (L.dbl * (2 * count))()
         _raise(self._lib.shs_shard_state_read(self._h, x, first, count, out))
@@ -240,6 +249,9 @@ class ShardedShorEngine:
             digits = [a + b for a, b in zip(digits, d)]
         digits = self.group.allreduce(digits)
         p0, p1 = digits_to_probs(digits)
+        if self.shards[0].kahan():  # the reference's sequential Kahan over all partials
+            self.group.barrier()  # (allreduce ordered the digits; partials are device-side)
+            p0, p1 = self.shards[0].kahan_probs()
         if self.options.check_norms and abs(p0 + p1 - 1.0) > NORM_TOLERANCE:
             raise Error(f"statevector norm drifted beyond 1e-9 at stage {s}")
         return p0, p1

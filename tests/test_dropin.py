@@ -59,9 +59,25 @@ def test_simulate_jsonl_byte_identical(cuda_ok, case):
     assert ours.stdout == ref.stdout
 
 
+@need
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [CASES[0], CASES[3], CASES[8]], ids=["4087", "4087-quantum", "262139"])
+def test_simulate_jsonl_byte_identical_over_virtual_shards(cuda_ok, case):
+    """Row N1: the reference's unchanged harness with the engine sharded over
+    devices (SHS_DEVICES=0,0: two shards on this GPU) — byte-identical JSONL."""
+    args = [x for x in case if x is not None]
+    ref = run(SIMULATE_REF, args)
+    env = dict(os.environ, SHS_DEVICES="0,0")
+    ours = subprocess.run([SIMULATE_B200] + args, capture_output=True, text=True, timeout=600,
+                          env=env)
+    assert ref.returncode == 0, ref.stderr
+    assert ours.returncode == 0, ours.stderr
+    assert ours.stdout == ref.stdout
+
+
 @pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(ACCEPTANCE_B200), reason="not built")
-@pytest.mark.parametrize("criterion", ["2", "10"])
+@pytest.mark.parametrize("criterion", ["1", "2", "10"])
 def test_reference_acceptance_criteria_on_b200(cuda_ok, criterion):
     r = run(ACCEPTANCE_B200, ["--criterion", criterion], timeout=1200)
     print(r.stdout)

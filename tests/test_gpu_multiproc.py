@@ -1,9 +1,10 @@
 """The multi-process sharded path (one shard per torch.distributed rank, peers
-attached through CUDA IPC handles, DistGroup barrier/allreduce) with 2 ranks
-sharing the one GPU of this run over gloo. No kernel waits on another rank: the
-ranks synchronise only on the host between launches (exchange -> barrier ->
-probs -> allreduce -> collapse -> barrier), exactly as across 8 GPUs over NVLink.
-Results must equal the single-GPU engine (exact combine) bit for bit."""
+attached through CUDA IPC handles: buffers, stage digits and ordering events)
+with 2-3 ranks sharing the one GPU of this run. run() is the device-resident
+loop (shs_shards_run): cross-rank order comes from IPC events, a shared-memory
+host barrier only orders their enqueues, and no kernel waits on another rank's
+kernel. run_stepwise() is the host-sequenced driver (gloo barrier/allreduce).
+Both must equal the single-GPU engine (exact combine) bit for bit."""
 import os
 import socket
 
@@ -41,7 +42,9 @@ def _worker(rank, world, port, q):
             eng = shs.ShardedShorEngine(prob, shs.ErrorConfig(), o, [shard],
                                         shs.DistGroup(shard, attach_ipc=True))
             for idx in range(2):
-                r = eng.run(21, idx)
+                r = eng.run(21, idx)  # device-resident: IPC events + shared-memory barrier
+                w = eng.run_stepwise(21, idx)  # host-sequenced per-stage driver
+                assert (w.bits.j, [x.p1 for x in w.trace]) == (r.bits.j, [x.p1 for x in r.trace])
                 out.append((N, idx, r.bits.j, [x.p1 for x in r.trace]))
             dist.barrier()
             shard.close()
@@ -52,12 +55,13 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_process_ipc_shards_match_single_engine(cuda_ok):
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_process_ipc_shards_match_single_engine(cuda_ok, world):
     import paper_2308_05047_b200 as shs
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -67,7 +71,8 @@ def test_two_process_ipc_shards_match_single_engine(cuda_ok):
         res[rank] = out
     for p in procs:
         p.join(timeout=60)
-    assert res[0] == res[1]
+    for r in range(1, world):
+        assert res[r] == res[0]
     k = 0
     for N, a, t, tiling in CASES:
         eng = shs.IterativeShorEngine(shs.FactoringProblem.make(N, a, t), shs.ErrorConfig(),

@@ -65,19 +65,68 @@ def test_virtual_shards_forced_sequence_bit_exact(cuda_ok, G, N, a, t, tiling):
     sharded.close()
 
 
-@pytest.mark.parametrize("err", [E(), E("classical_measure", 0.05), E("amplitude_init", 0.1),
-                                 E("bitflip", 0.02), E("quantum_measure", 0.02, (0.01, 0.01, 0.0))],
-                         ids=["none", "classical", "amplitude", "bitflip", "quantum"])
+def same_run(s, r):
+    assert s.bits.j == r.bits.j and s.j_sampled == r.j_sampled
+    assert [x.p1 for x in s.trace] == [x.p1 for x in r.trace]
+    assert [x.sampled_bit for x in s.trace] == [x.sampled_bit for x in r.trace]
+    assert [x.observed_bit for x in s.trace] == [x.observed_bit for x in r.trace]
+    assert [x.event.classical_flip for x in s.trace] == [x.event.classical_flip for x in r.trace]
+    assert [x.event.quantum_error_branch for x in s.trace] == \
+        [x.event.quantum_error_branch for x in r.trace]
+
+
+ERRS = [E(), E("classical_measure", 0.05), E("amplitude_init", 0.1), E("phase_init", 0.2),
+        E("bitflip", 0.02), E("quantum_measure", 0.02, (0.01, 0.01, 0.0))]
+ERR_IDS = ["none", "classical", "amplitude", "phase", "bitflip", "quantum"]
+
+
+@pytest.mark.parametrize("err", ERRS, ids=ERR_IDS)
 def test_virtual_shards_seeded_runs(cuda_ok, err):
+    """Device-resident sharded runs (shs_shards_run: exchange, probs, digit sum and
+    the measurement on the device, stages ordered by events) and the host-driven
+    per-stage driver equal the single engine."""
     N, a, t = 2097143, 777, 14
     single, sharded = pair(N, a, t, err, 4)
     for idx in range(2):
         r = single.run(11, idx)
-        s = sharded.run(11, idx)
-        assert s.bits.j == r.bits.j and s.j_sampled == r.j_sampled
-        assert [x.p1 for x in s.trace] == [x.p1 for x in r.trace]
-        assert [x.observed_bit for x in s.trace] == [x.observed_bit for x in r.trace]
+        same_run(sharded.run(11, idx), r)
+        same_run(sharded.run_stepwise(11, idx), r)
     sharded.close()
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_virtual_shards_device_run_shard_counts(cuda_ok, G):
+    N, a, t = 4194301, 1234567, 12
+    err = E("phase_init", 0.1)
+    single, sharded = pair(N, a, t, err, G)
+    for idx in range(2):
+        same_run(sharded.run(3, idx), single.run(3, idx))
+    # the pending state after a device-resident run equals the single engine's
+    for x in (0, 1):
+        want = np.ctypeslib.as_array(single.stage_read(x, 0, N))
+        assert np.array_equal(full_state(sharded, x, N, stage=True), want)
+        want = np.ctypeslib.as_array(single.state_read(x, 0, N))
+        assert np.array_equal(full_state(sharded, x, N), want)
+    sharded.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_virtual_shards_kahan_combine_small_n(cuda_ok, G):
+    """Below 1025 blocks (AUTO) the shards combine p0/p1 like the reference, with
+    the sequential Kahan over all shards' partials: p1 traces equal the single
+    engine's (which is bit-identical to the reference there)."""
+    import paper_2308_05047_b200 as shs
+    for N, a, t in [(262139, 31337, 12), (65521 * 3, 5, 14)]:
+        prob = shs.FactoringProblem.make(N, a, t)
+        for err in (E(), E("quantum_measure", 0.03, (0.02, 0.01, 0.05))):
+            single = shs.IterativeShorEngine(prob, err, shs.SimulatorOptions(qubit_ceiling=64))
+            sharded = shs.ShardedShorEngine.virtual(prob, err, shs.SimulatorOptions(qubit_ceiling=64),
+                                                    nshards=G)
+            for idx in range(3):
+                r = single.run(9, idx)
+                same_run(sharded.run(9, idx), r)
+                same_run(sharded.run_stepwise(9, idx), r)
+            sharded.close()
 
 
 def test_virtual_shards_config3_run(cuda_ok):
@@ -85,9 +134,42 @@ def test_virtual_shards_config3_run(cuda_ok):
     N, a = 16777207, 2
     single, sharded = pair(N, a, None, E(), 8)
     r = single.run(5, 0)
-    s = sharded.run(5, 0)
-    assert s.bits.j == r.bits.j and [x.p1 for x in s.trace] == [x.p1 for x in r.trace]
+    same_run(sharded.run(5, 0), r)
     sharded.close()
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0]])
+def test_engine_over_devices_equals_single(cuda_ok, devices):
+    """Row N1: IterativeShorEngine with SimulatorOptions.devices (shs_options.n_devices)
+    is the sharded engine behind the single-engine handle: run(), the step API and
+    state reads all equal the one-device engine (virtual shards on this GPU)."""
+    import paper_2308_05047_b200 as shs
+    N, a, t = 1048351, 12345, 10
+    err = E("amplitude_init", 0.1)
+    prob = shs.FactoringProblem.make(N, a, t)
+    single = shs.IterativeShorEngine(prob, err, opts())
+    multi = shs.IterativeShorEngine(prob, err, opts(devices=devices))
+    assert multi.devices() == devices and single.devices() == [0]
+    for idx in range(3):
+        same_run(multi.run(4, idx), single.run(4, idx))
+    single.state_init()
+    multi.state_init()
+    prefix = 0
+    rng = np.random.default_rng(1)
+    for s in range(t):
+        p = single.stage_probs(s, prefix)
+        assert multi.stage_probs(s, prefix) == p
+        b = int(rng.integers(0, 2)) if min(p) > 1e-6 else int(p[1] > p[0])
+        if s + 1 < t:
+            single.stage_collapse(b, p[b])
+            multi.stage_collapse(b, p[b])
+            idx = rng.integers(0, N, 500).astype(np.uint64)
+            for x in (0, 1):
+                assert np.array_equal(multi.state_gather(x, idx), single.state_gather(x, idx))
+                assert np.array_equal(np.ctypeslib.as_array(multi.state_read(x, N - 3000, 3000)),
+                                      np.ctypeslib.as_array(single.state_read(x, N - 3000, 3000)))
+        prefix |= b << s
+    multi.close()
 
 
 def test_shard_protocol_errors(cuda_ok):
