@@ -294,6 +294,53 @@ int shs_shard_kernel_times(const shs_shard* shard, double ms[3], uint64_t launch
 uint64_t shs_shard_launch_count(const shs_shard* shard);
 void* shs_shard_stream(const shs_shard* shard);
 
+/* ---- the per-gate API on a device-resident state ----
+ * shs_sv = ShardedState (statevector.hpp:33-65): 2^n complex amplitudes in
+ * device memory, the top index bit selects the group (x = 0: [0, 2^(n-1)),
+ * x = 1: [2^(n-1), 2^n)), global indices as the reference's amp()/set_amp().
+ * Gates reproduce the reference's arithmetic bit for bit. */
+typedef struct shs_sv shs_sv;
+/* ShardedState(n, shard_count) zeroed: make_shard_layout's validation and
+ * messages (statevector.cpp:65-72, invalid_argument) */
+int shs_sv_create(uint32_t n, uint32_t shard_count, int32_t device, shs_sv** out);
+int shs_sv_clone(const shs_sv* state, shs_sv** out); /* value copy (device to device) */
+void shs_sv_destroy(shs_sv* state);
+int shs_sv_layout(const shs_sv* state, uint32_t out[2]); /* {n, g}: shard_count = 2^g */
+/* amp / set_amp over [first, first+count), interleaved (re, im) */
+int shs_sv_read(const shs_sv* state, uint64_t first, uint64_t count, double* interleaved);
+int shs_sv_write(shs_sv* state, uint64_t first, uint64_t count, const double* interleaved);
+/* init_state (statevector.cpp:126-131) on this state: zero, then amp(1) = a0,
+ * amp(2^(n-1) + 1) = a1; pair = {a0.re, a0.im, a1.re, a1.im} */
+int shs_sv_init_state(shs_sv* state, const double pair[4]);
+/* apply_oracle (statevector.cpp:223-244): group 1 gathered through
+ * src[y] = a_inv y mod N for y < min(N, 2^(n-1)); NotInvertibleError as the reference */
+int shs_sv_apply_oracle(shs_sv* state, uint64_t a_pow, uint64_t N);
+/* apply_phase (statevector.cpp:246-253): group 1 *= e^{i pi prefix 2^-cbit}, skipped at phi = 0 */
+int shs_sv_apply_phase(shs_sv* state, uint32_t cbit, uint64_t prefix_lo, uint64_t prefix_hi);
+/* apply_hadamard_top (statevector.cpp:255-270) */
+int shs_sv_apply_hadamard_top(shs_sv* state);
+/* {group_norm_squared(0), group_norm_squared(1)} (statevector.cpp:95-117):
+ * fixed 256-blocks, sequential Kahan over the non-zero blocks */
+int shs_sv_group_norms(const shs_sv* state, double out[2]);
+/* reset_top(bit, branch, reinit, p_source) (statevector.cpp:263-283);
+ * DegenerateBranchError below 1e-300 */
+int shs_sv_reset_top(shs_sv* state, int32_t bit, int32_t error_branch, const double reinit[4],
+                     double p_source);
+uint64_t shs_sv_launch_count(const shs_sv* state);
+
+/* build_permutation_plan (statevector.cpp:133-154) on the device: a_inv,
+ * identity, y_limit = min(N, 2^(n-1)); gather[y_limit] (NULL to skip) and
+ * pair_counts[(2^(g-1))^2] row-major [src_xrank][dst_xrank] (NULL to skip) */
+int shs_plan_build(uint64_t a_pow, uint64_t N, uint32_t n, uint32_t shard_count, int32_t device,
+                   uint64_t* a_inv, int32_t* identity, uint64_t* y_limit, uint64_t* gather,
+                   uint64_t* pair_counts);
+/* plan_receive_lists (send = 0) / plan_send_lists (send = 1) for group shard
+ * xrank (statevector.cpp:156-181): counts[2^(g-1)] per peer, indices = the
+ * local indices grouped by ascending peer, each group in the reference's
+ * order (indices needs 2^(n-g) entries) */
+int shs_plan_lists(uint64_t a_pow, uint64_t N, uint32_t n, uint32_t shard_count, uint32_t xrank,
+                   int32_t send, int32_t device, uint64_t* counts, uint64_t* indices);
+
 /* ---- exhaustive_joint_distribution (statevector.hpp:193-198, statevector.cpp:533-579) ----
  * Exact distribution over the 2^t observed bit strings by enumerating every
  * measurement path on the device, error branches marginalised; out receives

@@ -18,6 +18,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -26,6 +27,12 @@
 #include "shorsim_b200.h"
 
 namespace shorsim::b200 {
+
+// CUDA device of engines created without an explicit one: SHS_DEVICE (default 0)
+inline int default_device() {
+    const char* d = std::getenv("SHS_DEVICE");
+    return d ? std::atoi(d) : 0;
+}
 
 // Map a status code to the reference's exception types (errors.hpp:8-43).
 inline void throw_status(int rc) {
@@ -86,7 +93,7 @@ inline shs_options to_c(const SimulatorOptions& o, int device, int combine = SHS
 class IterativeShorEngine {
 public:
     IterativeShorEngine(const FactoringProblem& problem, const ErrorConfig& error,
-                        const SimulatorOptions& options, int device = 0,
+                        const SimulatorOptions& options, int device = default_device(),
                         int combine = SHS_COMBINE_AUTO)
         : t_(problem.t) {
         shs_problem p{problem.N, problem.a, problem.L, problem.t, problem.seed};

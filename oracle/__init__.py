@@ -28,6 +28,10 @@ SIMULATE_REF = os.path.join(HERE, "_ref", "simulate_ref")
 SIMULATE_B200 = os.path.join(HERE, "_ref", "simulate_b200")
 ACCEPTANCE_REF = os.path.join(HERE, "_ref", "acceptance_ref")
 ACCEPTANCE_B200 = os.path.join(HERE, "_ref", "acceptance_b200")
+# the reference's own unit tests / harness compiled against include/dropin
+DROPIN_TESTS = {k: os.path.join(HERE, "_ref", f"test_{k}_b200")
+                for k in ("statevector", "noise", "harness")}
+SIMULATE_DROPIN = os.path.join(HERE, "_ref", "simulate_dropin")
 
 u64 = C.c_uint64
 u32 = C.c_uint32

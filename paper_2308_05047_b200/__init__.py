@@ -44,3 +44,20 @@ from .postprocess import (  # noqa: F401
     shor_standard_procedure,
 )
 from .sharded import DistGroup, LocalGroup, Shard, ShardedShorEngine, digits_to_probs  # noqa: F401
+from .state import (  # noqa: F401
+    ExchangePlan,
+    ShardedState,
+    ShardIndexList,
+    ShardLayout,
+    apply_hadamard_top,
+    apply_oracle,
+    apply_phase,
+    build_permutation_plan,
+    init_state,
+    make_shard_layout,
+    measure_top,
+    plan_receive_lists,
+    plan_send_lists,
+    reset_top,
+    stage_phase,
+)

@@ -117,6 +117,23 @@ SIGNATURES = [
     ("shs_shard_kernel_times", C.c_int, [vp, C.POINTER(dbl), C.POINTER(u64)]),
     ("shs_shard_launch_count", u64, [vp]),
     ("shs_shard_stream", vp, [vp]),
+    ("shs_sv_create", C.c_int, [u32, u32, i32, C.POINTER(vp)]),
+    ("shs_sv_clone", C.c_int, [vp, C.POINTER(vp)]),
+    ("shs_sv_destroy", None, [vp]),
+    ("shs_sv_layout", C.c_int, [vp, C.POINTER(u32)]),
+    ("shs_sv_read", C.c_int, [vp, u64, u64, C.POINTER(dbl)]),
+    ("shs_sv_write", C.c_int, [vp, u64, u64, C.POINTER(dbl)]),
+    ("shs_sv_init_state", C.c_int, [vp, C.POINTER(dbl)]),
+    ("shs_sv_apply_oracle", C.c_int, [vp, u64, u64]),
+    ("shs_sv_apply_phase", C.c_int, [vp, u32, u64, u64]),
+    ("shs_sv_apply_hadamard_top", C.c_int, [vp]),
+    ("shs_sv_group_norms", C.c_int, [vp, C.POINTER(dbl)]),
+    ("shs_sv_reset_top", C.c_int, [vp, i32, i32, C.POINTER(dbl), dbl]),
+    ("shs_sv_launch_count", u64, [vp]),
+    ("shs_plan_build", C.c_int, [u64, u64, u32, u32, i32, C.POINTER(u64), C.POINTER(i32),
+                                 C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+    ("shs_plan_lists", C.c_int, [u64, u64, u32, u32, u32, i32, i32, C.POINTER(u64),
+                                 C.POINTER(u64)]),
     ("shs_exhaustive_distribution", C.c_int, [C.POINTER(shs_problem), C.POINTER(shs_error), u64,
                                               i32, C.POINTER(dbl)]),
     ("shs_engine_set_sparse", C.c_int, [C.c_void_p, i32]),

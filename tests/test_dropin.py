@@ -9,7 +9,8 @@ import subprocess
 
 import pytest
 
-from oracle import ACCEPTANCE_B200, ACCEPTANCE_REF, SIMULATE_B200, SIMULATE_REF
+from oracle import (ACCEPTANCE_B200, ACCEPTANCE_REF, DROPIN_TESTS, SIMULATE_B200, SIMULATE_DROPIN,
+                    SIMULATE_REF)
 
 need = pytest.mark.skipif(not (os.path.exists(SIMULATE_REF) and os.path.exists(SIMULATE_B200)),
                           reason="drop-in binaries not built (need /root/reference at build time)")
@@ -83,3 +84,32 @@ def test_reference_acceptance_criteria_on_b200(cuda_ok, criterion):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert f"CRITERION {criterion}: PASS" in r.stdout
+
+
+# ---- the drop-in header (include/dropin/shorsim/statevector.hpp): the
+# reference's callers and unit tests compiled UNCHANGED against it (no
+# proj/src/statevector.cpp linked), with a doctest-compatible shim
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["statevector", "noise", "harness"])
+def test_reference_unit_tests_against_dropin_header(cuda_ok, name):
+    exe = DROPIN_TESTS[name]
+    if not os.path.exists(exe):
+        pytest.skip("not built")
+    r = run(exe, [], timeout=1800)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "| 0 failed |" in r.stdout
+
+
+@need
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [CASES[0], CASES[1], CASES[4], CASES[8]],
+                         ids=["4087", "8051", "4087-classical", "262139"])
+def test_simulate_jsonl_byte_identical_dropin_header(cuda_ok, case):
+    if not os.path.exists(SIMULATE_DROPIN):
+        pytest.skip("not built")
+    args = [x for x in case if x is not None]
+    ref = run(SIMULATE_REF, args)
+    ours = run(SIMULATE_DROPIN, args)
+    assert ref.returncode == 0 and ours.returncode == 0, ours.stderr
+    assert ours.stdout == ref.stdout
