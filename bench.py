@@ -135,9 +135,10 @@ def reference_sample(steps, warmup, threads):
     for i in range(warmup):
         eng.time_runs(1, i, 1)
     secs = [eng.time_runs(1, warmup + i, 1) for i in range(steps)]
-    run_s = sum(secs) / len(secs)
+    run_s = min(secs)  # best of k
     return {"value": N * t / run_s, "s_per_run": run_s, "ms_per_stage": 1e3 * run_s / t,
-            "construct_s": construct_s, "N": N, "t": t, "threads": threads, "runs": steps}
+            "s_per_run_all": secs, "construct_s": construct_s, "N": N, "t": t,
+            "threads": threads, "runs": steps, "build": ref.build}
 
 
 def cpu_model():
@@ -155,16 +156,17 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 10))
     warm = 1 if args.warmup > 0 else 0
     try:
         r = reference_sample(steps, warm, threads)
     except Exception as exc:  # the reference is always present here; report loudly
         print(json.dumps({"impl": "reference", "unavailable": f"{type(exc).__name__}: {exc}"}))
         return 0
-    sample = (f"{r['runs']} full IterativeShorEngine::run calls at N={r['N']} (config-3 problem), "
-              f"t={r['t']}, workers={threads} on {cpu_model()}; config 4 is out of the reference's "
-              "reach (n=33 needs 206 GB of buffers + up to 1.1 TB of u32 gather tables)")
+    sample = (f"best of {r['runs']} full IterativeShorEngine::run calls at N={r['N']} "
+              f"(config-3 problem), t={r['t']}, workers={threads} on {cpu_model()}; reference "
+              f"build {r['build']['variant']}: {r['build']['flags']}; config 4 is out of the "
+              "reference's reach (n=33 needs 206 GB of buffers + up to 1.1 TB of u32 gather tables)")
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
         "n_gpus": ws, "steps": r["runs"], "warmup": warm,
@@ -287,12 +289,15 @@ def run_ours(args):
     kname = {"probs": "k_tiled<1>" if tiled else "k_stage_probs<1,0>",
              "collapse": "k_tiled<0>" if tiled else "k_stage_collapse<1,0>"}[dom]
     traffic, traffic_src = None, None
-    try:  # DRAM bytes per amplitude from the committed ncu capture, scaled to this N
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")) as f:
-            ks = json.load(f)["kernels"][kname]
-        traffic = ks["dram_bytes_per_amp"] * N
-        traffic_src = f"profiles/r01/ncu_summary.json {kname} ({ks['version']}): " \
-                      f"{ks['dram_bytes_per_amp']} DRAM B/amp at N={ks.get('N', 'n29')} x this N"
+    try:  # DRAM bytes per launch of this kernel from the committed ncu capture at this N
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu_summary.json")) as f:
+            summ = json.load(f)
+        ks = summ["kernels"][kname]
+        if summ["N"] == N:
+            traffic = ks["dram_bytes_per_launch"]
+            traffic_src = (f"profiles/r02/ncu_summary.json {ks['name']}: dram__bytes_read.sum + "
+                           f"dram__bytes_write.sum of one launch at this N "
+                           f"({ks['dram_bytes_per_amp']} B/amp)")
     except (OSError, KeyError, ValueError):
         pass
     roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
@@ -363,13 +368,14 @@ def run_ours(args):
         line["config3_error_models"] = config3_runs(shs)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            r = reference_sample(1, 0, os.cpu_count() or 1)
+            r = reference_sample(3, 1, os.cpu_count() or 1)
             line["cpu_baseline"] = {
                 "value": r["value"], "unit": UNIT, "cores": r["threads"], "kind": "reference",
-                "sample": f"1 full IterativeShorEngine::run at N={r['N']}, t={r['t']} "
+                "sample": f"best of 3 full IterativeShorEngine::run at N={r['N']}, t={r['t']} "
                           f"(config-3 problem; config 4 exceeds the reference's reach), "
                           f"workers={r['threads']}, construct {r['construct_s']:.1f}s untimed; "
-                          f"{cpu_model()}"}
+                          f"{cpu_model()}; reference build {r['build']['variant']}: "
+                          f"{r['build']['flags']}"}
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {type(exc).__name__}: {exc}"}

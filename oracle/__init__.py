@@ -23,6 +23,34 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libshor_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libshorsim_ref.so")
+REF_SO_NATIVE = os.path.join(HERE, "_ref", "native", "libshorsim_ref.so")
+
+
+def native_reference_ok() -> bool:
+    """The -march=native build runs here iff this CPU has every ISA flag of the
+    machine it was built on (recorded at build time)."""
+    try:
+        need = set(open(os.path.join(HERE, "_ref", "native", "cpu_flags")).read().split())
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                return need <= set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return False
+
+
+def reference_build() -> dict:
+    """Which reference build Reference() loads and with which flags."""
+    flags = "-std=c++20 -O3 -DNDEBUG -ffp-contract=off -include cstdint"
+    if os.path.exists(REF_SO_NATIVE) and native_reference_ok():
+        try:
+            march = open(os.path.join(HERE, "_ref", "native", "march")).read().strip()
+        except OSError:
+            march = "-march=native"
+        return {"path": REF_SO_NATIVE, "variant": "native",
+                "flags": f"{flags} -march=native ({march} of the build host; SHORSIM_NATIVE=ON)"}
+    return {"path": REF_SO, "variant": "portable",
+            "flags": f"{flags} (SHORSIM_NATIVE=OFF: this CPU lacks the build host's ISA)"}
 REFERENCE_SRC = "/root/reference/proj/src"
 SIMULATE_REF = os.path.join(HERE, "_ref", "simulate_ref")
 SIMULATE_B200 = os.path.join(HERE, "_ref", "simulate_b200")
@@ -297,7 +325,10 @@ class OracleEngine:
 class Reference:
     """The unmodified reference library (oracle/_ref)."""
 
-    def __init__(self, path: str = REF_SO):
+    def __init__(self, path: str | None = None):
+        self.build = reference_build() if path is None else {"path": path, "variant": "explicit",
+                                                              "flags": ""}
+        path = self.build["path"]
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where "
                                     "/root/reference exists")
