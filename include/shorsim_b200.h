@@ -236,7 +236,7 @@ int shs_engine_devices(const shs_engine* engine, int32_t* out, int32_t max);
 typedef struct shs_shard shs_shard;
 #define SHS_MAX_SHARDS 16
 #define SHS_DIGITS 80 /* 2 groups x 40 x 32-bit digits (in uint64 words) */
-#define SHS_SHARD_IPC_BYTES 640 /* shs_shard_ipc_handles blob */
+#define SHS_SHARD_IPC_BYTES 1088 /* shs_shard_ipc_handles blob */
 
 int shs_shard_create(const shs_problem* problem, const shs_error* error,
                      const shs_options* options, uint32_t rank, uint32_t nshards,

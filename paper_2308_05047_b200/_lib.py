@@ -30,7 +30,7 @@ SHS_CUDA_ERROR = 8
 
 COMBINE = {"auto": 0, "kahan": 1, "exact": 2}
 SHS_DIGITS = 80
-SHS_SHARD_IPC_BYTES = 640
+SHS_SHARD_IPC_BYTES = 1088
 MAX_SHARDS = 16
 TILING = {"auto": 0, "force": 1, "off": 2}
 

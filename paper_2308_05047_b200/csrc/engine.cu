@@ -173,6 +173,11 @@ void resolve_marks(shs_engine* e) {
 
 template <typename F>
 int launch(shs_engine* e, int kind, F&& f) {
+    // an error left by an earlier runtime call is reported as such, not as this launch's
+    const cudaError_t stale = cudaGetLastError();
+    if (stale != cudaSuccess)
+        return set_error(SHS_CUDA_ERROR, std::string("pending CUDA error before a launch: ") +
+                                             cudaGetErrorString(stale));
     cudaEvent_t a = nullptr, b = nullptr;
     const bool timed = e->timing && kind >= 0;
     if (timed) {

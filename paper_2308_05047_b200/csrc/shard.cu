@@ -28,6 +28,8 @@
 #include "../../include/shorsim_b200.h"
 #include "device_math.cuh"
 #include "exchange.cuh"
+#include "exchange2.cuh"
+#include <cub/cub.cuh>
 #include "host_model.hpp"
 #include "stage_kernels.cuh"
 #include "tile_plan.hpp"
@@ -146,6 +148,31 @@ struct shs_shard {
     bool peer_S_ipc[kMaxShards] = {};
     double* Scat = nullptr;   // kahan: [2][nb_total] gathered partials
     double* d_p = nullptr;    // kahan step API: p0, p1
+    // exchange v2 (exchange2.cuh) in device-resident runs: two receive slots of
+    // x2_slot elements (peers write their streams into them), the per-stage
+    // stream offsets (data-independent, prepared once per shard set), the
+    // region base of every sender in this shard's slot per (stage, round)
+    // (exported: senders read them once), pack on its own stream
+    bool x2_on = true;                     // SHS_EXCHANGE=1: v1 in runs too
+    uint32_t x2_K = 1;                     // rounds per exchange stage
+    uint64_t x2_slot = 0;                  // elements per receive slot
+    double2* x2_recv = nullptr;            // [2][x2_slot]
+    double2* peer_recv[kMaxShards] = {};
+    bool peer_recv_ipc[kMaxShards] = {};
+    unsigned long long* x2_bases = nullptr;  // [t][x2_K][G]: base of sender q's region, per round
+    const unsigned long long* peer_bases[kMaxShards] = {};
+    bool peer_bases_ipc[kMaxShards] = {};
+    bool x2_ready = false;                 // offsets / bases prepared
+    std::vector<uint8_t> x2_stage;         // stage uses v2
+    std::vector<unsigned long long*> x2_soff, x2_roff;  // per stage: [G][nbands+1]
+    std::vector<uint64_t> x2_dst;          // [t][x2_K][G]: my region base in receiver r's slot
+    std::vector<uint64_t> x2_rbase;        // [t][x2_K][G]: sender q's region base in my slot
+    std::vector<std::vector<uint64_t>> x2_bounds;  // [t][x2_K + 1]: first band of each round
+    uint64_t x2_round = 0;                 // global round counter (event / slot parity)
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t evp[2] = {}, evu[2] = {};  // pack / unpack of a round done (interprocess)
+    cudaEvent_t pevp[kMaxShards][2] = {}, pevu[kMaxShards][2] = {};
+    double x2_ms[2] = {0, 0};              // instrumentation: pack, unpack
 };
 
 namespace {
@@ -261,6 +288,24 @@ void release(shs_shard* sh) {
     cudaFree(sh->d_dig2);
     cudaFree(sh->Scat);
     cudaFree(sh->d_p);
+    for (auto* x : sh->x2_soff) cudaFree(x);
+    for (auto* x : sh->x2_roff) cudaFree(x);
+    cudaFree(sh->x2_recv);
+    cudaFree(sh->x2_bases);
+    for (uint32_t q = 0; q < sh->G; ++q) {
+        if (sh->peer_recv_ipc[q] && sh->peer_recv[q]) cudaIpcCloseMemHandle(sh->peer_recv[q]);
+        if (sh->peer_bases_ipc[q] && sh->peer_bases[q])
+            cudaIpcCloseMemHandle(const_cast<unsigned long long*>(sh->peer_bases[q]));
+        if (sh->peer_ev_ipc[q])
+            for (int k = 0; k < 2; ++k) {
+                if (sh->pevp[q][k]) cudaEventDestroy(sh->pevp[q][k]);
+                if (sh->pevu[q][k]) cudaEventDestroy(sh->pevu[q][k]);
+            }
+    }
+    for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t e : {sh->evp[k], sh->evu[k]})
+            if (e) cudaEventDestroy(e);
+    if (sh->xstream) cudaStreamDestroy(sh->xstream);
     for (uint32_t q = 0; q < sh->G; ++q)
         if (sh->peer_S_ipc[q] && sh->peer_S[q])
             cudaIpcCloseMemHandle(const_cast<double*>(sh->peer_S[q]));
@@ -304,6 +349,112 @@ int launch_exchange(shs_shard* sh, uint32_t s) {
     return shard_launch(sh, 1, [&] {
         k_exchange_direct<<<grid(sh), kThreads, 0, sh->stream>>>(p, map, sh->buf[sh->parity ^ 1]);
     });
+}
+
+
+// ---- exchange v2 (exchange2.cuh)
+
+TileParams plan_tile_params(const shs_shard* sh, uint32_t s) {
+    const TilePlanHost& pl = sh->plans[s];
+    TileParams tp{};
+    tp.N = sh->N;
+    tp.A = pl.A;
+    tp.A_sh = pl.A_sh;
+    tp.m = pl.m;
+    tp.m_sh = pl.m_sh;
+    tp.m_chunk = mulmod(pl.m, kCols, sh->N);
+    tp.H = pl.H;
+    tp.u = pl.u;
+    tp.v = pl.v;
+    tp.du = pl.du;
+    tp.dv = pl.dv;
+    tp.ntiles = pl.ntiles;
+    return tp;
+}
+
+X2Params x2_params(const shs_shard* sh, uint32_t s) {
+    X2Params p{};
+    p.tp = plan_tile_params(sh, s);
+    p.S = sh->S;
+    p.S_inv = ~uint64_t(0) / sh->S;
+    p.N = sh->N;
+    p.G = static_cast<int>(sh->G);
+    p.me = static_cast<int>(sh->rank);
+    p.sel = sh->buf[sh->parity];
+    p.P = sh->buf[sh->parity ^ 1];
+    return p;
+}
+
+// a stage runs exchange v2 when it has a tile plan whose rows fit a shard
+bool x2_eligible(const shs_shard* sh, uint32_t s) {
+    const TilePlanHost& pl = sh->plans[s];
+    return sh->x2_on && sh->x2_recv && s > 0 && sh->a_pows[s] != 1 && pl.tiled &&
+           pl.du + pl.dv <= sh->S;
+}
+
+// Round boundaries of stage s: bands cut where the cumulative element count
+// (row lengths du, dv, du + dv by the three-distance classes) crosses k N / K,
+// so every round moves about N / K elements (a band-count split does not: the
+// length classes are contiguous in j).
+std::vector<uint64_t> x2_round_bounds(const TilePlanHost& pl, uint64_t N, uint32_t K) {
+    std::vector<uint64_t> b(K + 1, pl.ntiles);
+    b[0] = 0;
+    auto len = [&](uint64_t j) -> uint64_t {
+        if (j >= pl.H) return 0;
+        if (j + pl.u < pl.H) return pl.du;
+        if (j >= pl.v) return pl.dv;
+        return pl.du + pl.dv;
+    };
+    uint64_t cum = 0;
+    uint32_t k = 1;
+    for (uint64_t band = 0; band < pl.ntiles && k < K; ++band) {
+        while (k < K && cum >= (static_cast<unsigned __int128>(N) * k) / K) b[k++] = band;
+        for (uint64_t j = band * kRows; j < (band + 1) * kRows; ++j) cum += len(j);
+    }
+    return b;
+}
+
+uint64_t x2_band(const shs_shard* sh, uint32_t s, uint32_t k) { return sh->x2_bounds[s][k]; }
+
+int x2_grid(const shs_shard* sh, uint64_t bands) {
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(bands, 8ull * sh->num_sms)));
+}
+
+// round k of stage s, global round g: this shard's pack (its pack stream)
+int launch_x2_pack(shs_shard* sh, uint32_t s, uint32_t k, uint64_t g) {
+    const TilePlanHost& pl = sh->plans[s];
+    X2Params p = x2_params(sh, s);
+    p.b0 = x2_band(sh, s, k);
+    p.b1 = x2_band(sh, s, k + 1);
+    p.off = sh->x2_soff[s];
+    for (uint32_t r = 0; r < sh->G; ++r)
+        p.dst[r] = sh->peer_recv[r] + (g & 1) * sh->x2_slot +
+                   sh->x2_dst[(uint64_t(s) * sh->x2_K + k) * sh->G + r];
+    if (p.b0 == p.b1) return SHS_OK;
+    k_x2_pack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->xstream>>>(p);
+    sh->launches++;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SHS_OK
+                            : set_error(SHS_CUDA_ERROR, std::string("k_x2_pack: ") + cudaGetErrorString(e));
+}
+
+// ... and its unpack (main stream), into P
+int launch_x2_unpack(shs_shard* sh, uint32_t s, uint32_t k, uint64_t g) {
+    const std::vector<uint64_t>& rbase = sh->x2_rbase;
+    const TilePlanHost& pl = sh->plans[s];
+    X2Params p = x2_params(sh, s);
+    p.b0 = x2_band(sh, s, k);
+    p.b1 = x2_band(sh, s, k + 1);
+    p.off = sh->x2_roff[s];
+    for (uint32_t q = 0; q < sh->G; ++q)
+        p.src[q] = sh->x2_recv + (g & 1) * sh->x2_slot +
+                   rbase[(uint64_t(s) * sh->x2_K + k) * sh->G + q];
+    if (p.b0 == p.b1) return SHS_OK;
+    k_x2_unpack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->stream>>>(p);
+    sh->launches++;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SHS_OK
+                            : set_error(SHS_CUDA_ERROR, std::string("k_x2_unpack: ") + cudaGetErrorString(e));
 }
 
 // Host scalars of stage s for the observed prefix (statevector.cpp:338-349).
@@ -392,6 +543,113 @@ ShardPartials shard_partials(const shs_shard* sh, int k) {
 
 }  // namespace
 
+
+// Offsets of exchange v2 for every eligible stage (collective over the shard
+// set; once): per stage, count(b, me, r) and count(b, q, me) per band on the
+// device, their exclusive scans over bands, the region base of every sender in
+// this shard's receive slot per round (x2_bases, exported), then every
+// sender's own base in each receiver's slot read back from the peers.
+int x2_prepare(const std::vector<shs_shard*>& L, ShmBarrier* bar) {
+    const uint32_t t = L[0]->t, G = L[0]->G, K = L[0]->x2_K;
+    for (size_t li = 0; li < L.size(); ++li) {
+        shs_shard* q = L[li];
+        q->x2_rbase.assign(size_t(t) * K * G + t, 0);
+        RUN_CUDA(cudaSetDevice(q->dev));
+        q->x2_stage.assign(t, 0);
+        q->x2_bounds.assign(t, {});
+        q->x2_soff.assign(t, nullptr);
+        q->x2_roff.assign(t, nullptr);
+        std::vector<uint64_t>& hb = q->x2_rbase;
+        unsigned long long* cnt = nullptr;
+        uint64_t cnt_cap = 0;
+        void* tmp = nullptr;
+        size_t tmp_bytes = 0;
+        for (uint32_t s = 0; s < t; ++s) {
+            if (!x2_eligible(q, s)) continue;
+            const TilePlanHost& pl = q->plans[s];
+            const uint64_t nb1 = pl.ntiles + 1;
+            q->x2_bounds[s] = x2_round_bounds(pl, q->N, K);
+            RUN_CUDA(cudaMalloc(&q->x2_soff[s], sizeof(unsigned long long) * G * nb1));
+            RUN_CUDA(cudaMalloc(&q->x2_roff[s], sizeof(unsigned long long) * G * nb1));
+            if (nb1 > cnt_cap) {
+                cudaFree(cnt);
+                RUN_CUDA(cudaMalloc(&cnt, sizeof(unsigned long long) * G * nb1 * 2));
+                cnt_cap = nb1;
+            }
+            X2Params p = x2_params(q, s);
+            RUN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * G * nb1 * 2, q->stream));
+            const int grid = x2_grid(q, pl.ntiles);
+            k_x2_count<true><<<grid, kX2Threads, 0, q->stream>>>(p, cnt);
+            k_x2_count<false><<<grid, kX2Threads, 0, q->stream>>>(p, cnt + G * nb1);
+            RUN_CUDA(cudaGetLastError());
+            size_t need = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, q->x2_soff[s], static_cast<int>(nb1),
+                                          q->stream);
+            if (need > tmp_bytes) {
+                cudaFree(tmp);
+                RUN_CUDA(cudaMalloc(&tmp, need));
+                tmp_bytes = need;
+            }
+            for (uint32_t g = 0; g < G; ++g) {
+                size_t tb = tmp_bytes;
+                cub::DeviceScan::ExclusiveSum(tmp, tb, cnt + g * nb1, q->x2_soff[s] + g * nb1,
+                                              static_cast<int>(nb1), q->stream);
+                tb = tmp_bytes;
+                cub::DeviceScan::ExclusiveSum(tmp, tb, cnt + G * nb1 + g * nb1,
+                                              q->x2_roff[s] + g * nb1, static_cast<int>(nb1),
+                                              q->stream);
+            }
+            // receive offsets at the round boundaries -> this shard's region bases
+            std::vector<unsigned long long> at(size_t(G) * (K + 1));
+            for (uint32_t g = 0; g < G; ++g)
+                for (uint32_t k = 0; k <= K; ++k)
+                    RUN_CUDA(cudaMemcpyAsync(&at[g * (K + 1) + k],
+                                             q->x2_roff[s] + g * nb1 + q->x2_bounds[s][k],
+                                             sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                             q->stream));
+            RUN_CUDA(cudaStreamSynchronize(q->stream));
+            bool fits = true;
+            for (uint32_t k = 0; k < K; ++k) {
+                uint64_t base = 0;
+                for (uint32_t g = 0; g < G; ++g) {
+                    hb[(uint64_t(s) * K + k) * G + g] = base;
+                    base += at[g * (K + 1) + k + 1] - at[g * (K + 1) + k];
+                }
+                fits = fits && base <= q->x2_slot;
+            }
+            // a stage whose rounds overflow some rank's slot (few, lumpy rows at
+            // small N) runs exchange v1: decided with every rank's flag below
+            hb[uint64_t(t) * K * G + s] = fits ? 1 : 0;
+            q->x2_stage[s] = 1;
+        }
+        RUN_CUDA(cudaMemcpyAsync(q->x2_bases, hb.data(), sizeof(uint64_t) * hb.size(),
+                                 cudaMemcpyHostToDevice, q->stream));
+        RUN_CUDA(cudaStreamSynchronize(q->stream));
+        cudaFree(cnt);
+        cudaFree(tmp);
+    }
+    if (bar) {
+        int rc = bar->arrive();
+        if (rc) return rc;
+    }
+    std::vector<uint64_t> pb(size_t(t) * K * G + t);
+    for (shs_shard* q : L) {
+        RUN_CUDA(cudaSetDevice(q->dev));
+        q->x2_dst.assign(size_t(t) * K * G, 0);
+        for (uint32_t r = 0; r < G; ++r) {
+            RUN_CUDA(cudaMemcpy(pb.data(), q->peer_bases[r], sizeof(uint64_t) * pb.size(),
+                                cudaMemcpyDefault));
+            for (uint64_t sk = 0; sk < uint64_t(t) * K; ++sk)
+                q->x2_dst[sk * G + r] = pb[sk * G + q->rank];
+            for (uint32_t s = 0; s < t; ++s)  // the same decision on every rank
+                if (!pb[uint64_t(t) * K * G + s]) q->x2_stage[s] = 0;
+        }
+        q->x2_ready = true;
+    }
+    if (bar) return bar->arrive();  // nobody packs before every peer read the bases
+    return SHS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Device-resident sharded run (IterativeShorEngine::run, statevector.cpp:323-412,
 // over G block shards). `L` = the shards THIS host thread drives: all G of them
@@ -441,6 +699,14 @@ int shards_run(const std::vector<shs_shard*>& L, ShmBarrier* bar, u64 seed, u64 
     double inv = 1.0;
     StageScalars sc = shard_scalars(s0, 0, 0, 1.0);
     int status = SHS_OK;
+    if (G > 1 && s0->x2_on && s0->x2_recv && !s0->x2_ready) {
+        for (shs_shard* q : L)
+            for (uint32_t r = 0; r < G; ++r)
+                if (!q->peer_recv[r] || !q->peer_bases[r] || !q->pevp[r][0])
+                    return set_error(SHS_INVALID_ARGUMENT, "sharded run: exchange buffers of shard " +
+                                                               std::to_string(r) + " not attached");
+        if ((status = x2_prepare(L, bar))) return status;
+    }
     auto absorb = [&](uint32_t r) -> int {
         RUN_CUDA(cudaSetDevice(s0->dev));
         RUN_CUDA(cudaEventSynchronize(s0->evm[r & 1]));
@@ -481,7 +747,33 @@ int shards_run(const std::vector<shs_shard*>& L, ShmBarrier* bar, u64 seed, u64 
     for (uint32_t s = 0; s < t; ++s) {
         const int k = s & 1;
         const bool ex = stage_needs_exchange(s0, s);
-        if (ex) {
+        if (ex && s0->x2_ready && s0->x2_stage[s]) {
+            // exchange v2: K rounds of pack (pack streams) -> unpack (main streams);
+            // pack of round g+1 overlaps unpack of round g
+            for (uint32_t kr = 0; kr < s0->x2_K; ++kr) {
+                const uint64_t g = s0->x2_round;
+                for (shs_shard* q : L) {
+                    RUN_CUDA(cudaSetDevice(q->dev));
+                    if (kr == 0)  // own sel written by the previous collapse
+                        RUN_CUDA(cudaStreamWaitEvent(q->xstream, q->evc[(s - 1) & 1], 0));
+                    if (g >= 2)  // every receiver unpacked round g-2 out of slot g & 1
+                        for (uint32_t r = 0; r < G; ++r)
+                            RUN_CUDA(cudaStreamWaitEvent(q->xstream, q->pevu[r][g & 1], 0));
+                    if ((status = launch_x2_pack(q, s, kr, g))) return drain(status);
+                    RUN_CUDA(cudaEventRecord(q->evp[g & 1], q->xstream));
+                }
+                if ((status = barrier())) return drain(status);
+                for (shs_shard* q : L) {
+                    RUN_CUDA(cudaSetDevice(q->dev));
+                    for (uint32_t r = 0; r < G; ++r)  // every sender's round g landed
+                        RUN_CUDA(cudaStreamWaitEvent(q->stream, q->pevp[r][g & 1], 0));
+                    if ((status = launch_x2_unpack(q, s, kr, g))) return drain(status);
+                    RUN_CUDA(cudaEventRecord(q->evu[g & 1], q->stream));
+                }
+                if ((status = barrier())) return drain(status);
+                for (shs_shard* q : L) q->x2_round++;
+            }
+        } else if (ex) {
             for (shs_shard* q : L) {
                 RUN_CUDA(cudaSetDevice(q->dev));
                 if (s > 0 && (status = wait_peers(q, q->pevc, (s - 1) & 1))) return drain(status);
@@ -889,6 +1181,47 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
         sh->pevd[rank][k] = sh->evd[k];
         sh->pevc[rank][k] = sh->evc[k];
     }
+    if (nshards >= 2) {  // exchange v2: receive slots, round count, bases, pack stream
+        const char* xe = std::getenv("SHS_EXCHANGE");
+        sh->x2_on = !(xe && xe[0] == '1');
+        size_t fr = 0, tot = 0;
+        if ((ce = cudaMemGetInfo(&fr, &tot)) != cudaSuccess) return fail(ce, "cudaMemGetInfo");
+        // a round receives ~S/K elements (more where few rows make the z-spread
+        // lumpy): slots of c S / K with c = 2 when memory allows, down to 1.25,
+        // then more rounds
+        const double slot_cap = std::max(0.0, static_cast<double>(fr) - 3.0e9) / (2 * sizeof(double2));
+        const double Sd = static_cast<double>(sh->S);
+        uint32_t K = 1;
+        double c = 2.0;
+        while (c * Sd / K + 65536.0 > slot_cap) {
+            if (c > 1.25) c = std::max(1.25, c - 0.25);
+            else if (K < 256) ++K;
+            else break;
+        }
+        if (const char* kr = std::getenv("SHS_X2_ROUNDS")) K = std::max(1, std::atoi(kr));
+        sh->x2_K = K;
+        sh->x2_slot = static_cast<uint64_t>(c * Sd / K) + 65536;
+        if ((ce = cudaMalloc(&sh->x2_recv, 2 * sizeof(double2) * sh->x2_slot)) != cudaSuccess)
+            return fail(ce, "cudaMalloc(exchange receive slots)");
+        // [t][K][G] region bases, then [t] "every round of the stage fits my slot"
+        if ((ce = cudaMalloc(&sh->x2_bases,
+                             sizeof(unsigned long long) * sh->t * (uint64_t(K) * nshards + 1))) !=
+            cudaSuccess)
+            return fail(ce, "cudaMalloc(exchange bases)");
+        if ((ce = cudaStreamCreateWithFlags(&sh->xstream, cudaStreamNonBlocking)) != cudaSuccess)
+            return fail(ce, "cudaStreamCreate(pack)");
+        for (int k = 0; k < 2; ++k) {
+            const unsigned ipc = cudaEventDisableTiming | cudaEventInterprocess;
+            if ((ce = cudaEventCreateWithFlags(&sh->evp[k], ipc)) != cudaSuccess ||
+                (ce = cudaEventCreateWithFlags(&sh->evu[k], ipc)) != cudaSuccess)
+                return fail(ce, "cudaEventCreate(exchange events)");
+            sh->pevp[rank][k] = sh->evp[k];
+            sh->pevu[rank][k] = sh->evu[k];
+        }
+        sh->peer_recv[rank] = sh->x2_recv;
+        sh->peer_bases[rank] = sh->x2_bases;
+        sh->device_bytes += 2 * sizeof(double2) * sh->x2_slot;
+    }
     sh->peer_dig[rank] = sh->d_dig2;
     sh->peer_S[rank] = sh->Sb;
     sh->peer[rank][0] = sh->buf[0];
@@ -910,6 +1243,12 @@ int shs_shard_attach_local(shs_shard* sh, shs_shard* peer) {
     if (rc) return rc;
     sh->peer_dig[peer->rank] = peer->d_dig2;
     sh->peer_S[peer->rank] = peer->Sb;
+    sh->peer_recv[peer->rank] = peer->x2_recv;
+    sh->peer_bases[peer->rank] = peer->x2_bases;
+    for (int k = 0; k < 2; ++k) {
+        sh->pevp[peer->rank][k] = peer->evp[k];
+        sh->pevu[peer->rank][k] = peer->evu[k];
+    }
     for (int k = 0; k < 2; ++k) {  // cross-device stream waits on events work in-process
         sh->pevx[peer->rank][k] = peer->evx[k];
         sh->pevd[peer->rank][k] = peer->evd[k];
@@ -993,6 +1332,9 @@ struct ShardIpcBlob {
     cudaIpcMemHandle_t dig;
     cudaIpcMemHandle_t sb;
     cudaIpcEventHandle_t evx[2], evd[2], evc[2];
+    cudaIpcMemHandle_t recv, bases;  // exchange v2
+    cudaIpcEventHandle_t evp[2], evu[2];
+    int32_t has_x2;
 };
 static_assert(sizeof(ShardIpcBlob) <= SHS_SHARD_IPC_BYTES, "SHS_SHARD_IPC_BYTES too small");
 
@@ -1004,6 +1346,15 @@ int shs_shard_ipc_handles(const shs_shard* csh, void* out) {
         for (int k = 0; k < 2; ++k) SHD_CUDA(cudaIpcGetMemHandle(&b.buf[k], sh->buf[k]));
         SHD_CUDA(cudaIpcGetMemHandle(&b.dig, sh->d_dig2));
         SHD_CUDA(cudaIpcGetMemHandle(&b.sb, sh->Sb));
+        b.has_x2 = sh->x2_recv ? 1 : 0;
+        if (b.has_x2) {
+            SHD_CUDA(cudaIpcGetMemHandle(&b.recv, sh->x2_recv));
+            SHD_CUDA(cudaIpcGetMemHandle(&b.bases, sh->x2_bases));
+            for (int k = 0; k < 2; ++k) {
+                SHD_CUDA(cudaIpcGetEventHandle(&b.evp[k], sh->evp[k]));
+                SHD_CUDA(cudaIpcGetEventHandle(&b.evu[k], sh->evu[k]));
+            }
+        }
         for (int k = 0; k < 2; ++k) {
             SHD_CUDA(cudaIpcGetEventHandle(&b.evx[k], sh->evx[k]));
             SHD_CUDA(cudaIpcGetEventHandle(&b.evd[k], sh->evd[k]));
@@ -1067,6 +1418,20 @@ int shs_shard_attach_ipc(shs_shard* sh, uint32_t peer, const void* handles) {
         SHD_CUDA(cudaIpcOpenMemHandle(&sp, b.sb, cudaIpcMemLazyEnablePeerAccess));
         sh->peer_S[peer] = static_cast<const double*>(sp);
         sh->peer_S_ipc[peer] = true;
+        if (b.has_x2 && sh->x2_recv) {
+            void* rp = nullptr;
+            SHD_CUDA(cudaIpcOpenMemHandle(&rp, b.recv, cudaIpcMemLazyEnablePeerAccess));
+            sh->peer_recv[peer] = static_cast<double2*>(rp);
+            sh->peer_recv_ipc[peer] = true;
+            void* bp = nullptr;
+            SHD_CUDA(cudaIpcOpenMemHandle(&bp, b.bases, cudaIpcMemLazyEnablePeerAccess));
+            sh->peer_bases[peer] = static_cast<const unsigned long long*>(bp);
+            sh->peer_bases_ipc[peer] = true;
+            for (int k = 0; k < 2; ++k) {
+                SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevp[peer][k], b.evp[k]));
+                SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevu[peer][k], b.evu[k]));
+            }
+        }
         for (int k = 0; k < 2; ++k) {
             SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevx[peer][k], b.evx[k]));
             SHD_CUDA(cudaIpcOpenEventHandle(&sh->pevd[peer][k], b.evd[k]));

@@ -449,8 +449,8 @@ int shs_plan_build(uint64_t a_pow, uint64_t N, uint32_t n, uint32_t shard_count,
     unsigned long long* dc = nullptr;
     const size_t cells = size_t(pa.gs) * pa.gs;
     auto done = [&](int code) {
-        cudaFreeAsync(dg, st);
-        cudaFreeAsync(dc, st);
+        if (dg) cudaFreeAsync(dg, st);
+        if (dc) cudaFreeAsync(dc, st);
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
         return code;

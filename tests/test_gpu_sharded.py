@@ -184,3 +184,28 @@ def test_shard_protocol_errors(cuda_ok):
     with pytest.raises(ValueError):  # probs before this stage's exchange
         sh.probs(1, 0)
     eng.close()
+
+
+@pytest.mark.parametrize("G,rounds", [(2, "1"), (3, "2"), (4, "3"), (8, "1"), (5, "4")])
+def test_exchange_v2_equals_v1_and_single(cuda_ok, monkeypatch, G, rounds):
+    """Device-resident runs with exchange v2 (exchange2.cuh: pack into the
+    receivers' streams, unpack through shared-memory transposes, K rounds) equal
+    the v1 exchange (SHS_EXCHANGE=1) and the single engine, amplitudes included."""
+    import paper_2308_05047_b200 as shs
+    monkeypatch.setenv("SHS_X2_ROUNDS", rounds)
+    N, a, t = 4194301, 1234567, 10
+    err = E("phase_init", 0.1)
+    prob = shs.FactoringProblem.make(N, a, t)
+    single = shs.IterativeShorEngine(prob, err, opts())
+    v2 = shs.ShardedShorEngine.virtual(prob, err, opts(), nshards=G)
+    monkeypatch.setenv("SHS_EXCHANGE", "1")
+    v1 = shs.ShardedShorEngine.virtual(prob, err, opts(), nshards=G)
+    for idx in range(3):
+        r = single.run(6, idx)
+        same_run(v2.run(6, idx), r)
+        same_run(v1.run(6, idx), r)
+    for x in (0, 1):  # the pending state after the runs
+        want = np.ctypeslib.as_array(single.stage_read(x, 0, N))
+        assert np.array_equal(full_state(v2, x, N, stage=True), want)
+    v2.close()
+    v1.close()
