@@ -40,6 +40,9 @@ WORKLOADS = {
     # config 3 (BASELINE.json configs[2]): ~24-bit semiprime
     "c3": dict(N=16777207, a=2, p=4093, q=4099,
                desc="config 3: N=16777207=4093*4099, a=2 (order 2794836), t=48"),
+    # 31-qubit profiling size: 34 GB per buffer (the sharded exchange at ~8k bands)
+    "n31": dict(N=2146005049, a=3, p=46301, q=46349,
+                desc="31-qubit profiling size: N=2146005049=46301*46349, a=3, t=62"),
     # profiling size for the round-robin tiled variant (config 4's): 17 GB per buffer
     "n30": dict(N=1073217479, a=2, p=32749, q=32771,
                 desc="30-qubit profiling size: N=1073217479=32749*32771, a=2 (order 536575980), t=60"),
@@ -553,14 +556,16 @@ def config3_runs(shs):
 def run_sharded(args):
     """N > 1 GPUs (one process per GPU under torchrun): one block shard of the
     config-4 state per rank (strong scaling: the same N as at 1 GPU). Peers
-    attach through CUDA IPC (buffers, stage digits, ordering events).
+    attach through CUDA IPC (buffers, receive slots, stage digits, ordering
+    events).
 
-    step (value, ms_per_step): one non-identity stage through the per-stage
-    shard API, as at 1 GPU: exchange -> probs -> digit allreduce -> measurement
-    -> collapse, device time max over ranks.
-    e2e: full device-resident runs through ShardedShorEngine.run
-    (shs_shards_run: no host round trip per stage; stages ordered across ranks
-    by IPC events), wall time max over ranks."""
+    A step here is one full iterative-Shor run, device-resident
+    (ShardedShorEngine.run -> shs_shards_run): per stage the exchange v2
+    all-to-all (pack -> NVLink -> unpack, in rounds), probs, the exact digit
+    sum and the measurement on every device, collapse; no host round trip per
+    stage. value = N * t * steps / device time (CUDA events on each rank's main
+    stream, max over ranks) — every stage dense, so comparable with the 1-GPU
+    line's e2e (s_per_run_dense)."""
     import torch
     import torch.distributed as dist
 
@@ -595,20 +600,9 @@ def run_sharded(args):
     eng = shs.ShardedShorEngine(prob, err, opts, [shard], group)
     stream = torch.cuda.ExternalStream(shard.stream_handle(), device=dev)
     seed = 2308
-    state = {"s": 0, "prefix": 0}
-    eng.state_init()
 
-    def step():
-        s = state["s"]
-        p0, p1 = eng.stage_probs(s, state["prefix"])
-        b = shs.sample_measurement(p1, seed, 0, s, err)["sampled_bit"]
-        eng.stage_collapse(b, p1 if b else p0)
-        state["prefix"] = (state["prefix"] | (b << s)) & ((1 << t) - 1)
-        state["s"] = s + 1 if s + 1 < t else 1
-        return s
-
-    for _ in range(max(args.warmup, 1)):
-        step()
+    for i in range(max(args.warmup, 1)):  # the first run also prepares the exchange offsets
+        eng.run(seed, 100 + i)
     launches0 = shard.launch_count()
     clocks = ClockSampler(local)
     dist.barrier()
@@ -616,71 +610,68 @@ def run_sharded(args):
     clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
     ev0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for i in range(args.steps):
+        res = eng.run(seed, 1000 + i)
     ev1.record(stream)
     ev1.synchronize()
+    wall = time.perf_counter() - wall0
     dist.barrier()
     clock_info = clocks.stop()
     ms_per_step = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    wall_per_run = max_over_ranks(wall / args.steps)
     launches = shard.launch_count() - launches0
 
-    shard.set_timing(True)
-    for _ in range(3):
-        step()
+    shard.set_timing(True)  # one more run, every launch timed (serialised)
+    eng.run(seed, 999)
     kt = shard.kernel_times()
     shard.set_timing(False)
     kms = {k: max_over_ranks(v[0] / max(v[1], 1)) for k, v in kt.items()}
+    kn = {k: v[1] for k, v in kt.items()}
     nloc = shard.hi - shard.lo
-    # exchange (exchange.cuh): every rank executes a round-robin share of the
-    # tiles, pulling 512 B source runs from their owners and pushing 512 B row
-    # runs into the owners' P: per GPU and direction 2 x 16 B x (N/G)(G-1)/G
-    # cross the links (the all-to-all minimum is half that)
-    nvlink_bytes = 32 * nloc * (ws - 1) / ws
-    nvlink_min_bytes = 16 * nloc * (ws - 1) / ws
+    rounds = max(1, kn["pack"] // max(1, kn["probs"] - 1)) if kn["pack"] else 1
+    pack_stage_ms = kms["pack"] * kn["pack"] / max(1, kn["probs"])  # per stage (all rounds)
+    unpack_stage_ms = kms["unpack"] * kn["unpack"] / max(1, kn["probs"])
+    # exchange v2 (exchange2.cuh): each element crosses once, sender -> receiver:
+    # per GPU and direction 16 B x (N/G)(G-1)/G, the all-to-all minimum
+    nvlink_bytes = 16 * nloc * (ws - 1) / ws
     nvlink_peak = 900.0  # GB/s per direction per GPU (NVLink 5, north_star)
     hbm_peak, peak_src = peaks()
-    ex_gbs = nvlink_bytes / (kms["exchange"] * 1e-3) / 1e9 if kms["exchange"] else None
+    ex_gbs = nvlink_bytes / (pack_stage_ms * 1e-3) / 1e9 if pack_stage_ms else None
     local_ms = kms["probs"] + kms["collapse"]
     local_gbs = 80 * nloc / (local_ms * 1e-3) / 1e9 if local_ms else None
 
-    res = eng.run(seed, 1000)  # warm the device-resident path
-    e2e_runs = max(1, args.e2e_runs)
-    dist.barrier()
-    t0 = time.perf_counter()
-    for i in range(e2e_runs):
-        res = eng.run(seed, 1001 + i)
-    run_s = max_over_ranks((time.perf_counter() - t0) / e2e_runs)
-
     line = {
-        "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": ws,
+        "metric": METRIC, "value": N * t / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the deterministic iterative-Shor state from |1> (no dataset)",
         "config": {"workload": args.workload, "desc": w["desc"], "N": N, "a": a, "t": t,
+                   "step": "one full device-resident run (t stages, every stage dense)",
                    "shard_amplitudes": nloc, "parallelism": f"{ws} shards (block-sharded state)",
-                   "backend": backend,
+                   "backend": backend, "exchange_rounds": rounds,
                    "l2": "state far larger than L2: no flush needed"},
-        "s_per_run": run_s,
-        "s_per_run_dense": run_s,
+        "s_per_run": ms_per_step * 1e-3,
+        "s_per_run_dense": ms_per_step * 1e-3,
         "sparse_prefix_stages": 0,
         "kernels_max_over_ranks_ms": kms,
+        "per_stage_ms": {"pack": pack_stage_ms, "unpack": unpack_stage_ms,
+                         "probs": kms["probs"], "collapse": kms["collapse"]},
         "roofline": {"kernel": "k_stage_probs + k_stage_collapse <kSrcBuffer> (shard-local)",
                      "bound": "hbm", "achieved": local_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": local_gbs / hbm_peak if local_gbs else None,
                      "peak_source": peak_src, "traffic": None, "bytes_per_amp": 80},
-        "nvlink": {"kernel": "k_exchange", "achieved": ex_gbs, "peak": nvlink_peak,
-                   "unit": "GB/s per direction", "frac": ex_gbs / nvlink_peak if ex_gbs else None,
-                   "bytes_per_gpu_per_direction": nvlink_bytes,
-                   "all_to_all_minimum_bytes": nvlink_min_bytes,
-                   "note": "one GPU per process; with ranks sharing a GPU (gloo) the exchange "
-                           "runs over local HBM and this is not an NVLink number"},
-        "e2e": {"value": N * t / run_s, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 16, "last_j": str(res.bits.j),
-                "what": "ShardedShorEngine.run over the C ABI (shs_shards_run): exchange, probs, "
-                        "digit sum and measurement on every device, stages ordered across ranks "
-                        "by IPC events; bit string returned to the host"},
+        "nvlink": {"kernel": "k_x2_pack (peer stores into the receivers' streams)",
+                   "achieved": ex_gbs, "peak": nvlink_peak, "unit": "GB/s per direction",
+                   "frac": ex_gbs / nvlink_peak if ex_gbs else None,
+                   "bytes_per_gpu_per_direction_per_stage": nvlink_bytes,
+                   "note": "one GPU per process; with ranks sharing a GPU (gloo) the streams go "
+                           "through local HBM and this is not an NVLink number"},
+        "e2e": {"value": N * t / wall_per_run, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 16 + 32 * t, "last_j": str(res.bits.j),
+                "what": "ShardedShorEngine.run over the C ABI (shs_shards_run), wall clock per "
+                        "run, bit string and stage trace returned to the host"},
         "gpu_launches": launches, "clocks": clock_info,
     }
     if rank == 0:

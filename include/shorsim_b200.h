@@ -287,10 +287,11 @@ int shs_shard_kahan(const shs_shard* shard);
 int shs_shard_kahan_probs(shs_shard* shard, double* p0, double* p1);
 /* correctly rounded p0, p1 from summed exact digits (host-side, no device) */
 int shs_digits_to_probs(const uint64_t digits[SHS_DIGITS], double* p0, double* p1);
-/* per-kernel CUDA-event times like shs_engine_kernel_times: kind 0 probs,
- * 1 exchange, 2 collapse */
+/* per-kernel CUDA-event times like shs_engine_kernel_times (each timed launch
+ * synchronises its stream): kind 0 probs, 1 exchange (v1), 2 collapse,
+ * 3 pack and 4 unpack (exchange v2, device-resident runs) */
 int shs_shard_set_timing(shs_shard* shard, int32_t enable);
-int shs_shard_kernel_times(const shs_shard* shard, double ms[3], uint64_t launches[3]);
+int shs_shard_kernel_times(const shs_shard* shard, double ms[5], uint64_t launches[5]);
 uint64_t shs_shard_launch_count(const shs_shard* shard);
 void* shs_shard_stream(const shs_shard* shard);
 

@@ -32,9 +32,8 @@
 
 namespace shs {
 
-constexpr int kX2Warps = 8;
+constexpr int kX2Warps = 4;  // one band per warp
 constexpr int kX2Threads = 32 * kX2Warps;
-constexpr int kX2ColsPerWarp = kCols / kX2Warps;  // 4 columns of a 32-column chunk per warp
 
 struct X2Params {
     TileParams tp;          // plan (A, m, H, u, v, du, dv, ntiles); X / Y unused
@@ -51,6 +50,7 @@ struct X2Params {
     const double2* src[kMaxShards];
     // off[(peer) * (nbands + 1) + b]: pack = off(b, me, peer), unpack = off(b, peer, me)
     const unsigned long long* off;
+    uint64_t mstep[33];     // c * m mod N, c <= 32 (host-computed)
 };
 
 __device__ __forceinline__ int x2_owner(uint64_t x, uint64_t S, uint64_t S_inv) {
@@ -59,226 +59,369 @@ __device__ __forceinline__ int x2_owner(uint64_t x, uint64_t S, uint64_t S_inv) 
     return static_cast<int>(q);
 }
 
-// The rows of band b: z (start), len, the owner of its first element and the
-// column where the owner changes (rows are shorter than a shard: at most one
-// change; ~0 when none).
-struct X2Rows {
-    uint64_t z[kRows], len[kRows], cut[kRows];
-    int own[kRows];
-    uint64_t maxlen;
+// The warp's band: lane k holds row j0 + k — its start z, length, the owner of
+// its first element and the column where the owner changes (rows are shorter
+// than a shard: at most one change; ~0 when none).
+struct X2Row {
+    uint64_t z, len, cut;
+    int own;
 };
 
-__device__ __forceinline__ void x2_load_rows(const X2Params& p, uint64_t b, X2Rows& R) {
-    const int t = threadIdx.x;
-    if (t < kRows) {
-        const uint64_t j = b * kRows + t;
-        const uint64_t len = tile_row_len(j, p.tp);
-        const uint64_t z = len ? mulmod_shoup(j, p.tp.A, p.tp.A_sh, p.N) : 0;
-        R.z[t] = z;
-        R.len[t] = len;
-        const int o = x2_owner(z, p.S, p.S_inv);
-        R.own[t] = o;
-        const uint64_t end = (uint64_t(o) + 1) * p.S;  // first index of the next shard
-        R.cut[t] = z + len > end ? end - z : ~0ull;
-    }
-    __syncthreads();
-    if (t == 0) {
-        uint64_t mx = 0;
-        for (int k = 0; k < kRows; ++k) mx = R.len[k] > mx ? R.len[k] : mx;
-        R.maxlen = mx;
-    }
-    __syncthreads();
+__device__ __forceinline__ X2Row x2_row(const X2Params& p, uint64_t j) {
+    X2Row r;
+    r.len = tile_row_len(j, p.tp);
+    r.z = r.len ? mulmod_shoup(j, p.tp.A, p.tp.A_sh, p.N) : 0;
+    r.own = x2_owner(r.z, p.S, p.S_inv);
+    const uint64_t end = (uint64_t(r.own) + 1) * p.S;  // first index of the next shard
+    r.cut = r.z + r.len > end ? end - r.z : ~0ull;
+    return r;
 }
 
-// (src owner, dst owner) of element (k, i): valid == false past the row's end
-struct X2Elem {
-    bool valid;
-    int qs, rd;
-    uint64_t src;
-};
-
-__device__ __forceinline__ X2Elem x2_elem(const X2Params& p, const X2Rows& R, uint64_t col_src,
-                                          int k, uint64_t i) {
-    X2Elem e;
-    e.valid = i < R.len[k];
-    uint64_t s = col_src + k;  // (j0 + i m + k) mod N, col_src < N
-    if (s >= p.N) s -= p.N;
-    e.src = s;
-    e.qs = x2_owner(s, p.S, p.S_inv);
-    e.rd = R.own[k] + (i >= R.cut[k] ? 1 : 0);
-    return e;
+__device__ __forceinline__ uint64_t warp_max(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
 }
 
-// count(b, me, r) (kSend) or count(b, q, me) for every band of the plan, into
+// Pack side of band b, canonical order (column i ascending, then row k): the
+// columns whose 32-element source run touches this shard, kX2Batch at a time
+// (their loads issued together); lane k takes element (k, i). A row's
+// destination rank only changes at its cut column, so the lanes' destination
+// groups (match_any over the rows) are recomputed only when a cut is passed;
+// per column the group is that mask & the column's ballot of live elements.
+// `emit(n, live[], r[], grp[], v[])` sees each batch of n columns (r: this
+// lane's row's rank).
+constexpr int kX2Batch = 8;
+
+template <typename Emit>
+__device__ __forceinline__ void x2_pack_band(const X2Params& p, uint64_t b, bool load, Emit&& emit) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t j0 = b * kRows;
+    const X2Row row = x2_row(p, j0 + lane);
+    const uint64_t maxlen = warp_max(row.len);
+    const uint64_t lo = uint64_t(p.me) * p.S, hi = lo + p.S;
+    const uint64_t m32 = p.mstep[32];  // source advance per 32 columns
+    // lane c: the source run start of column i0 + c
+    uint64_t cs = addmod(j0, p.mstep[lane], p.N);
+    // destination groups valid for columns below next_cut
+    uint64_t next_cut = 0;
+    int r = 0;
+    unsigned rowgrp = 0;
+    unsigned pend = 0;      // touched columns of the current 32-column group not yet emitted
+    uint64_t pend_i0 = 0;
+    unsigned whole = 0;
+    uint64_t pend_cs = cs;
+    uint64_t i0 = 0;
+    bool live[kX2Batch];
+    double2 v[kX2Batch];
+    unsigned grp[kX2Batch];
+    int rr[kX2Batch];
+    int n = 0;
+    // gather kX2Batch touched columns (possibly from several 32-column groups),
+    // then emit; every guard below is warp-uniform
+    while (true) {
+        while (!pend && i0 < maxlen) {  // next group with touched columns
+            const uint64_t last = cs + (kRows - 1) >= p.N ? cs + (kRows - 1) - p.N : cs + (kRows - 1);
+            const bool in0 = cs >= lo && cs < hi, in1 = last >= lo && last < hi;
+            pend = __ballot_sync(0xffffffffu, i0 + lane < maxlen && (in0 || in1));
+            whole = __ballot_sync(0xffffffffu, in0 && in1 && last > cs);  // no straddle
+            pend_i0 = i0;
+            pend_cs = cs;
+            i0 += 32;
+            cs = addmod(cs, m32, p.N);
+        }
+        if (!pend && n == 0) break;
+        if (pend) {
+            const int c = __ffs(pend) - 1;
+            pend &= pend - 1;
+            const uint64_t i = pend_i0 + c;
+            const uint64_t c0 = __shfl_sync(0xffffffffu, pend_cs, c);
+            uint64_t s = c0 + lane;
+            if (s >= p.N) s -= p.N;
+            const bool lv = i < row.len && (((whole >> c) & 1u) || (s >= lo && s < hi));
+            if (i >= next_cut) {  // regroup the rows by destination
+                r = row.own + (i >= row.cut ? 1 : 0);
+                rowgrp = __match_any_sync(0xffffffffu, r);
+                uint64_t nc = row.cut > i && row.cut < row.len ? row.cut : ~0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const uint64_t w = __shfl_xor_sync(0xffffffffu, nc, o);
+                    nc = w < nc ? w : nc;
+                }
+                next_cut = nc;
+            }
+            const unsigned g = rowgrp & __ballot_sync(0xffffffffu, lv);
+            const double2 val = load && lv ? __ldg(p.sel + (s - lo)) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < kX2Batch; ++t)
+                if (t == n) {
+                    live[t] = lv;
+                    grp[t] = g;
+                    rr[t] = r;
+                    v[t] = val;
+                }
+            ++n;
+        }
+        if (n == kX2Batch || (!pend && i0 >= maxlen)) {
+            emit(n, live, rr, grp, v);
+            n = 0;
+        }
+    }
+}
+
+// Unpack side of band b: this shard's rows of the band, compacted onto the
+// lanes (lane L: row my[L % m], column offset L / m), so a warp step covers
+// floor(32 / m) columns in canonical order (column, then row); kX2Batch steps
+// per `take(n, mine[], q[], grp[], z[])` call.
+template <typename Take>
+__device__ __forceinline__ void x2_unpack_band(const X2Params& p, uint64_t b, Take&& take) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t j0 = b * kRows;
+    const X2Row row = x2_row(p, j0 + lane);
+    const bool has = row.len && (row.own == p.me || (row.cut != ~0ull && row.own + 1 == p.me));
+    const unsigned rows = __ballot_sync(0xffffffffu, has);
+    if (!rows) return;
+    const int m = __popc(rows);
+    const int cpi = 32 / m;  // columns per warp step
+    // lane L serves row k = the (L % m)-th set bit of rows
+    int k = 0;
+    {
+        unsigned rr = rows;
+        for (int t = 0; t < lane % m; ++t) rr &= rr - 1;
+        k = __ffs(rr) - 1;
+    }
+    const int coff = lane / m;
+    const bool lane_on = lane < cpi * m;
+    const uint64_t z = __shfl_sync(0xffffffffu, row.z, k);
+    const uint64_t len = __shfl_sync(0xffffffffu, row.len, k);
+    const uint64_t cut = __shfl_sync(0xffffffffu, row.cut, k);
+    const int own = __shfl_sync(0xffffffffu, row.own, k);
+    const uint64_t maxlen = warp_max(has ? row.len : 0);
+    // source run start of this lane's column, advanced by cpi columns per step
+    const uint64_t step = p.mstep[cpi];
+    uint64_t cs = addmod(j0, p.mstep[coff], p.N);
+    bool mine[kX2Batch];
+    int qq[kX2Batch];
+    unsigned grp[kX2Batch];
+    uint64_t zz[kX2Batch];
+    for (uint64_t i0 = 0; i0 < maxlen; i0 += uint64_t(cpi) * kX2Batch) {
+        int n = 0;
+#pragma unroll
+        for (int t = 0; t < kX2Batch; ++t) {
+            const uint64_t i = i0 + uint64_t(t) * cpi + coff;
+            const bool mn = lane_on && i < len && own + (i >= cut ? 1 : 0) == p.me;
+            uint64_t s = cs + k;
+            if (s >= p.N) s -= p.N;
+            qq[t] = mn ? x2_owner(s, p.S, p.S_inv) : -1;
+            mine[t] = mn;
+            grp[t] = __match_any_sync(0xffffffffu, qq[t]);
+            zz[t] = z + i;
+            cs = addmod(cs, step, p.N);
+            if (i0 + uint64_t(t) * cpi < maxlen) n = t + 1;
+        }
+        take(n, mine, qq, grp, zz);
+    }
+}
+
+// count(b, me, r) (kSend) or count(b, q, me) for every band, into
 // counts[peer * (nbands + 1) + b]
 template <bool kSend>
 __global__ void __launch_bounds__(kX2Threads) k_x2_count(X2Params p,
                                                          unsigned long long* __restrict__ counts) {
-    __shared__ X2Rows R;
-    __shared__ unsigned int cnt[kMaxShards];
+    __shared__ unsigned int cnt[kX2Warps][kMaxShards];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t nb = p.tp.ntiles;
-    for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        if (threadIdx.x < kMaxShards) cnt[threadIdx.x] = 0;
-        x2_load_rows(p, b, R);
-        const uint64_t j0 = b * kRows;
-        for (uint64_t i = warp; i < R.maxlen; i += kX2Warps) {
-            const uint64_t cs = addmod(j0, mulmod_shoup(i, p.tp.m, p.tp.m_sh, p.N), p.N);
-            const X2Elem e = x2_elem(p, R, cs, lane, i);
-            const bool mine = e.valid && (kSend ? e.qs == p.me : e.rd == p.me);
-            const int peer = mine ? (kSend ? e.rd : e.qs) : -1;
-            const unsigned grp = __match_any_sync(0xffffffffu, peer);
-            if (mine && (grp & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[peer], __popc(grp));
-        }
-        __syncthreads();
-        if (threadIdx.x < p.G) counts[uint64_t(threadIdx.x) * (nb + 1) + b] = cnt[threadIdx.x];
-        __syncthreads();
-    }
-}
-
-// Chunk bookkeeping shared by pack and unpack: per-column element counts per
-// peer, then their exclusive prefix in column order (one warp-wide scan per peer).
-struct X2Chunk {
-    unsigned int colcnt[kMaxShards][kCols];   // [peer][column]
-    unsigned int colbase[kMaxShards][kCols];  // exclusive prefix over columns
-    unsigned int total[kMaxShards];
-};
-
-__device__ __forceinline__ void x2_chunk_prefix(X2Chunk& C, int G) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int g = warp; g < G; g += kX2Warps) {
-        const unsigned v = C.colcnt[g][lane];
-        unsigned x = v;
+    for (uint64_t b = uint64_t(blockIdx.x) * kX2Warps + warp; b < nb;
+         b += uint64_t(gridDim.x) * kX2Warps) {
+        if (lane < kMaxShards) cnt[warp][lane] = 0;
+        __syncwarp();
+        auto add = [&](int n, const bool* mine, const int* peer, const unsigned* grp) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        C.colbase[g][lane] = x - v;
-        if (lane == 31) C.total[g] = x;
+            for (int t = 0; t < kX2Batch; ++t)
+                if (t < n && mine[t] && (grp[t] & ((1u << lane) - 1)) == 0)
+                    atomicAdd(&cnt[warp][peer[t]], __popc(grp[t]));
+            __syncwarp();
+        };
+        if (kSend)
+            x2_pack_band(p, b, false, [&](int n, const bool* live, const int* r,
+                                          const unsigned* grp, const double2*) {
+                add(n, live, r, grp);
+            });
+        else
+            x2_unpack_band(p, b, [&](int n, const bool* mine, const int* q, const unsigned* grp,
+                                     const uint64_t*) { add(n, mine, q, grp); });
+        __syncwarp();
+        if (lane < p.G) counts[uint64_t(lane) * (nb + 1) + b] = cnt[warp][lane];
+        __syncwarp();
     }
-    __syncthreads();
 }
 
-// one column of a chunk: element (lane, i) classified against this shard's side
-// (pack: its sources; unpack: its destinations), grouped by the other side's rank
-struct X2Col {
-    X2Elem e;
-    int peer;      // -1: not this shard's element
-    unsigned grp;  // lanes of this column with the same peer
-};
-
-template <bool kPack>
-__device__ __forceinline__ X2Col x2_col(const X2Params& p, const X2Rows& R, uint64_t j0,
-                                        uint64_t i, int lane) {
-    X2Col c;
-    const uint64_t cs = addmod(j0, mulmod_shoup(i, p.tp.m, p.tp.m_sh, p.N), p.N);
-    c.e = x2_elem(p, R, cs, lane, i);
-    const bool mine = c.e.valid && (kPack ? c.e.qs == p.me : c.e.rd == p.me);
-    c.peer = mine ? (kPack ? c.e.rd : c.e.qs) : -1;
-    c.grp = __match_any_sync(0xffffffffu, c.peer);
-    return c;
-}
-
-__device__ __forceinline__ void x2_count_col(X2Chunk& C, const X2Col& c, int col, int lane) {
-    if (c.peer >= 0 && (c.grp & ((1u << lane) - 1)) == 0) C.colcnt[c.peer][col] = __popc(c.grp);
-}
-
-// pack: this shard's source elements of the round's bands into the receivers' streams
+// pack: this shard's source elements of the round's bands into the receivers'
+// streams. Per band a row's destination rank only changes at its cut column,
+// so for a "regular" column (its source run inside this shard, every live row
+// still running, no cut passed) every lane's stream slot just advances by its
+// destination group's size: the fast path is a load and a store per element
+// (kX2Batch columns' loads in flight). Other columns (band tails, run
+// straddles, cuts) take the general path; both write the canonical order.
 __global__ void __launch_bounds__(kX2Threads) k_x2_pack(X2Params p) {
-    __shared__ X2Rows R;
-    __shared__ X2Chunk C;
-    __shared__ unsigned long long pos[kMaxShards];  // band's next slot per receiver (round-relative)
+    __shared__ unsigned long long pos[kX2Warps][kMaxShards];  // next slot per receiver
+    __shared__ double2* dstp[kMaxShards];  // (dynamically indexed: shared, not param space)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < kMaxShards) dstp[threadIdx.x] = p.dst[threadIdx.x];
+    __syncthreads();
     const uint64_t nb = p.tp.ntiles;
-    const uint64_t lo = uint64_t(p.me) * p.S;
-    for (uint64_t b = p.b0 + blockIdx.x; b < p.b1; b += gridDim.x) {
-        x2_load_rows(p, b, R);
-        if (threadIdx.x < p.G) {
-            const unsigned long long* o = p.off + uint64_t(threadIdx.x) * (nb + 1);
-            pos[threadIdx.x] = o[b] - o[p.b0];
+    const uint64_t lo = uint64_t(p.me) * p.S, hi = lo + p.S;
+    const unsigned lt = (1u << lane) - 1;
+    for (uint64_t b = p.b0 + uint64_t(blockIdx.x) * kX2Warps + warp; b < p.b1;
+         b += uint64_t(gridDim.x) * kX2Warps) {
+        if (lane < p.G) {
+            const unsigned long long* o = p.off + uint64_t(lane) * (nb + 1);
+            pos[warp][lane] = o[b] - o[p.b0];
         }
+        __syncwarp();
         const uint64_t j0 = b * kRows;
-        for (uint64_t i0 = 0; i0 < R.maxlen; i0 += kCols) {
-            for (int k = threadIdx.x; k < kMaxShards * kCols; k += kX2Threads)
-                (&C.colcnt[0][0])[k] = 0;
-            __syncthreads();
-            X2Col col[kX2ColsPerWarp];
-            double2 v[kX2ColsPerWarp];
+        const X2Row row = x2_row(p, j0 + lane);
+        const uint64_t maxlen = warp_max(row.len);
+        uint64_t minlen = row.len ? row.len : ~0ull;
 #pragma unroll
-            for (int h = 0; h < kX2ColsPerWarp; ++h) {
-                const int c = warp + kX2Warps * h;
-                col[h] = x2_col<true>(p, R, j0, i0 + c, lane);
-                v[h] = col[h].peer >= 0 ? __ldg(p.sel + (col[h].e.src - lo)) : make_double2(0.0, 0.0);
-                x2_count_col(C, col[h], c, lane);
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t w = __shfl_xor_sync(0xffffffffu, minlen, o);
+            minlen = w < minlen ? w : minlen;
+        }
+        const unsigned base = __ballot_sync(0xffffffffu, row.len > 0);
+        // destination groups (valid below next_cut) and the fast-path pointer
+        uint64_t next_cut = 0;
+        int r = 0;
+        unsigned rowgrp = 0, gsize = 0, rank = 0;
+        double2* ptr = nullptr;
+        uint64_t nreg = 0;  // regular columns written since pos was last updated
+        auto flush = [&]() {  // fold the fast path's advance into pos
+            if (nreg) {
+                if (row.len && (rowgrp & base & lt) == 0) pos[warp][r] += nreg * gsize;
+                nreg = 0;
             }
-            __syncthreads();
-            x2_chunk_prefix(C, p.G);
+            __syncwarp();
+        };
+        auto regroup = [&](uint64_t i) {  // rows -> destination groups at column i
+            r = row.own + (i >= row.cut ? 1 : 0);
+            rowgrp = __match_any_sync(0xffffffffu, row.len ? r : -1);
+            uint64_t nc = row.cut > i && row.cut < row.len ? row.cut : ~0ull;
 #pragma unroll
-            for (int h = 0; h < kX2ColsPerWarp; ++h) {
-                const int c = warp + kX2Warps * h;
-                const int g = col[h].peer;
-                if (g >= 0) {
-                    const unsigned rank = __popc(col[h].grp & ((1u << lane) - 1));
-                    p.dst[g][pos[g] + C.colbase[g][c] + rank] = v[h];
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t w = __shfl_xor_sync(0xffffffffu, nc, o);
+                nc = w < nc ? w : nc;
+            }
+            next_cut = nc;
+            gsize = __popc(rowgrp & base);
+            rank = __popc(rowgrp & base & lt);
+        };
+        auto repoint = [&]() {
+            ptr = row.len ? dstp[r] + pos[warp][r] + rank : nullptr;
+        };
+        uint64_t cs = addmod(j0, p.mstep[lane], p.N);  // lane c: source run of column i0 + c
+        for (uint64_t i0 = 0; i0 < maxlen; i0 += 32) {
+            const uint64_t last = cs + (kRows - 1) >= p.N ? cs + (kRows - 1) - p.N : cs + (kRows - 1);
+            const bool in0 = cs >= lo && cs < hi, in1 = last >= lo && last < hi;
+            unsigned cols = __ballot_sync(0xffffffffu, i0 + lane < maxlen && (in0 || in1));
+            const unsigned whole = __ballot_sync(0xffffffffu, in0 && in1 && last > cs);
+            while (cols) {
+                int ci[kX2Batch];
+                int n = 0;
+                bool regular = true;
+#pragma unroll
+                for (int t = 0; t < kX2Batch; ++t) {
+                    ci[t] = cols ? __ffs(cols) - 1 : -1;
+                    if (ci[t] >= 0) {
+                        cols &= cols - 1;
+                        n = t + 1;
+                        const uint64_t i = i0 + ci[t];
+                        regular = regular && ((whole >> ci[t]) & 1u) && i < minlen && i < next_cut;
+                    }
+                }
+                if (regular) {  // all n columns: one load and one store per lane each
+                    if (nreg == 0) repoint();
+                    double2 v[kX2Batch];
+#pragma unroll
+                    for (int t = 0; t < kX2Batch; ++t)
+                        if (t < n) {
+                            const uint64_t c0 = __shfl_sync(0xffffffffu, cs, ci[t]);
+                            uint64_t sx = c0 + lane;
+                            if (sx >= p.N) sx -= p.N;
+                            if (row.len) v[t] = __ldg(p.sel + (sx - lo));
+                        }
+#pragma unroll
+                    for (int t = 0; t < kX2Batch; ++t)
+                        if (t < n && row.len) {
+                            *ptr = v[t];
+                            ptr += gsize;
+                        }
+                    nreg += n;
+                    continue;
+                }
+                flush();
+#pragma unroll 1
+                for (int t = 0; t < n; ++t) {  // the general path, column by column
+                    const uint64_t i = i0 + ci[t];
+                    if (i >= next_cut) regroup(i);
+                    const uint64_t c0 = __shfl_sync(0xffffffffu, cs, ci[t]);
+                    uint64_t sx = c0 + lane;
+                    if (sx >= p.N) sx -= p.N;
+                    const bool lv = i < row.len && sx >= lo && sx < hi;
+                    const unsigned g = rowgrp & __ballot_sync(0xffffffffu, lv);
+                    const unsigned below = g & lt;
+                    if (lv) dstp[r][pos[warp][r] + __popc(below)] = __ldg(p.sel + (sx - lo));
+                    __syncwarp();
+                    if (lv && !below) pos[warp][r] += __popc(g);
+                    __syncwarp();
                 }
             }
-            __syncthreads();
-            if (threadIdx.x < p.G) pos[threadIdx.x] += C.total[threadIdx.x];
+            cs = addmod(cs, p.mstep[32], p.N);
         }
-        __syncthreads();
+        flush();
     }
 }
 
 // unpack: this shard's destination elements of the round's bands from the
-// senders' streams into P (rows through a shared-memory transpose)
+// senders' streams into P (a row's columns of one warp step are contiguous)
 __global__ void __launch_bounds__(kX2Threads) k_x2_unpack(X2Params p) {
-    __shared__ X2Rows R;
-    __shared__ X2Chunk C;
-    __shared__ unsigned long long pos[kMaxShards];  // band's next slot per sender (round-relative)
-    __shared__ double2 tile[kRows][kCols + 1];
+    __shared__ unsigned long long pos[kX2Warps][kMaxShards];  // next slot per sender
+    __shared__ const double2* srcp[kMaxShards];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < kMaxShards) srcp[threadIdx.x] = p.src[threadIdx.x];
+    __syncthreads();
     const uint64_t nb = p.tp.ntiles;
     const uint64_t lo = uint64_t(p.me) * p.S;
-    for (uint64_t b = p.b0 + blockIdx.x; b < p.b1; b += gridDim.x) {
-        x2_load_rows(p, b, R);
-        if (threadIdx.x < p.G) {
-            const unsigned long long* o = p.off + uint64_t(threadIdx.x) * (nb + 1);
-            pos[threadIdx.x] = o[b] - o[p.b0];
+    for (uint64_t b = p.b0 + uint64_t(blockIdx.x) * kX2Warps + warp; b < p.b1;
+         b += uint64_t(gridDim.x) * kX2Warps) {
+        if (lane < p.G) {
+            const unsigned long long* o = p.off + uint64_t(lane) * (nb + 1);
+            pos[warp][lane] = o[b] - o[p.b0];
         }
-        const uint64_t j0 = b * kRows;
-        for (uint64_t i0 = 0; i0 < R.maxlen; i0 += kCols) {
-            for (int k = threadIdx.x; k < kMaxShards * kCols; k += kX2Threads)
-                (&C.colcnt[0][0])[k] = 0;
-            __syncthreads();
-            X2Col col[kX2ColsPerWarp];
+        __syncwarp();
+        x2_unpack_band(p, b, [&](int n, const bool* mine, const int* q, const unsigned* grp,
+                                 const uint64_t* z) {
+            unsigned long long at[kX2Batch];
 #pragma unroll
-            for (int h = 0; h < kX2ColsPerWarp; ++h) {
-                const int c = warp + kX2Warps * h;
-                col[h] = x2_col<false>(p, R, j0, i0 + c, lane);
-                x2_count_col(C, col[h], c, lane);
-            }
-            __syncthreads();
-            x2_chunk_prefix(C, p.G);
-#pragma unroll
-            for (int h = 0; h < kX2ColsPerWarp; ++h) {
-                const int c = warp + kX2Warps * h;
-                const int g = col[h].peer;
-                if (g >= 0) {
-                    const unsigned rank = __popc(col[h].grp & ((1u << lane) - 1));
-                    tile[lane][c] = p.src[g][pos[g] + C.colbase[g][c] + rank];
+            for (int t = 0; t < kX2Batch; ++t) {  // stream positions first (counters only) ...
+                if (t < n && mine[t]) {
+                    const unsigned below = grp[t] & ((1u << lane) - 1);
+                    at[t] = pos[warp][q[t]] + __popc(below);
+                    if (!below) pos[warp][q[t]] += __popc(grp[t]);
                 }
+                __syncwarp();
             }
-            __syncthreads();
-            for (int k = warp; k < kRows; k += kX2Warps) {  // row runs: lane = column
-                const uint64_t i = i0 + lane;
-                if (i < R.len[k] && R.own[k] + (i >= R.cut[k] ? 1 : 0) == p.me)
-                    p.P[R.z[k] + i - lo] = tile[k][lane];
-            }
-            if (threadIdx.x < p.G) pos[threadIdx.x] += C.total[threadIdx.x];
-            __syncthreads();
-        }
-        __syncthreads();
+            double2 v[kX2Batch];
+#pragma unroll
+            for (int t = 0; t < kX2Batch; ++t)  // ... then every load of the batch in flight
+                if (t < n && mine[t]) v[t] = srcp[q[t]][at[t]];
+#pragma unroll
+            for (int t = 0; t < kX2Batch; ++t)
+                if (t < n && mine[t]) p.P[z[t] - lo] = v[t];
+        });
+        __syncwarp();
     }
 }
 

@@ -120,8 +120,8 @@ struct shs_shard {
     // instrumentation
     bool timing = false;
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    double kms[3] = {0, 0, 0};
-    uint64_t klaunch[3] = {0, 0, 0};
+    double kms[5] = {0, 0, 0, 0, 0};  // probs, exchange v1, collapse, pack, unpack
+    uint64_t klaunch[5] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
     // device-resident runs (shard_run): stage slots and host-mapped records as
     // the single engine's, this shard's exact digits per stage parity (read by
@@ -196,17 +196,19 @@ int shard_guard(shs_shard* sh, F&& f) {
 }
 
 template <typename F>
-int shard_launch(shs_shard* sh, int kind, F&& f) {
-    static const char* kNames[3] = {"shs shard probs", "shs shard exchange", "shs shard collapse"};
+int shard_launch(shs_shard* sh, int kind, F&& f, cudaStream_t st = nullptr) {
+    static const char* kNames[5] = {"shs shard probs", "shs shard exchange", "shs shard collapse",
+                                    "shs shard pack", "shs shard unpack"};
     nvtxRangePushA(kNames[kind]);
     struct Pop {
         ~Pop() { nvtxRangePop(); }
     } pop;
-    if (sh->timing) cudaEventRecord(sh->ev[0], sh->stream);
+    if (!st) st = sh->stream;
+    if (sh->timing) cudaEventRecord(sh->ev[0], st);
     f();
     cudaError_t err = cudaGetLastError();
     if (sh->timing) {
-        cudaEventRecord(sh->ev[1], sh->stream);
+        cudaEventRecord(sh->ev[1], st);
         cudaEventSynchronize(sh->ev[1]);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, sh->ev[0], sh->ev[1]);
@@ -382,6 +384,7 @@ X2Params x2_params(const shs_shard* sh, uint32_t s) {
     p.me = static_cast<int>(sh->rank);
     p.sel = sh->buf[sh->parity];
     p.P = sh->buf[sh->parity ^ 1];
+    for (uint64_t c = 0; c <= 32; ++c) p.mstep[c] = mulmod(p.tp.m, c, sh->N);
     return p;
 }
 
@@ -416,8 +419,9 @@ std::vector<uint64_t> x2_round_bounds(const TilePlanHost& pl, uint64_t N, uint32
 
 uint64_t x2_band(const shs_shard* sh, uint32_t s, uint32_t k) { return sh->x2_bounds[s][k]; }
 
-int x2_grid(const shs_shard* sh, uint64_t bands) {
-    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(bands, 8ull * sh->num_sms)));
+int x2_grid(const shs_shard* sh, uint64_t bands) {  // one band per warp
+    const uint64_t ctas = (bands + kX2Warps - 1) / kX2Warps;
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ctas, 12ull * sh->num_sms)));
 }
 
 // round k of stage s, global round g: this shard's pack (its pack stream)
@@ -431,11 +435,9 @@ int launch_x2_pack(shs_shard* sh, uint32_t s, uint32_t k, uint64_t g) {
         p.dst[r] = sh->peer_recv[r] + (g & 1) * sh->x2_slot +
                    sh->x2_dst[(uint64_t(s) * sh->x2_K + k) * sh->G + r];
     if (p.b0 == p.b1) return SHS_OK;
-    k_x2_pack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->xstream>>>(p);
-    sh->launches++;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? SHS_OK
-                            : set_error(SHS_CUDA_ERROR, std::string("k_x2_pack: ") + cudaGetErrorString(e));
+    return shard_launch(sh, 3, [&] {
+        k_x2_pack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->xstream>>>(p);
+    }, sh->xstream);
 }
 
 // ... and its unpack (main stream), into P
@@ -450,11 +452,9 @@ int launch_x2_unpack(shs_shard* sh, uint32_t s, uint32_t k, uint64_t g) {
         p.src[q] = sh->x2_recv + (g & 1) * sh->x2_slot +
                    rbase[(uint64_t(s) * sh->x2_K + k) * sh->G + q];
     if (p.b0 == p.b1) return SHS_OK;
-    k_x2_unpack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->stream>>>(p);
-    sh->launches++;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? SHS_OK
-                            : set_error(SHS_CUDA_ERROR, std::string("k_x2_unpack: ") + cudaGetErrorString(e));
+    return shard_launch(sh, 4, [&] {
+        k_x2_unpack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->stream>>>(p);
+    });
 }
 
 // Host scalars of stage s for the observed prefix (statevector.cpp:338-349).
@@ -1627,16 +1627,16 @@ int shs_digits_to_probs(const uint64_t digits[SHS_DIGITS], double* p0, double* p
 int shs_shard_set_timing(shs_shard* sh, int32_t enable) {
     if (!sh) return set_error(SHS_INVALID_ARGUMENT, "null shard");
     sh->timing = enable != 0;
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 5; ++k) {
         sh->kms[k] = 0;
         sh->klaunch[k] = 0;
     }
     return SHS_OK;
 }
 
-int shs_shard_kernel_times(const shs_shard* sh, double ms[3], uint64_t launches[3]) {
+int shs_shard_kernel_times(const shs_shard* sh, double ms[5], uint64_t launches[5]) {
     if (!sh) return set_error(SHS_INVALID_ARGUMENT, "null shard");
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 5; ++k) {
         if (ms) ms[k] = sh->kms[k];
         if (launches) launches[k] = sh->klaunch[k];
     }

@@ -136,10 +136,11 @@ class Shard:
         _raise(self._lib.shs_shard_set_timing(self._h, 1 if enable else 0))
 
     def kernel_times(self):
-        ms = (L.dbl * 3)()
-        n = (L.u64 * 3)()
+        ms = (L.dbl * 5)()
+        n = (L.u64 * 5)()
         _raise(self._lib.shs_shard_kernel_times(self._h, ms, n))
-        return {"probs": (ms[0], n[0]), "exchange": (ms[1], n[1]), "collapse": (ms[2], n[2])}
+        return {k: (ms[i], n[i]) for i, k in enumerate(("probs", "exchange", "collapse", "pack",
+                                                         "unpack"))}
 
     def launch_count(self) -> int:
         return self._lib.shs_shard_launch_count(self._h)
