@@ -142,7 +142,10 @@ public:
             have_last_ = true;
             last_seed_ = seed;
             last_idx_ = bitstring_index;
-            if (!hit && consecutive && !in_failed) hit = prefetch(seed, bitstring_index);
+            // a first call (or a jump) fetches just this run, through the same
+            // batched path (pooled buffers: no per-engine allocation); a call that
+            // continues the previous index fetches the next window
+            if (!hit && !in_failed) hit = prefetch(seed, bitstring_index, consecutive);
             if (hit) return unpack(bitstring_index - cache_lo_);
         }
         std::uint64_t j[2], js[2];
@@ -165,11 +168,11 @@ private:
     static constexpr std::uint32_t kFetchFirst = 256;     // first fetch ...
     static constexpr std::uint32_t kFetchMax = 4096;      // ... doubling up to this
 
-    // true when [idx0, idx0 + n) is now cached
-    bool prefetch(u64 seed, u64 idx0) {
+    // true when [idx0, idx0 + n) is now cached; window = false: n = 1
+    bool prefetch(u64 seed, u64 idx0, bool window) {
         const bool next = cache_n_ && cache_seed_ == seed && idx0 == cache_lo_ + cache_n_;
-        next_fetch_ = next ? std::min(2 * next_fetch_, kFetchMax) : kFetchFirst;
-        const std::uint32_t n = next_fetch_;
+        if (window) next_fetch_ = next && next_fetch_ ? std::min(2 * next_fetch_, kFetchMax) : kFetchFirst;
+        const std::uint32_t n = window ? next_fetch_ : 1;
         c_j_.resize(2 * std::size_t(n));
         c_js_.resize(2 * std::size_t(n));
         c_p1_.resize(std::size_t(n) * t_);

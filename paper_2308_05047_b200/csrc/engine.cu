@@ -1034,8 +1034,18 @@ int ensure_batch_tables(shs_engine* e) {
     SHS_CUDA(cudaMemcpy(e->d_ainvsh, invsh.data(), sizeof(uint64_t) * e->t, cudaMemcpyHostToDevice));
     SHS_CUDA(cudaMemcpy(e->d_phase, phase.data(), sizeof(double2) * phase.size(), cudaMemcpyHostToDevice));
     const size_t smem = batch_smem_bytes(e->N);
-    SHS_CUDA(cudaFuncSetAttribute(k_batch_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    {  // the attribute is process-wide: set it once per device to the largest size any
+       // engine needs (per-engine values raced between harness threads: a launch of a
+       // larger problem failed with "invalid argument" after another thread lowered it)
+        static std::mutex mu;
+        static std::vector<int> done;
+        std::lock_guard<std::mutex> g(mu);
+        if (std::find(done.begin(), done.end(), e->dev) == done.end()) {
+            SHS_CUDA(cudaFuncSetAttribute(k_batch_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(batch_smem_bytes(kBatchMaxN))));
+            done.push_back(e->dev);
+        }
+    }
     int occ = 0;
     SHS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch_runs, batch_threads(e->N), smem));
     e->batch_grid = std::max(1, occ) * e->num_sms;
@@ -1052,7 +1062,7 @@ constexpr uint64_t kLockBudget = uint64_t(16) << 30;         // HBM for the batc
 constexpr uint64_t kLockMinShots = 64;
 
 bool lockstep_ok(const shs_engine* e, uint32_t count) {
-    return count >= 2 && !e->group && !batchable(e) && e->N <= kLockMaxN;
+    return count >= 1 && !e->group && !batchable(e) && e->N <= kLockMaxN;
 }
 
 int run_many_lockstep(shs_engine* e, u64 seed, u64 idx0, uint32_t count, uint64_t* j,
