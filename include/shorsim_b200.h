@@ -267,6 +267,14 @@ int shs_shard_set_barrier(shs_shard* shard, const char* shm_name);
 int shs_shards_run(shs_shard* const* shards, uint32_t count, uint64_t seed, uint64_t idx,
                    uint64_t j[2], uint64_t j_sampled[2], shs_stage_trace* trace);
 uint64_t shs_shard_device_bytes(const shs_shard* shard);
+/* the node-local host barrier shs_shard_set_barrier installs (a sense-reversing
+ * counter in POSIX shared memory; it orders enqueues, never GPU work), on its
+ * own: every one of `parties` processes opens the same name and arrives */
+typedef struct shs_node_barrier shs_node_barrier;
+int shs_node_barrier_open(const char* shm_name, uint32_t parties, int32_t unlink_at_close,
+                          shs_node_barrier** out);
+int shs_node_barrier_arrive(shs_node_barrier* barrier);
+void shs_node_barrier_close(shs_node_barrier* barrier);
 int shs_shard_init(shs_shard* shard);
 int shs_shard_needs_exchange(const shs_shard* shard, uint32_t s);
 int shs_shard_exchange(shs_shard* shard, uint32_t s);

@@ -103,6 +103,9 @@ SIGNATURES = [
                                  C.POINTER(shs_stage_trace)]),
     ("shs_shard_device_bytes", u64, [vp]),
     ("shs_shard_kahan", C.c_int, [vp]),
+    ("shs_node_barrier_open", C.c_int, [C.c_char_p, u32, i32, C.POINTER(vp)]),
+    ("shs_node_barrier_arrive", C.c_int, [vp]),
+    ("shs_node_barrier_close", None, [vp]),
     ("shs_shard_kahan_probs", C.c_int, [vp, C.POINTER(dbl), C.POINTER(dbl)]),
     ("shs_shard_init", C.c_int, [vp]),
     ("shs_shard_needs_exchange", C.c_int, [vp, u32]),

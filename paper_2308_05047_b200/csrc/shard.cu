@@ -1283,6 +1283,33 @@ int shs_shards_run(shs_shard* const* shards, uint32_t count, uint64_t seed, uint
 }
 
 uint64_t shs_shard_device_bytes(const shs_shard* sh) { return sh ? sh->device_bytes : 0; }
+// The node-local host barrier of multi-process runs, exposed on its own (no
+// device involved) so the host side of the protocol is testable without a GPU.
+struct shs_node_barrier {
+    ShmBarrier bar;
+};
+
+int shs_node_barrier_open(const char* name, uint32_t parties, int32_t unlink_at_close,
+                          shs_node_barrier** out) {
+    if (!name || name[0] != '/' || parties < 1 || !out)
+        return set_error(SHS_INVALID_ARGUMENT, "barrier: name must start with '/', parties >= 1");
+    auto* b = new shs_node_barrier;
+    int rc = b->bar.open(name, parties, unlink_at_close != 0);
+    if (rc) {
+        delete b;
+        return rc;
+    }
+    *out = b;
+    return SHS_OK;
+}
+
+int shs_node_barrier_arrive(shs_node_barrier* b) {
+    if (!b) return set_error(SHS_INVALID_ARGUMENT, "null barrier");
+    return b->bar.arrive();
+}
+
+void shs_node_barrier_close(shs_node_barrier* b) { delete b; }
+
 
 int shs_shard_kahan(const shs_shard* sh) { return sh && sh->kahan ? 1 : 0; }
 

@@ -121,3 +121,56 @@ def test_too_many_shards_is_rejected():
     with pytest.raises(ValueError):
         shs.Shard(shs.FactoringProblem.make(15, 7, 8), shs.ErrorConfig(),
                   shs.SimulatorOptions(qubit_ceiling=64), 1, 2)
+
+
+def _barrier_worker(rank, parties, name, rounds, path, q):
+    import ctypes as C
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2308_05047_b200 import _lib as L
+    lib = L.load()
+    h = C.c_void_p()
+    try:
+        assert lib.shs_node_barrier_open(name.encode(), parties, 1 if rank == 0 else 0,
+                                         C.byref(h)) == 0
+        seen = []
+        for r in range(rounds):
+            # phase A: everyone appends "r", barrier, everyone checks all parties wrote r
+            with open(path, "a") as f:
+                f.write(f"{rank}:{r}\n")
+            assert lib.shs_node_barrier_arrive(h) == 0
+            lines = open(path).read().split()
+            seen.append(sum(1 for x in lines if x.endswith(f":{r}")))
+            assert lib.shs_node_barrier_arrive(h) == 0  # nobody starts r+1 before all checked r
+        q.put((rank, seen))
+    except Exception as exc:
+        q.put((rank, f"{type(exc).__name__}: {exc}"))
+    finally:
+        if h:
+            lib.shs_node_barrier_close(h)
+
+
+def test_node_barrier_orders_processes(tmp_path):
+    """The host barrier of multi-process sharded runs (shs_shards_run): with 3
+    processes, every process sees every party's write of round r after the
+    barrier, and nobody's write of round r+1 before the second barrier."""
+    import uuid
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    parties, rounds = 3, 40
+    name = f"/shs_test_{uuid.uuid4().hex[:12]}"
+    path = str(tmp_path / "log.txt")
+    open(path, "w").close()
+    procs = [ctx.Process(target=_barrier_worker, args=(r, parties, name, rounds, path, q))
+             for r in range(parties)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in procs:
+        rank, res = q.get(timeout=120)
+        assert not isinstance(res, str), res
+        out[rank] = res
+    for p in procs:
+        p.join(timeout=30)
+    for r in range(parties):
+        assert out[r] == [parties] * rounds
