@@ -292,6 +292,11 @@ int shs_shard_stage_read(shs_shard* shard, int32_t x, uint64_t first, uint64_t c
  * once every shard's probs of the stage is done, shs_shard_kahan_probs runs that
  * combine on this shard's device over all shards' partials (peer pointers) */
 int shs_shard_kahan(const shs_shard* shard);
+/* sparse prefix of device-resident sharded runs (on by default where it applies,
+ * as shs_engine_set_sparse): every shard runs the first stages on the support
+ * redundantly and scatters its own range; results identical */
+int shs_shard_set_sparse(shs_shard* shard, int32_t enable);
+uint32_t shs_shard_sparse_stages(const shs_shard* shard);
 int shs_shard_kahan_probs(shs_shard* shard, double* p0, double* p1);
 /* correctly rounded p0, p1 from summed exact digits (host-side, no device) */
 int shs_digits_to_probs(const uint64_t digits[SHS_DIGITS], double* p0, double* p1);

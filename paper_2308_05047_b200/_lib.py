@@ -103,6 +103,8 @@ SIGNATURES = [
                                  C.POINTER(shs_stage_trace)]),
     ("shs_shard_device_bytes", u64, [vp]),
     ("shs_shard_kahan", C.c_int, [vp]),
+    ("shs_shard_set_sparse", C.c_int, [vp, i32]),
+    ("shs_shard_sparse_stages", u32, [vp]),
     ("shs_node_barrier_open", C.c_int, [C.c_char_p, u32, i32, C.POINTER(vp)]),
     ("shs_node_barrier_arrive", C.c_int, [vp]),
     ("shs_node_barrier_close", None, [vp]),

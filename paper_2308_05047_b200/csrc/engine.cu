@@ -42,6 +42,7 @@
 #include "sparse.cuh"
 #include "lockstep.cuh"
 #include "shard_group.hpp"
+#include "sparse_plan.hpp"
 
 using namespace shs;
 
@@ -455,58 +456,14 @@ void release(shs_engine* e) {
 // The two N-amplitude buffers (sel and its successor) and the block partials
 // are allocated on first use, so engines used only for validation or index
 // maps never reserve 2 x 16 N bytes of HBM.
-// Smallest j in [1, M) with A^j = 1 (mod N), or 0 when there is none
-// (baby-step giant-step, O(sqrt M) multiplications). A is a unit mod N.
-uint64_t small_order(uint64_t A, uint64_t N, uint64_t M) {
-    if (A % N == 1) return 1;
-    uint64_t m = 1;
-    while (m * m < M) ++m;
-    std::unordered_map<uint64_t, uint64_t> baby;
-    baby.reserve(2 * m);
-    uint64_t x = 1;
-    for (uint64_t i = 0; i < m; ++i) {
-        if (i > 0 && x == 1) return i < M ? i : 0;
-        baby.emplace(x, i);
-        x = mulmod(x, A, N);
-    }
-    uint64_t ginv = 0, g = 0;  // x = A^m
-    if (mod_inverse(x, N, &ginv, &g) != SHS_OK) return 0;
-    uint64_t y = 1;
-    for (uint64_t q = 1; q <= m; ++q) {
-        y = mulmod(y, ginv, N);  // A^(-q m)
-        auto it = baby.find(y);
-        if (it != baby.end()) {
-            const uint64_t j = q * m + it->second;
-            return j < M ? j : 0;
-        }
-    }
-    return 0;
-}
-
-constexpr uint64_t kSparseMinN = 1ull << 22;  // sparse prefix from 64 MB of state
-constexpr uint64_t kSparseDensity = 16;       // support <= N / 16 (A/B: 64 / 32 / 16 / 8 -> config 4 2345 / 2299 / 2269 / 2290 ms per run)
-
-// Stages run on the support: the largest n <= t - 1 with 2^n <= N / 16 whose
-// last multiplier A_{n-1} has order >= 2^n (then every earlier stage's has
-// too: ord(A_s) >= ord(A_{n-1}) / 2^(n-1-s)), so the orbit never wraps.
+// Stages run on the support (sparse_plan.hpp): the largest n <= t - 1 with
+// 2^n <= N / 16 whose orbit does not wrap.
 uint32_t plan_sparse_prefix(const shs_engine* e) {
-    if (e->N < kSparseMinN || e->kahan) return 0;
+    if (e->kahan) return 0;
     uint64_t density = kSparseDensity;
     if (const char* d = std::getenv("SHS_SPARSE_DENSITY"))  // A/B hook (>= 8: buffers fit Y)
         density = std::max<uint64_t>(8, std::strtoull(d, nullptr, 10));
-    const uint64_t cap = e->N / density;
-    uint32_t n = 0;
-    while (n + 1 <= e->t - 1 && (uint64_t(1) << (n + 1)) <= cap) ++n;
-    if (n == 0) return 0;
-    const uint64_t ord = small_order(e->a_pows[n - 1], e->N, uint64_t(1) << n);
-    if (ord == 0) return n;
-    // ord(A_{n-1}) < 2^n: the largest s with ord(A_s) >= 2^(s+1)
-    for (uint32_t m = n; m > 0; --m) {
-        uint64_t o = ord;
-        for (uint32_t k = 0; k < n - m && o % 2 == 0; ++k) o /= 2;  // ord(A_{m-1})
-        if (o >= (uint64_t(1) << m)) return m;
-    }
-    return 0;
+    return sparse_prefix_stages(e->N, e->t, e->a_pows, e->N / density);
 }
 
 // Sparse buffers inside the current Y (free until the first dense collapse of a
@@ -1506,10 +1463,12 @@ uint32_t shs_engine_stages(const shs_engine* e) { return e ? e->t : 0; }
 int shs_engine_set_sparse(shs_engine* e, int32_t enable) {
     if (!e) return set_error(SHS_INVALID_ARGUMENT, "null engine");
     e->sparse_on = enable != 0;
+    if (e->group) group_set_sparse(e->group, enable != 0);
     return SHS_OK;
 }
 
 uint32_t shs_engine_sparse_stages(const shs_engine* e) {
+    if (e && e->group) return group_sparse_stages(e->group);
     return e && e->sparse_on ? e->sparse_n : 0;
 }
 

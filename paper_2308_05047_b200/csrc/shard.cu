@@ -29,6 +29,8 @@
 #include "device_math.cuh"
 #include "exchange.cuh"
 #include "exchange2.cuh"
+#include "sparse.cuh"
+#include "sparse_plan.hpp"
 #include <cub/cub.cuh>
 #include "host_model.hpp"
 #include "stage_kernels.cuh"
@@ -173,6 +175,19 @@ struct shs_shard {
     cudaEvent_t evp[2] = {}, evu[2] = {};  // pack / unpack of a round done (interprocess)
     cudaEvent_t pevp[kMaxShards][2] = {}, pevu[kMaxShards][2] = {};
     double x2_ms[2] = {0, 0};              // instrumentation: pack, unpack
+    // sparse prefix of device-resident runs (sparse.cuh): every shard runs the
+    // first stages on the support redundantly (identical results, no peer
+    // traffic), its buffers carved out of its P, then scatters the points of
+    // its own range into its sel
+    uint32_t sparse_n = 0;
+    bool sparse_on = true;
+    uint64_t* sZ[2] = {nullptr, nullptr};
+    double2* sV[2] = {nullptr, nullptr};
+    uint64_t* sKeys = nullptr;
+    double2* sNrm = nullptr;
+    double2* sNrm2 = nullptr;
+    void* sTemp = nullptr;
+    size_t sTempBytes = 0;
 };
 
 namespace {
@@ -455,6 +470,103 @@ int launch_x2_unpack(shs_shard* sh, uint32_t s, uint32_t k, uint64_t g) {
     return shard_launch(sh, 4, [&] {
         k_x2_unpack<<<x2_grid(sh, p.b1 - p.b0), kX2Threads, 0, sh->stream>>>(p);
     });
+}
+
+
+// ---- sparse prefix (sparse.cuh) on a shard
+
+int shard_sparse_grid(const shs_shard* sh, uint64_t n) {
+    return static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((n + kSparseThreads - 1) / kSparseThreads, sh->grid_cap)));
+}
+
+// the support buffers in this shard's P (free until the first dense stage)
+int shard_carve_sparse(shs_shard* sh) {
+    const uint64_t K = uint64_t(1) << sh->sparse_n;
+    char* p = reinterpret_cast<char*>(sh->buf[sh->parity ^ 1]);
+    char* const base = p;
+    auto take = [&](size_t bytes) {
+        char* q = p;
+        p += (bytes + 255) & ~size_t(255);
+        return q;
+    };
+    sh->sZ[0] = reinterpret_cast<uint64_t*>(take(8 * K));
+    sh->sZ[1] = reinterpret_cast<uint64_t*>(take(8 * K));
+    sh->sV[0] = reinterpret_cast<double2*>(take(16 * K));
+    sh->sV[1] = reinterpret_cast<double2*>(take(16 * K));
+    sh->sKeys = reinterpret_cast<uint64_t*>(take(8 * K));
+    sh->sNrm = reinterpret_cast<double2*>(take(16 * K));
+    sh->sNrm2 = reinterpret_cast<double2*>(take(16 * K));
+    if (!sh->sTempBytes) {
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, sh->sTempBytes, sh->sZ[0],
+                                                        sh->sKeys, sh->sNrm, sh->sNrm2,
+                                                        static_cast<int>(K), 0, 64, sh->stream);
+        if (e != cudaSuccess) return set_error(SHS_CUDA_ERROR, cudaGetErrorString(e));
+    }
+    sh->sTemp = take(sh->sTempBytes);
+    if (static_cast<size_t>(p - base) > sizeof(double2) * sh->nloc)
+        return set_error(SHS_CUDA_ERROR, "sparse prefix buffers exceed the shard's P");
+    return SHS_OK;
+}
+
+SparseParams shard_sparse_params(const shs_shard* sh, uint32_t s, const DevStage* dev) {
+    SparseParams p{};
+    p.Zo = sh->sZ[s & 1];
+    p.Vo = sh->sV[s & 1];
+    p.Ko = uint64_t(1) << s;
+    p.A = sh->a_pows[s];
+    p.A_sh = shoup(p.A, sh->N);
+    p.N = sh->N;
+    p.sc = sh->sc;
+    p.dev = dev;
+    p.Zn = sh->sZ[(s + 1) & 1];
+    p.Vn = sh->sV[(s + 1) & 1];
+    p.nrm = sh->sNrm;
+    return p;
+}
+
+// probs of sparse stage s: expand, sort by z, in-order block folds (exact digits)
+int launch_shard_sparse_probs(shs_shard* sh, uint32_t s, const DevStage* dev, int* nparts) {
+    SparseParams p = shard_sparse_params(sh, s, dev);
+    const uint64_t Kn = 2 * p.Ko;
+    int end_bit = 1;
+    while (end_bit < 64 && (sh->N - 1) >> end_bit) ++end_bit;
+    const int gf = shard_sparse_grid(sh, Kn);
+    cudaError_t sort_err = cudaSuccess;
+    int rc = shard_launch(sh, 0, [&] {
+        if (s == 0) k_sparse_init<<<1, 1, 0, sh->stream>>>(sh->sZ[0], sh->sV[0]);
+        k_sparse_expand<<<shard_sparse_grid(sh, p.Ko), kSparseThreads, 0, sh->stream>>>(p);
+        size_t bytes = sh->sTempBytes;
+        sort_err = cub::DeviceRadixSort::SortPairs(sh->sTemp, bytes, p.Zn, sh->sKeys, sh->sNrm,
+                                                   sh->sNrm2, static_cast<int>(Kn), 0, end_bit,
+                                                   sh->stream);
+        k_sparse_fold<<<gf, kSparseThreads, 0, sh->stream>>>(sh->sKeys, sh->sNrm2, Kn, sh->partials);
+    });
+    if (rc) return rc;
+    if (sort_err != cudaSuccess)
+        return set_error(SHS_CUDA_ERROR, std::string("sparse sort: ") + cudaGetErrorString(sort_err));
+    *nparts = gf;
+    return SHS_OK;
+}
+
+int launch_shard_sparse_collapse(shs_shard* sh, uint32_t s, const DevStage* dev) {
+    SparseParams p = shard_sparse_params(sh, s, dev);
+    return shard_launch(sh, 2, [&] {
+        k_sparse_collapse<<<shard_sparse_grid(sh, p.Ko), kSparseThreads, 0, sh->stream>>>(p, 0);
+    });
+}
+
+// the shard's dense sel from the support entering stage s (its own range only)
+int shard_materialize_sparse(shs_shard* sh, uint32_t s) {
+    const uint64_t K = uint64_t(1) << s;
+    double2* X = sh->buf[sh->parity];
+    SHD_CUDA(cudaMemsetAsync(X, 0, sizeof(double2) * sh->nloc, sh->stream));
+    int rc = shard_launch(sh, 0, [&] {  // (timed with the probs passes)
+        k_sparse_scatter_range<<<shard_sparse_grid(sh, K), kSparseThreads, 0, sh->stream>>>(
+            sh->sZ[s & 1], sh->sV[s & 1], K, sh->lo, sh->hi, X);
+    });
+    sh->e1 = false;
+    return rc;
 }
 
 // Host scalars of stage s for the observed prefix (statevector.cpp:338-349).
@@ -744,7 +856,61 @@ int shards_run(const std::vector<shs_shard*>& L, ShmBarrier* bar, u64 seed, u64 
         }
         return code;
     };
-    for (uint32_t s = 0; s < t; ++s) {
+    // sparse prefix: every shard runs stages 0 .. nsp-1 on the support on its own
+    // device (identical results, no peer traffic), then scatters its range
+    const uint32_t nsp = s0->sparse_on ? s0->sparse_n : 0;
+    if (nsp)
+        for (shs_shard* q : L) {
+            RUN_CUDA(cudaSetDevice(q->dev));
+            if ((status = shard_carve_sparse(q))) return status;
+        }
+    for (uint32_t s = 0; s < nsp; ++s) {
+        const int k = s & 1;
+        int nparts = 0;
+        for (shs_shard* q : L) {
+            RUN_CUDA(cudaSetDevice(q->dev));
+            q->sc = sc;
+            q->ps = s;
+            if ((status = launch_shard_sparse_probs(q, s, s == 0 ? nullptr : q->d_slots + k,
+                                                    &nparts)))
+                return drain(status);
+        }
+        if (s > 0 && (status = absorb(s - 1))) return drain(status);
+        MeasureStep ms{};
+        ms.cfg = mc;
+        ms.s = s;
+        ms.collapse = s + 1 < t ? 1 : 0;
+        ms.init_cur = s == 0 ? 1 : 0;
+        ms.sc0 = sc;
+        for (int bit = 0; bit < 2; ++bit) {
+            const StageScalars c =
+                shard_scalars(s0, s + 1, observed | (u128{static_cast<unsigned>(bit)} << s), 0.0);
+            ms.nph.phr[bit] = c.phr;
+            ms.nph.phi[bit] = c.phi;
+            ms.nph.phase_mul[bit] = c.phase_mul;
+        }
+        for (shs_shard* q : L) {
+            RUN_CUDA(cudaSetDevice(q->dev));
+            ms.cur = q->d_slots + k;
+            ms.next = q->d_slots + (k ^ 1);
+            ms.rec = q->d_rec;
+            k_finalize_measure<<<1, kFinalizeThreads, 0, q->stream>>>(q->partials, nparts, nullptr,
+                                                                    0, 0, ms);
+            q->launches++;
+            RUN_CUDA(cudaGetLastError());
+            RUN_CUDA(cudaEventRecord(q->evm[k], q->stream));
+            if ((status = launch_shard_sparse_collapse(q, s, q->d_slots + k))) return drain(status);
+        }
+    }
+    if (nsp) {  // the dense state entering stage nsp, each shard its own range
+        for (shs_shard* q : L) {
+            RUN_CUDA(cudaSetDevice(q->dev));
+            if ((status = shard_materialize_sparse(q, nsp))) return drain(status);
+            RUN_CUDA(cudaEventRecord(q->evc[(nsp - 1) & 1], q->stream));
+        }
+        if ((status = barrier())) return drain(status);
+    }
+    for (uint32_t s = nsp; s < t; ++s) {
         const int k = s & 1;
         const bool ex = stage_needs_exchange(s0, s);
         if (ex && s0->x2_ready && s0->x2_stage[s]) {
@@ -1035,6 +1201,13 @@ int group_state_gather(ShardGroup* g, int x, const uint64_t* idx, uint64_t count
     return SHS_OK;
 }
 
+int group_set_sparse(ShardGroup* g, bool on) {
+    for (shs_shard* q : g->shards) shs_shard_set_sparse(q, on ? 1 : 0);
+    return SHS_OK;
+}
+
+uint32_t group_sparse_stages(const ShardGroup* g) { return shs_shard_sparse_stages(g->shards[0]); }
+
 uint64_t group_launches(const ShardGroup* g) {
     uint64_t n = 0;
     for (const shs_shard* q : g->shards) n += q->launches;
@@ -1226,6 +1399,14 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
     sh->peer_S[rank] = sh->Sb;
     sh->peer[rank][0] = sh->buf[0];
     sh->peer[rank][1] = sh->buf[1];
+    if (!sh->kahan) {  // support points fit every shard's P (the last shard is the smallest)
+        const uint64_t smallest = sh->N - uint64_t(nshards - 1) * sh->S;
+        const uint64_t bytes = sizeof(double2) * std::min(smallest, sh->S);
+        // 88 B of carved arrays + the radix sort's ~24 B per point, 1 MB of slack
+        const uint64_t kcap = bytes > (1ull << 20) ? (bytes - (1ull << 20)) / 128 : 0;
+        sh->sparse_n = sparse_prefix_stages(sh->N, sh->t, sh->a_pows,
+                                            std::min<uint64_t>(sh->N / kSparseDensity, kcap));
+    }
     sh->device_bytes = 2 * sizeof(double2) * sh->nloc + sizeof(double) * 2 * sh->nb +
                        sizeof(unsigned long long) * (2 * kDigits * sh->grid_cap + 6 * kDigits);
     *out = sh;
@@ -1312,6 +1493,16 @@ void shs_node_barrier_close(shs_node_barrier* b) { delete b; }
 
 
 int shs_shard_kahan(const shs_shard* sh) { return sh && sh->kahan ? 1 : 0; }
+
+int shs_shard_set_sparse(shs_shard* sh, int32_t enable) {
+    if (!sh) return set_error(SHS_INVALID_ARGUMENT, "null shard");
+    sh->sparse_on = enable != 0;
+    return SHS_OK;
+}
+
+uint32_t shs_shard_sparse_stages(const shs_shard* sh) {
+    return sh && sh->sparse_on ? sh->sparse_n : 0;
+}
 
 int shs_shard_kahan_probs(shs_shard* sh, double* p0, double* p1) {
     return shard_guard(sh, [&]() -> int {

@@ -38,6 +38,8 @@ int group_state_read(ShardGroup* g, int x, uint64_t first, uint64_t count, doubl
 int group_stage_read(ShardGroup* g, int x, uint64_t first, uint64_t count, double* host);
 int group_state_gather(ShardGroup* g, int x, const uint64_t* idx, uint64_t count, double* host);
 uint64_t group_launches(const ShardGroup* g);
+int group_set_sparse(ShardGroup* g, bool on);
+uint32_t group_sparse_stages(const ShardGroup* g);
 int shard_device(const shs_shard* sh);
 uint64_t group_device_bytes(const ShardGroup* g);
 // the devices a state of N amplitudes needs (SHS_DEVICES overrides); 1 = fits one device

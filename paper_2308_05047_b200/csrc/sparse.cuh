@@ -124,4 +124,16 @@ static __global__ void k_sparse_scatter(const uint64_t* __restrict__ Z,
         X[Z[k]] = V[k];
 }
 
+// one shard's dense sel (zeroed beforehand) from the support: the points in
+// [lo, hi), at local index z - lo (the sharded engine's materialisation)
+static __global__ void k_sparse_scatter_range(const uint64_t* __restrict__ Z,
+                                              const double2* __restrict__ V, uint64_t K,
+                                              uint64_t lo, uint64_t hi, double2* __restrict__ X) {
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < K;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t z = Z[k];
+        if (z >= lo && z < hi) X[z - lo] = V[k];
+    }
+}
+
 }  // namespace shs

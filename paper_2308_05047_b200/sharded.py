@@ -113,6 +113,12 @@ class Shard:
     def sync(self):
         _raise(self._lib.shs_shard_sync(self._h))
 
+    def set_sparse(self, enable: bool):
+        _raise(self._lib.shs_shard_set_sparse(self._h, 1 if enable else 0))
+
+    def sparse_stages(self) -> int:
+        return self._lib.shs_shard_sparse_stages(self._h)
+
     def kahan(self) -> bool:
         """p0/p1 combined like the reference (sequential Kahan; small N under AUTO)"""
         return bool(self._lib.shs_shard_kahan(self._h))
@@ -233,6 +239,14 @@ class ShardedShorEngine:
     def close(self):
         for sh in self.shards:
             sh.close()
+
+    def set_sparse(self, enable: bool):
+        """sparse prefix of run() (on by default where it applies); results identical"""
+        for sh in self.shards:
+            sh.set_sparse(enable)
+
+    def sparse_stages(self) -> int:
+        return self.shards[0].sparse_stages()
 
     # -- step API (what run() is made of)
     def state_init(self):

@@ -209,3 +209,27 @@ def test_exchange_v2_equals_v1_and_single(cuda_ok, monkeypatch, G, rounds):
         assert np.array_equal(full_state(v2, x, N, stage=True), want)
     v2.close()
     v1.close()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_sparse_prefix_equals_dense(cuda_ok, G):
+    """The sparse prefix of sharded runs (every shard runs the first stages on the
+    support, then scatters its range) equals the dense sharded run and the single
+    engine (which runs its own sparse prefix) — bits, p1 and the pending state."""
+    import paper_2308_05047_b200 as shs
+    N, a, t = 4206457, 12345, 26
+    for err in (E("phase_init", 0.1), E("quantum_measure", 0.02, (0.01, 0.01, 0.0))):
+        prob = shs.FactoringProblem.make(N, a, t)
+        single = shs.IterativeShorEngine(prob, err, opts())
+        sharded = shs.ShardedShorEngine.virtual(prob, err, opts(), nshards=G)
+        assert sharded.sparse_stages() > 0
+        for idx in range(2):
+            r = single.run(8, idx)
+            same_run(sharded.run(8, idx), r)
+        for x in (0, 1):
+            want = np.ctypeslib.as_array(single.stage_read(x, 0, N))
+            assert np.array_equal(full_state(sharded, x, N, stage=True), want)
+        sharded.set_sparse(False)
+        assert sharded.sparse_stages() == 0
+        same_run(sharded.run(8, 5), single.run(8, 5))
+        sharded.close()
