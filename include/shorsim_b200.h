@@ -306,6 +306,12 @@ int shs_digits_to_probs(const uint64_t digits[SHS_DIGITS], double* p0, double* p
 int shs_shard_set_timing(shs_shard* shard, int32_t enable);
 int shs_shard_kernel_times(const shs_shard* shard, double ms[5], uint64_t launches[5]);
 uint64_t shs_shard_launch_count(const shs_shard* shard);
+/* launch timeline of the next device-resident runs (no per-launch sync): after a
+ * run, out[3 i .. 3 i + 2] = {kind (as shs_shard_kernel_times), start ms, end ms}
+ * relative to the run's start on this shard's main stream; returns the entry
+ * count (entries beyond max_entries are counted, not written) */
+int shs_shard_set_timeline(shs_shard* shard, int32_t enable);
+int64_t shs_shard_timeline(shs_shard* shard, double* out, uint64_t max_entries);
 void* shs_shard_stream(const shs_shard* shard);
 
 /* ---- the per-gate API on a device-resident state ----

@@ -121,6 +121,8 @@ SIGNATURES = [
     ("shs_shard_set_timing", C.c_int, [vp, i32]),
     ("shs_shard_kernel_times", C.c_int, [vp, C.POINTER(dbl), C.POINTER(u64)]),
     ("shs_shard_launch_count", u64, [vp]),
+    ("shs_shard_set_timeline", C.c_int, [vp, i32]),
+    ("shs_shard_timeline", C.c_int64, [vp, C.POINTER(dbl), u64]),
     ("shs_shard_stream", vp, [vp]),
     ("shs_sv_create", C.c_int, [u32, u32, i32, C.POINTER(vp)]),
     ("shs_sv_clone", C.c_int, [vp, C.POINTER(vp)]),

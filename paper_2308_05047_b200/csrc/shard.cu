@@ -122,6 +122,15 @@ struct shs_shard {
     // instrumentation
     bool timing = false;
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // timeline (shs_shard_set_timeline): start / end events of every launch, on
+    // the stream it ran on, resolved against tl0 after the run (no sync per launch)
+    struct TLRec {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    bool tl_on = false;
+    std::vector<TLRec> tl;
+    cudaEvent_t tl0 = nullptr;
     double kms[5] = {0, 0, 0, 0, 0};  // probs, exchange v1, collapse, pack, unpack
     uint64_t klaunch[5] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
@@ -220,8 +229,18 @@ int shard_launch(shs_shard* sh, int kind, F&& f, cudaStream_t st = nullptr) {
     } pop;
     if (!st) st = sh->stream;
     if (sh->timing) cudaEventRecord(sh->ev[0], st);
+    shs_shard::TLRec tr{kind, nullptr, nullptr};
+    if (sh->tl_on) {
+        cudaEventCreate(&tr.a);
+        cudaEventCreate(&tr.b);
+        cudaEventRecord(tr.a, st);
+    }
     f();
     cudaError_t err = cudaGetLastError();
+    if (sh->tl_on) {
+        cudaEventRecord(tr.b, st);
+        sh->tl.push_back(tr);
+    }
     if (sh->timing) {
         cudaEventRecord(sh->ev[1], st);
         cudaEventSynchronize(sh->ev[1]);
@@ -323,6 +342,11 @@ void release(shs_shard* sh) {
         for (cudaEvent_t e : {sh->evp[k], sh->evu[k]})
             if (e) cudaEventDestroy(e);
     if (sh->xstream) cudaStreamDestroy(sh->xstream);
+    for (auto& r : sh->tl) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    if (sh->tl0) cudaEventDestroy(sh->tl0);
     for (uint32_t q = 0; q < sh->G; ++q)
         if (sh->peer_S_ipc[q] && sh->peer_S[q])
             cudaIpcCloseMemHandle(const_cast<double*>(sh->peer_S[q]));
@@ -791,6 +815,16 @@ int shards_run(const std::vector<shs_shard*>& L, ShmBarrier* bar, u64 seed, u64 
     shs_shard* s0 = L.front();
     const uint32_t t = s0->t, G = s0->G;
     for (shs_shard* q : L) {
+        if (q->tl_on) {  // time zero of this run's timeline
+            RUN_CUDA(cudaSetDevice(q->dev));
+            if (!q->tl0) RUN_CUDA(cudaEventCreate(&q->tl0));
+            for (auto& r : q->tl) {
+                cudaEventDestroy(r.a);
+                cudaEventDestroy(r.b);
+            }
+            q->tl.clear();
+            RUN_CUDA(cudaEventRecord(q->tl0, q->stream));
+        }
         for (uint32_t r = 0; r < G; ++r)
             if (!q->peer[r][0] || !q->peer_dig[r] || !q->pevd[r][0])
                 return set_error(SHS_INVALID_ARGUMENT, "sharded run: shard " + std::to_string(r) +
@@ -1493,6 +1527,31 @@ void shs_node_barrier_close(shs_node_barrier* b) { delete b; }
 
 
 int shs_shard_kahan(const shs_shard* sh) { return sh && sh->kahan ? 1 : 0; }
+
+int shs_shard_set_timeline(shs_shard* sh, int32_t enable) {
+    if (!sh) return set_error(SHS_INVALID_ARGUMENT, "null shard");
+    sh->tl_on = enable != 0;
+    return SHS_OK;
+}
+
+int64_t shs_shard_timeline(shs_shard* sh, double* out, uint64_t max_entries) {
+    if (!sh || !sh->tl0) return 0;
+    if (cudaSetDevice(sh->dev) != cudaSuccess) return -1;
+    cudaDeviceSynchronize();
+    uint64_t n = 0;
+    for (const auto& r : sh->tl) {
+        if (n < max_entries && out) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, sh->tl0, r.a);
+            cudaEventElapsedTime(&b, sh->tl0, r.b);
+            out[3 * n] = r.kind;
+            out[3 * n + 1] = a;
+            out[3 * n + 2] = b;
+        }
+        ++n;
+    }
+    return static_cast<int64_t>(n);
+}
 
 int shs_shard_set_sparse(shs_shard* sh, int32_t enable) {
     if (!sh) return set_error(SHS_INVALID_ARGUMENT, "null shard");

@@ -151,6 +151,17 @@ class Shard:
     def launch_count(self) -> int:
         return self._lib.shs_shard_launch_count(self._h)
 
+    def set_timeline(self, enable: bool):
+        _raise(self._lib.shs_shard_set_timeline(self._h, 1 if enable else 0))
+
+    def timeline(self):
+        """[(kind, start_ms, end_ms)] of the last device-resident run's launches"""
+        n = self._lib.shs_shard_timeline(self._h, None, 0)
+        out = (L.dbl * (3 * max(n, 1)))()
+        self._lib.shs_shard_timeline(self._h, out, n)
+        kinds = ("probs", "exchange", "collapse", "pack", "unpack")
+        return [(kinds[int(out[3 * i])], out[3 * i + 1], out[3 * i + 2]) for i in range(n)]
+
     def stream_handle(self) -> int:
         return self._lib.shs_shard_stream(self._h) or 0
 
