@@ -40,6 +40,11 @@
 
 using namespace shs;
 
+// Shards of one in-process group that share a device (virtual shards): set by
+// group_create while it creates them, so each sizes its receive slots for its
+// share of the device (1 outside group_create).
+static thread_local uint32_t g_coresident = 1;
+
 // Host barrier for one-process-per-GPU sharded runs: a sense-reversing counter
 // in a POSIX shared-memory segment (every rank of a run lives on one node: the
 // NVLink domain). It orders ENQUEUES, never GPU work: a rank records its event
@@ -1117,12 +1122,15 @@ int group_create(const shs_problem& problem, const shs_error& error, const shs_o
     auto* g = new ShardGroup;
     const uint32_t G = static_cast<uint32_t>(devices.size());
     for (uint32_t q = 0; q < G; ++q) {
+        // the group's shards on this device (this one included)
+        g_coresident = static_cast<uint32_t>(std::count(devices.begin(), devices.end(), devices[q]));
         shs_options o = options;
         o.device = devices[q];
         o.n_devices = 0;
         o.devices = nullptr;
         shs_shard* sh = nullptr;
         int rc = shs_shard_create(&problem, &error, &o, q, G, &sh);
+        g_coresident = 1;
         if (rc) {
             group_destroy(g);
             return rc;
@@ -1395,8 +1403,14 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
         if ((ce = cudaMemGetInfo(&fr, &tot)) != cudaSuccess) return fail(ce, "cudaMemGetInfo");
         // a round receives ~S/K elements (more where few rows make the z-spread
         // lumpy): slots of c S / K with c = 2 when memory allows, down to 1.25,
-        // then more rounds
-        const double slot_cap = std::max(0.0, static_cast<double>(fr) - 3.0e9) / (2 * sizeof(double2));
+        // then more rounds. K is collective (every rank must cut the same rounds):
+        // a function of the device's TOTAL memory and S only, identical on
+        // identical GPUs; peers' K are checked when they attach. The device is
+        // shared by the group's g_coresident shards placed on it.
+        const double reserve = 6.0e9;  // contexts, partials, plans, scratch
+        const double state = 2.0 * sizeof(double2) * static_cast<double>(sh->S);
+        const double avail = (static_cast<double>(tot) - reserve) / g_coresident - state;
+        const double slot_cap = std::max(0.0, avail) / (2 * sizeof(double2));
         const double Sd = static_cast<double>(sh->S);
         uint32_t K = 1;
         double c = 2.0;
@@ -1453,6 +1467,8 @@ int shs_shard_attach_local(shs_shard* sh, shs_shard* peer) {
     if (!sh || !peer || peer->G != sh->G || peer->rank >= sh->G)
         return set_error(SHS_INVALID_ARGUMENT, "bad local attach");
     if (peer == sh) return SHS_OK;
+    if (peer->x2_K != sh->x2_K)
+        return set_error(SHS_INVALID_ARGUMENT, "exchange rounds differ between shards");
     void* bufs[2] = {peer->buf[0], peer->buf[1]};
     int rc = shs_shard_attach(sh, peer->rank, bufs);
     if (rc) return rc;
@@ -1612,6 +1628,7 @@ struct ShardIpcBlob {
     cudaIpcMemHandle_t recv, bases;  // exchange v2
     cudaIpcEventHandle_t evp[2], evu[2];
     int32_t has_x2;
+    uint32_t x2_K;
 };
 static_assert(sizeof(ShardIpcBlob) <= SHS_SHARD_IPC_BYTES, "SHS_SHARD_IPC_BYTES too small");
 
@@ -1624,6 +1641,7 @@ int shs_shard_ipc_handles(const shs_shard* csh, void* out) {
         SHD_CUDA(cudaIpcGetMemHandle(&b.dig, sh->d_dig2));
         SHD_CUDA(cudaIpcGetMemHandle(&b.sb, sh->Sb));
         b.has_x2 = sh->x2_recv ? 1 : 0;
+        b.x2_K = sh->x2_K;
         if (b.has_x2) {
             SHD_CUDA(cudaIpcGetMemHandle(&b.recv, sh->x2_recv));
             SHD_CUDA(cudaIpcGetMemHandle(&b.bases, sh->x2_bases));
@@ -1696,6 +1714,10 @@ int shs_shard_attach_ipc(shs_shard* sh, uint32_t peer, const void* handles) {
         sh->peer_S[peer] = static_cast<const double*>(sp);
         sh->peer_S_ipc[peer] = true;
         if (b.has_x2 && sh->x2_recv) {
+            if (b.x2_K != sh->x2_K)
+                return set_error(SHS_INVALID_ARGUMENT,
+                                 "exchange rounds differ between shards (" + std::to_string(b.x2_K) +
+                                     " vs " + std::to_string(sh->x2_K) + "): set SHS_X2_ROUNDS");
             void* rp = nullptr;
             SHD_CUDA(cudaIpcOpenMemHandle(&rp, b.recv, cudaIpcMemLazyEnablePeerAccess));
             sh->peer_recv[peer] = static_cast<double2*>(rp);

@@ -159,3 +159,30 @@ def test_above_2_32_dense_stages_vs_sparse_support_oracle(cuda_ok, oracle):
     t = 66
     kept = _forced_dense_vs_sparse_oracle(oracle, N, a, t, 21, "amplitude_init")
     assert 0 < sum(kept) < len(kept)
+
+
+@pytest.mark.slow
+def test_c4_sharded_run_equals_single(cuda_ok):
+    """Config 4 through the multi-device engine (row N1): the state split over 2
+    virtual shards of this GPU (2 x 2 x 34.4 GB + exchange-v2 receive slots, K
+    rounds sized to the remaining memory), a full device-resident run with the
+    sharded sparse prefix and exchange v2 — bits, sampled bits and every p1 equal
+    the single engine's run (exact combine at 16.7 M blocks in both)."""
+    import paper_2308_05047_b200 as shs
+    N, a = 4294967213, 5
+    err = ERRORS["quantum_measure"]
+    prob = shs.FactoringProblem.make(N, a)
+    single = shs.IterativeShorEngine(prob, err, shs.SimulatorOptions(qubit_ceiling=64))
+    r = single.run(31, 7)
+    single.close()
+    gc.collect()
+    multi = shs.IterativeShorEngine(prob, err, shs.SimulatorOptions(qubit_ceiling=64,
+                                                                  devices=[0, 0]))
+    assert multi.devices() == [0, 0] and multi.sparse_stages() > 0
+    s = multi.run(31, 7)
+    multi.close()
+    gc.collect()
+    assert s.bits.j == r.bits.j and s.j_sampled == r.j_sampled
+    assert [x.p1 for x in s.trace] == [x.p1 for x in r.trace]
+    assert [x.event.quantum_error_branch for x in s.trace] == \
+        [x.event.quantum_error_branch for x in r.trace]
