@@ -22,6 +22,7 @@
  *   6 NotInvertibleError    (the gcd is reported in shs_last_error())
  *   7 std::invalid_argument (layout / argument validation, statevector.cpp:65-72)
  *   8 CUDA error / no device (the engine never falls back to the CPU)
+ *   9 FactorizationTimeoutError (Pollard rho budget, numtheory.cpp:137, 149)
  */
 #ifndef SHORSIM_B200_H
 #define SHORSIM_B200_H
@@ -41,6 +42,7 @@ extern "C" {
 #define SHS_NOT_INVERTIBLE 6
 #define SHS_INVALID_ARGUMENT 7
 #define SHS_CUDA_ERROR 8
+#define SHS_FACTORIZATION_TIMEOUT 9 /* FactorizationTimeoutError (numtheory.cpp:137, 149) */
 
 /* ErrorKind order of proj/include/shorsim/noise.hpp:13-20 */
 #define SHS_ERR_NONE 0
@@ -397,11 +399,14 @@ int shs_shor_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t
 typedef struct {
     uint64_t B, c;
     uint32_t k, varsigma, m, ell;
+    uint64_t rho_budget; /* factorize()'s Pollard-rho step budget in recover_order
+                            (0: the reference's default 10^7) */
 } shs_ekera_params;
 typedef struct {
     int32_t classification;     /* SHS_CLASS_SUCCESS or SHS_CLASS_FAIL */
     uint8_t order_match;        /* 0/1, 2 = no known order */
-    uint8_t has_recovered_order, has_offset, pad;
+    uint8_t has_recovered_order, has_offset;
+    uint8_t timeout;            /* recover_order's factorize ran out of its rho budget */
     uint64_t k[2], r[2];        /* extract_denominator(j) */
     uint64_t recovered_order;
     int64_t candidate_offset;   /* the j' = j + offset that factored N */
@@ -412,6 +417,12 @@ int shs_ekera_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_
                           const shs_ekera_params* params, uint64_t seed, uint64_t idx0,
                           uint64_t known_order, int32_t has_known_order, int32_t device,
                           shs_ekera_outcome* out);
+
+/* factorize (numtheory.cpp:170-187) on the device: sorted prime powers of n
+ * (primes / exponents need 64 entries); SHS_FACTORIZATION_TIMEOUT when the
+ * Pollard-rho steps exceed rho_budget (0: 10^7), as the reference throws */
+int shs_factorize(uint64_t n, uint64_t rho_budget, int32_t device, uint64_t* primes,
+                  uint32_t* exponents, uint32_t* count);
 
 /* thread-local message of the last failing call */
 const char* shs_last_error(void);

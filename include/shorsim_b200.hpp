@@ -43,6 +43,7 @@ inline void throw_status(int rc) {
         case SHS_CEILING_EXCEEDED: throw CeilingExceededError(msg);
         case SHS_DEGENERATE_BRANCH: throw DegenerateBranchError(msg);
         case SHS_BUDGET_EXCEEDED: throw BudgetExceededError(msg);
+        case SHS_FACTORIZATION_TIMEOUT: throw FactorizationTimeoutError(msg);
         case SHS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case SHS_NOT_INVERTIBLE: {
             // "not invertible: gcd(a, n) = g"

@@ -372,6 +372,7 @@ class Reference:
         L.ref_shor_standard_procedure.argtypes = [u64, u64, C.c_uint, u64, u64, u64, C.c_int,
                                                   C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)]
         L.ref_multiplicative_order.argtypes = [u64, u64, u64, u64, C.POINTER(u64)]
+        L.ref_factorize.argtypes = [u64, u64, C.POINTER(u64), C.POINTER(u32), C.POINTER(u32)]
         L.ref_ekera_postprocess.argtypes = [u64, u64, C.c_uint, u64, u64, u64, u64, C.c_uint,
                                             C.c_uint, C.c_uint, C.c_uint, u64, u32, u64, C.c_int,
                                             C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)]
@@ -442,6 +443,12 @@ class Reference:
                 "candidate_offset": off if ints[3] else None,
                 "k": us[0] | (us[1] << 64), "r": us[2] | (us[3] << 64),
                 "factors": list(f[:ints[4]])}
+
+    def factorize(self, n, budget=10_000_000):
+        """[(prime, exponent)]; OracleError code 9 on FactorizationTimeoutError"""
+        pr, ex, cnt = (u64 * 64)(), (u32 * 64)(), u32()
+        _check(self.lib.ref_factorize(n, budget, pr, ex, C.byref(cnt)), self.lib)
+        return [(pr[i], ex[i]) for i in range(cnt.value)]
 
     def multiplicative_order(self, a, N, p=0, q=0):
         out = u64()

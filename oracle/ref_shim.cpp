@@ -54,6 +54,8 @@ int guarded(F&& f) {
         return fail(e, 6);
     } catch (const ConfigError& e) {
         return fail(e, 2);
+    } catch (const FactorizationTimeoutError& e) {
+        return fail(e, 9);
     } catch (const Error& e) {
         return fail(e, 1);
     } catch (const std::invalid_argument& e) {
@@ -304,6 +306,18 @@ int ref_shor_standard_procedure(uint64_t j_lo, uint64_t j_hi, unsigned t, uint64
         kr[2] = static_cast<uint64_t>(o.convergent.r);
         kr[3] = static_cast<uint64_t>(o.convergent.r >> 64);
         for (size_t i = 0; i < 4; ++i) factors[i] = i < o.factors.size() ? o.factors[i] : 0;
+    });
+}
+
+// factorize (numtheory.cpp:170-187) with an explicit rho budget
+int ref_factorize(uint64_t n, uint64_t budget, uint64_t* primes, uint32_t* exps, uint32_t* count) {
+    return guarded([&] {
+        auto f = factorize(n, budget);
+        *count = static_cast<uint32_t>(f.size());
+        for (size_t i = 0; i < f.size(); ++i) {
+            primes[i] = f[i].prime;
+            exps[i] = f[i].exponent;
+        }
     });
 }
 

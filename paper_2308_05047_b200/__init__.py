@@ -16,6 +16,7 @@ from .engine import (  # noqa: F401
     ErrorEvent,
     ErrorKind,
     FactoringProblem,
+    FactorizationTimeoutError,
     IterativeShorEngine,
     NotInvertibleError,
     PauliProbs,
@@ -36,6 +37,7 @@ from .postprocess import (  # noqa: F401
     EkeraParams,
     ekera_postprocess,
     ekera_postprocess_array,
+    factorize,
     PostProcessOutcome,
     ProblemResult,
     multiplicative_order,

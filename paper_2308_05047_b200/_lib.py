@@ -27,6 +27,7 @@ SHS_BUDGET_EXCEEDED = 5
 SHS_NOT_INVERTIBLE = 6
 SHS_INVALID_ARGUMENT = 7
 SHS_CUDA_ERROR = 8
+SHS_FACTORIZATION_TIMEOUT = 9
 
 COMBINE = {"auto": 0, "kahan": 1, "exact": 2}
 SHS_DIGITS = 80
@@ -149,6 +150,7 @@ SIGNATURES = [
                                        C.c_void_p]),
     ("shs_ekera_postprocess", C.c_int, [C.POINTER(u64), u32, u32, u64, u64, C.c_void_p, u64,
                                         u64, u64, i32, i32, C.c_void_p]),
+    ("shs_factorize", C.c_int, [u64, u64, i32, C.POINTER(u64), C.POINTER(u32), C.POINTER(u32)]),
     ("shs_last_error", C.c_char_p, []),
     ("shs_build_info", C.c_char_p, []),
 ]

@@ -180,30 +180,46 @@ __device__ bool pp_is_prime(uint64_t n) {  // is_probable_prime, numtheory.cpp:9
     return true;
 }
 
-__device__ uint64_t pp_rho(uint64_t n) {  // a nontrivial divisor of composite n (Brent)
+// Brent's rho with the reference's batch of 128 and its step budget
+// (numtheory.cpp:120-157): the budget counts rho steps over one factorize()
+// call; running out sets *timeout (FactorizationTimeoutError there). The same
+// batch, restart and backtracking order gives the same divisor, hence the same
+// recursion and the same budget use as the reference.
+__device__ uint64_t pp_rho(uint64_t n, uint64_t* budget, bool* timeout) {
     if ((n & 1) == 0) return 2;
     for (uint64_t c = 1;; ++c) {
-        uint64_t x = 2, y = 2, d = 1, q = 1, ys = 2, r = 1;
+        uint64_t x = 2, y = 2, d = 1, q = 1, ys = 0, r = 1;
+        constexpr uint64_t kBatch = 128;
         auto step = [&](uint64_t v) { return (pp_mulmod(v, v, n) + c) % n; };
         while (d == 1) {
             x = y;
             for (uint64_t i = 0; i < r; ++i) y = step(y);
-            for (uint64_t k = 0; k < r && d == 1; k += 64) {
+            for (uint64_t k = 0; k < r && d == 1; k += kBatch) {
                 ys = y;
-                const uint64_t lim = r - k < 64 ? r - k : 64;
+                const uint64_t lim = r - k < kBatch ? r - k : kBatch;
                 for (uint64_t i = 0; i < lim; ++i) {
                     y = step(y);
                     q = pp_mulmod(q, x > y ? x - y : y - x, n);
                 }
+                if (*budget < lim) {
+                    *timeout = true;
+                    return 0;
+                }
+                *budget -= lim;
                 d = pp_gcd(q, n);
             }
             r *= 2;
         }
-        if (d == n) {
+        if (d == n) {  // backtrack one by one from the last saved point
             d = 1;
             while (d == 1) {
                 ys = step(ys);
                 d = pp_gcd(x > ys ? x - ys : ys - x, n);
+                if (*budget == 0) {
+                    *timeout = true;
+                    return 0;
+                }
+                --*budget;
             }
         }
         if (d != n) return d;
@@ -211,34 +227,54 @@ __device__ uint64_t pp_rho(uint64_t n) {  // a nontrivial divisor of composite n
 }
 
 constexpr int kMaxPrimes = 32;
+constexpr uint64_t kRhoBudget = 10000000;  // factorize()'s default, numtheory.hpp:53
 
-// distinct primes of n (unsorted) appended to p[*np]
-__device__ void pp_prime_factors(uint64_t n, uint64_t* p, int* np) {
+// factorize (numtheory.cpp:170-187): trial division by the primes below 100,
+// then factor_rec's depth-first splits (d first). Primes with multiplicity are
+// appended to p[*np] in discovery order; false on a budget timeout.
+__device__ bool pp_factorize(uint64_t n, uint64_t budget, uint64_t* p, int* np, int cap) {
+    const uint8_t small[25] = {2,  3,  5,  7,  11, 13, 17, 19, 23, 29, 31, 37, 41,
+                               43, 47, 53, 59, 61, 67, 71, 73, 79, 83, 89, 97};
+    for (int i = 0; i < 25; ++i)
+        while (n % small[i] == 0) {
+            if (*np < cap) p[(*np)++] = small[i];
+            n /= small[i];
+        }
     uint64_t stack[64];
     int top = 0;
-    for (uint64_t q = 2; q < 100 && q * q <= n; ++q) {
-        if (n % q) continue;
-        p[(*np)++] = q;
-        while (n % q == 0) n /= q;
-    }
     if (n > 1) stack[top++] = n;
-    while (top) {
+    bool timeout = false;
+    while (top) {  // LIFO: push n / d, then d, so d is factored first
         const uint64_t m = stack[--top];
         if (m == 1) continue;
         if (pp_is_prime(m)) {
-            bool seen = false;
-            for (int i = 0; i < *np; ++i) seen |= p[i] == m;
-            if (!seen && *np < kMaxPrimes) p[(*np)++] = m;
+            if (*np < cap) p[(*np)++] = m;
             continue;
         }
-        const uint64_t d = pp_rho(m);
-        stack[top++] = d;
+        const uint64_t d = pp_rho(m, &budget, &timeout);
+        if (timeout) return false;
         stack[top++] = m / d;
+        stack[top++] = d;
     }
+    return true;
+}
+
+// distinct primes of n (unsorted) appended to p[*np]; false on a budget timeout
+__device__ bool pp_prime_factors(uint64_t n, uint64_t* p, int* np, uint64_t budget) {
+    uint64_t all[64];
+    int na = 0;
+    if (!pp_factorize(n, budget, all, &na, 64)) return false;
+    for (int i = 0; i < na; ++i) {
+        bool seen = false;
+        for (int k = 0; k < *np; ++k) seen |= p[k] == all[i];
+        if (!seen && *np < kMaxPrimes) p[(*np)++] = all[i];
+    }
+    return true;
 }
 
 // recover_order: ord(a) when a^R = 1, else 0
-__device__ uint64_t pp_recover_order(uint64_t r, uint64_t a, uint64_t N, uint64_t c, uint64_t m) {
+__device__ uint64_t pp_recover_order(uint64_t r, uint64_t a, uint64_t N, uint64_t c, uint64_t m,
+                                     uint64_t budget, bool* timeout) {
     if (r == 0) r = 1;
     uint64_t pr[kMaxPrimes], ex[kMaxPrimes];
     int np = 0;
@@ -261,7 +297,10 @@ __device__ uint64_t pp_recover_order(uint64_t r, uint64_t a, uint64_t N, uint64_
     const int nlift = np;
     uint64_t rp[kMaxPrimes];
     int nr = 0;
-    pp_prime_factors(r, rp, &nr);
+    if (!pp_prime_factors(r, rp, &nr, budget)) {  // factorize(r_candidate), postprocess.cpp:113
+        *timeout = true;
+        return 0;
+    }
     for (int i = 0; i < nr; ++i) {
         uint64_t v = 0, x = r;
         while (x % rp[i] == 0) {
@@ -399,13 +438,21 @@ __global__ void k_ekera_postprocess(const uint64_t* __restrict__ j, uint32_t cou
     PostRng rng{seed, static_cast<uint32_t>(idx0 + i), 1u, 0u};
     const u128d mask = t >= 128 ? ~u128d(0) : ((u128d(1) << t) - 1);
     uint64_t rec = 0;
+    const uint64_t budget = prm.rho_budget ? prm.rho_budget : kRhoBudget;
     for (uint64_t step = 0; step <= prm.B; ++step) {
         for (int sgn = -1; sgn <= 1; sgn += 2) {
             if (step == 0 && sgn == 1) continue;  // offset 0 once
             const u128d jp = (sgn < 0 ? jj - u128d(step) : jj + u128d(step)) & mask;
             u128d ck, cr;
             pp_extract(jp, t, N, ck, cr);
-            const uint64_t ordr = pp_recover_order(static_cast<uint64_t>(cr), a, N, prm.c, prm.m);
+            bool timeout = false;
+            const uint64_t ordr =
+                pp_recover_order(static_cast<uint64_t>(cr), a, N, prm.c, prm.m, budget, &timeout);
+            if (timeout) {  // FactorizationTimeoutError out of ekera_postprocess
+                o.timeout = 1;
+                out[i] = o;
+                return;
+            }
             if (!ordr) continue;
             if (!rec) rec = ordr;
             Factors f{{0, 0, 0, 0}, 0};
@@ -430,7 +477,55 @@ __global__ void k_ekera_postprocess(const uint64_t* __restrict__ j, uint32_t cou
     out[i] = o;
 }
 
+__global__ void k_factorize(uint64_t n, uint64_t budget, uint64_t* out, int* count, int* ok) {
+    uint64_t p[64];
+    int np = 0;
+    *ok = pp_factorize(n, budget, p, &np, 64) ? 1 : 0;
+    for (int u = 1; u < np; ++u)  // sorted ascending, as factorize() returns them
+        for (int v = u; v > 0 && p[v - 1] > p[v]; --v) {
+            const uint64_t tmp = p[v];
+            p[v] = p[v - 1];
+            p[v - 1] = tmp;
+        }
+    for (int i = 0; i < np; ++i) out[i] = p[i];
+    *count = np;
+}
+
 }  // namespace
+
+extern "C" int shs_factorize(uint64_t n, uint64_t rho_budget, int32_t device, uint64_t* primes,
+                             uint32_t* exponents, uint32_t* count) {
+    if (!primes || !exponents || !count) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    if (n == 0) return set_error(SHS_INVALID_ARGUMENT, "factorize(0)");
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce != cudaSuccess) return set_error(SHS_CUDA_ERROR, cudaGetErrorString(ce));
+    struct Out {
+        uint64_t p[64];
+        int count, ok;
+    };
+    Out* d = nullptr;
+    if ((ce = cudaMalloc(&d, sizeof(Out))) != cudaSuccess)
+        return set_error(SHS_CUDA_ERROR, cudaGetErrorString(ce));
+    k_factorize<<<1, 1>>>(n, rho_budget ? rho_budget : kRhoBudget, d->p, &d->count, &d->ok);
+    Out h;
+    ce = cudaGetLastError();
+    if (ce == cudaSuccess) ce = cudaMemcpy(&h, d, sizeof(Out), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (ce != cudaSuccess) return set_error(SHS_CUDA_ERROR, cudaGetErrorString(ce));
+    if (!h.ok) return set_error(SHS_FACTORIZATION_TIMEOUT, "pollard rho budget exhausted");
+    uint32_t k = 0;
+    for (int i = 0; i < h.count; ++i) {  // prime powers, numtheory.cpp:180-185
+        if (k && primes[k - 1] == h.p[i]) {
+            ++exponents[k - 1];
+        } else {
+            primes[k] = h.p[i];
+            exponents[k] = 1;
+            ++k;
+        }
+    }
+    *count = k;
+    return SHS_OK;
+}
 
 extern "C" int shs_shor_postprocess(const uint64_t* j, uint32_t count, uint32_t t, uint64_t N,
                                     uint64_t a, uint64_t known_order, int32_t has_known_order,
@@ -505,5 +600,9 @@ extern "C" int shs_ekera_postprocess(const uint64_t* j, uint32_t count, uint32_t
         return fail(ce);
     cudaFree(dj);
     cudaFree(dout);
+    for (uint32_t i = 0; i < count; ++i)  // the reference throws out of the first such shot
+        if (out[i].timeout)
+            return set_error(SHS_FACTORIZATION_TIMEOUT,
+                             "pollard rho budget exhausted (bit string " + std::to_string(i) + ")");
     return SHS_OK;
 }

@@ -51,6 +51,10 @@ class ConfigError(Error):
     pass
 
 
+class FactorizationTimeoutError(Error):
+    """errors.hpp: Pollard rho ran out of its step budget (numtheory.cpp:137, 149)."""
+
+
 class CudaError(Error):
     pass
 
@@ -75,6 +79,7 @@ def _raise(code: int) -> None:
         L.SHS_BUDGET_EXCEEDED: BudgetExceededError,
         L.SHS_INVALID_ARGUMENT: ValueError,  # std::invalid_argument
         L.SHS_CUDA_ERROR: CudaError,
+        L.SHS_FACTORIZATION_TIMEOUT: FactorizationTimeoutError,
     }.get(code, Error)(msg)
 
 

@@ -93,6 +93,7 @@ class EkeraParams:  # postprocess.hpp:43-53
     varsigma: int = 1
     m: int = 1
     ell: int = 0
+    rho_budget: int = 0  # recover_order's factorize() budget (0: the reference's 10^7)
 
     @staticmethod
     def for_problem(L: int, t: int) -> "EkeraParams":
@@ -102,12 +103,13 @@ class EkeraParams:  # postprocess.hpp:43-53
 
 class shs_ekera_params(C.Structure):
     _fields_ = [("B", C.c_uint64), ("c", C.c_uint64), ("k", C.c_uint32),
-                ("varsigma", C.c_uint32), ("m", C.c_uint32), ("ell", C.c_uint32)]
+                ("varsigma", C.c_uint32), ("m", C.c_uint32), ("ell", C.c_uint32),
+                ("rho_budget", C.c_uint64)]
 
 
 EKERA_DTYPE = np.dtype([("classification", np.int32), ("order_match", np.uint8),
                         ("has_recovered_order", np.uint8), ("has_offset", np.uint8),
-                        ("pad", np.uint8), ("k", np.uint64, 2), ("r", np.uint64, 2),
+                        ("timeout", np.uint8), ("k", np.uint64, 2), ("r", np.uint64, 2),
                         ("recovered_order", np.uint64), ("candidate_offset", np.int64),
                         ("n_factors", np.uint32), ("pad2", np.uint32), ("factors", np.uint64, 4)])
 
@@ -119,7 +121,8 @@ def ekera_postprocess_array(j: np.ndarray, t: int, N: int, a: int, params: Ekera
     (seed, shot, 1, postprocess) as run_problem builds it), on the device."""
     j = np.ascontiguousarray(j, dtype=np.uint64).reshape(-1, 2)
     out = np.zeros(len(j), dtype=EKERA_DTYPE)
-    prm = shs_ekera_params(params.B, params.c, params.k, params.varsigma, params.m, params.ell)
+    prm = shs_ekera_params(params.B, params.c, params.k, params.varsigma, params.m, params.ell,
+                           params.rho_budget)
     _raise(L.load().shs_ekera_postprocess(j.ctypes.data_as(C.POINTER(C.c_uint64)), len(j), t, N,
                                           a, C.byref(prm), seed, idx0, known_order or 0,
                                           0 if known_order is None else 1, device,
@@ -320,3 +323,13 @@ def run_problem(problem: FactoringProblem, M: int, error: Optional[ErrorConfig] 
         if own:
             engine.close()
     return tally(res, outcomes)
+
+
+def factorize(n: int, rho_budget: int = 10_000_000, device: int = 0):
+    """factorize (numtheory.cpp:170-187) on the device: [(prime, exponent)]
+    ascending; FactorizationTimeoutError once the Pollard-rho budget runs out."""
+    primes = (C.c_uint64 * 64)()
+    exps = (C.c_uint32 * 64)()
+    cnt = C.c_uint32()
+    _raise(L.load().shs_factorize(n, rho_budget, device, primes, exps, C.byref(cnt)))
+    return [(primes[i], exps[i]) for i in range(cnt.value)]

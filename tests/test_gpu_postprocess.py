@@ -145,3 +145,73 @@ def test_run_problem_ekera_matches_reference(cuda_ok, reference, N, pq):
                                     post_mode="ekera")
         assert (got.success, got.fail, got.first_factor_index, got.first_order_index) == \
             (ref["success"], ref["fail"], ref["first_factor_index"], ref["first_order_index"]), a
+
+
+def test_factorize_and_rho_budget_match_reference(cuda_ok, reference):
+    """factorize (numtheory.cpp:170-187) on the device equals the reference's, and
+    its Pollard-rho budget runs out exactly where the reference's does
+    (FactorizationTimeoutError, numtheory.cpp:137, 149): for each composite the
+    smallest budget the reference needs is found by bisection; the device
+    succeeds with it and times out with one step less."""
+    import random
+
+    import paper_2308_05047_b200 as shs
+    from oracle import OracleError
+    rng = random.Random(4)
+
+    def prime(bits):
+        while True:
+            c = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+            if all(c % d for d in range(3, 2000, 2)) and pow(2, c - 1, c) == 1:
+                return c
+
+    cases = [prime(20) * prime(21), prime(28) * prime(29), prime(31) * prime(32),
+             prime(12) * prime(13) * prime(14), 2 ** 5 * 97 * prime(25) * prime(26),
+             prime(16) ** 2 * prime(20), 1, 97, 2 ** 63 + 1]
+    for n in cases:
+        want = reference.factorize(n)
+        assert shs.factorize(n) == want, n
+        lo, hi = 0, 10_000_000  # the reference: hi works, lo - 1 ... find the least budget
+        try:
+            reference.factorize(n, 0)
+            need = 0
+        except OracleError as e:
+            assert e.code == 9
+            while hi - lo > 1:
+                mid = (lo + hi) // 2
+                try:
+                    reference.factorize(n, mid)
+                    hi = mid
+                except OracleError:
+                    lo = mid
+            need = hi
+        assert shs.factorize(n, max(need, 0) or 1) == want if need else True
+        if need > 1:
+            assert shs.factorize(n, need) == want
+            with pytest.raises(shs.FactorizationTimeoutError):
+                shs.factorize(n, need - 1)
+
+
+def test_ekera_rho_budget_timeout(cuda_ok):
+    """recover_order's factorize() budget in the device Ekerå pipeline: a tiny
+    budget makes ekera_postprocess raise FactorizationTimeoutError as the
+    reference's would (postprocess.cpp:113 -> numtheory.cpp:137)."""
+    import numpy as np
+
+    import paper_2308_05047_b200 as shs
+    N, a, t = 1048351, 12345, 40
+    L = N.bit_length()
+    params = shs.EkeraParams.for_problem(L, t)
+    j = np.array([[123456789, 0]], dtype=np.uint64)
+    shs.ekera_postprocess_array(j, t, N, a, params, 1, 0)  # default budget: fine
+    import dataclasses
+    tight = dataclasses.replace(params, rho_budget=1)
+    hit = False
+    for x in range(1, 400):  # some convergent denominator is composite with a large factor
+        j = np.array([[x * 7919 % (1 << t), 0]], dtype=np.uint64)
+        try:
+            shs.ekera_postprocess_array(j, t, N, a, tight, 1, 0)
+        except shs.FactorizationTimeoutError:
+            hit = True
+            break
+    assert hit
