@@ -1319,8 +1319,12 @@ int shs_shard_create(const shs_problem* problem, const shs_error* error,
         auto it = std::find_if(cache.begin(), cache.end(),
                                [&](const auto& kv) { return kv.first == sh->a_pows[s]; });
         if (it == cache.end()) {
+            // shards keep no per-row head scratch (the single engine's reason for
+            // the 2^18-row cap): rows of ~8192 at every size, so the exchanges
+            // have as many bands (warps / tiles) as the state has rows
             cache.emplace_back(sh->a_pows[s],
-                               make_tile_plan(sh->a_pows[s], sh->a_invs[s], sh->N, o.tiling));
+                               make_tile_plan(sh->a_pows[s], sh->a_invs[s], sh->N, o.tiling, 0,
+                                              uint64_t(1) << 22));
             it = cache.end() - 1;
         }
         sh->plans[s] = it->second;

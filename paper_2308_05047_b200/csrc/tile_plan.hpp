@@ -124,7 +124,8 @@ inline TilePlanHost make_small_a_plan(uint64_t A, uint64_t m, uint64_t N, uint64
 }
 
 inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tiling,
-                                   uint64_t small_a_scratch = 0) {
+                                   uint64_t small_a_scratch = 0,
+                                   uint64_t max_rows = kTileMaxRows) {
     TilePlanHost pl;
     if (tiling == SHS_TILING_OFF || A == 1) return pl;
     if (tiling == SHS_TILING_AUTO && N < kTileAutoMinN) return pl;
@@ -132,7 +133,7 @@ inline TilePlanHost make_tile_plan(uint64_t A, uint64_t m, uint64_t N, int tilin
         pl = make_small_a_plan(A, m, N, small_a_scratch);
         if (pl.tiled) return pl;
     }
-    const uint64_t hmax = std::min<uint64_t>(N / kTileAvgRow, kTileMaxRows);
+    const uint64_t hmax = std::min<uint64_t>(N / kTileAvgRow, max_rows);
     std::vector<uint64_t> cands;
     for (uint64_t h = 2; h <= hmax; h *= 2) {
         cands.push_back(h);
