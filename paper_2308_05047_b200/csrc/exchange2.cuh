@@ -173,56 +173,98 @@ __device__ __forceinline__ void x2_pack_band(const X2Params& p, uint64_t b, bool
 }
 
 // Unpack side of band b: this shard's rows of the band, compacted onto the
-// lanes (lane L: row my[L % m], column offset L / m), so a warp step covers
-// floor(32 / m) columns in canonical order (column, then row); kX2Batch steps
-// per `take(n, mine[], q[], grp[], z[])` call.
-template <typename Take>
-__device__ __forceinline__ void x2_unpack_band(const X2Params& p, uint64_t b, Take&& take) {
+// lanes (lane L: row my[L % m], column offset L / m), so a warp step covers cpi
+// columns (the largest power of two with cpi * m <= 32, so steps tile 32-column
+// chunks) in canonical order (column, then row).
+struct X2Lanes {
+    unsigned rows;           // ballot of the band's rows with elements of this shard
+    int m, cpi, ri, coff, k; // k: this lane's row (the ri-th set bit of rows)
+    bool on;                 // lane < cpi * m
+    uint64_t z, len, cut;    // row k
+    int own;
+};
+
+// Walks the band in 32-column chunks. A chunk is "regular" when every one of its
+// columns is inside every row of this shard (no band tail, no cut) and each
+// column's source elements of those rows come from one sender q (no shard
+// boundary or wrap inside the column's run): then the column holds m
+// consecutive slots of q's stream and `fast(i0, q, L)` (lane c: column i0 + c)
+// serves the chunk. Otherwise the chunk goes step by step through
+// `take(n, mine[], q[], grp[], z[])`, kX2SlowBatch steps per call.
+constexpr int kX2SlowBatch = 1;  // steps per take() call (irregular chunks only)
+
+template <typename Fast, typename Take>
+__device__ __forceinline__ void x2_unpack_band(const X2Params& p, uint64_t b, Fast&& fast,
+                                               Take&& take) {
     const int lane = threadIdx.x & 31;
     const uint64_t j0 = b * kRows;
     const X2Row row = x2_row(p, j0 + lane);
     const bool has = row.len && (row.own == p.me || (row.cut != ~0ull && row.own + 1 == p.me));
-    const unsigned rows = __ballot_sync(0xffffffffu, has);
-    if (!rows) return;
-    const int m = __popc(rows);
-    const int cpi = 32 / m;  // columns per warp step
-    // lane L serves row k = the (L % m)-th set bit of rows
-    int k = 0;
+    X2Lanes L;
+    L.rows = __ballot_sync(0xffffffffu, has);
+    if (!L.rows) return;
+    L.m = __popc(L.rows);
+    L.cpi = 1;
+    while (L.cpi * 2 * L.m <= 32) L.cpi *= 2;
+    L.ri = lane % L.m;
+    L.coff = lane / L.m;
+    L.on = lane < L.cpi * L.m;
     {
-        unsigned rr = rows;
-        for (int t = 0; t < lane % m; ++t) rr &= rr - 1;
-        k = __ffs(rr) - 1;
+        unsigned rr = L.rows;
+        for (int t = 0; t < L.ri; ++t) rr &= rr - 1;
+        L.k = __ffs(rr) - 1;
     }
-    const int coff = lane / m;
-    const bool lane_on = lane < cpi * m;
-    const uint64_t z = __shfl_sync(0xffffffffu, row.z, k);
-    const uint64_t len = __shfl_sync(0xffffffffu, row.len, k);
-    const uint64_t cut = __shfl_sync(0xffffffffu, row.cut, k);
-    const int own = __shfl_sync(0xffffffffu, row.own, k);
+    L.z = __shfl_sync(0xffffffffu, row.z, L.k);
+    L.len = __shfl_sync(0xffffffffu, row.len, L.k);
+    L.cut = __shfl_sync(0xffffffffu, row.cut, L.k);
+    L.own = __shfl_sync(0xffffffffu, row.own, L.k);
     const uint64_t maxlen = warp_max(has ? row.len : 0);
-    // source run start of this lane's column, advanced by cpi columns per step
-    const uint64_t step = p.mstep[cpi];
-    uint64_t cs = addmod(j0, p.mstep[coff], p.N);
-    bool mine[kX2Batch];
-    int qq[kX2Batch];
-    unsigned grp[kX2Batch];
-    uint64_t zz[kX2Batch];
-    for (uint64_t i0 = 0; i0 < maxlen; i0 += uint64_t(cpi) * kX2Batch) {
-        int n = 0;
+    // columns [rlo, rhi) are this shard's in every one of its rows
+    uint64_t rlo = !has ? 0 : row.own == p.me ? 0 : row.cut;
+    uint64_t rhi = !has ? ~0ull : row.own == p.me ? (row.cut < row.len ? row.cut : row.len) : row.len;
 #pragma unroll
-        for (int t = 0; t < kX2Batch; ++t) {
-            const uint64_t i = i0 + uint64_t(t) * cpi + coff;
-            const bool mn = lane_on && i < len && own + (i >= cut ? 1 : 0) == p.me;
-            uint64_t s = cs + k;
-            if (s >= p.N) s -= p.N;
-            qq[t] = mn ? x2_owner(s, p.S, p.S_inv) : -1;
-            mine[t] = mn;
-            grp[t] = __match_any_sync(0xffffffffu, qq[t]);
-            zz[t] = z + i;
-            cs = addmod(cs, step, p.N);
-            if (i0 + uint64_t(t) * cpi < maxlen) n = t + 1;
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, rlo, o);
+        const uint64_t c = __shfl_xor_sync(0xffffffffu, rhi, o);
+        rlo = a > rlo ? a : rlo;
+        rhi = c < rhi ? c : rhi;
+    }
+    const int kmin = __ffs(L.rows) - 1, kmax = 31 - __clz(L.rows);
+    uint64_t cc = addmod(j0, p.mstep[lane], p.N);  // lane c: source run start of column i0 + c
+    const uint64_t m32 = p.mstep[32];
+    const int steps = kCols / L.cpi;
+    bool mine[kX2SlowBatch];
+    int qq[kX2SlowBatch];
+    unsigned grp[kX2SlowBatch];
+    uint64_t zz[kX2SlowBatch];
+    for (uint64_t i0 = 0; i0 < maxlen; i0 += kCols) {
+        const uint64_t i = i0 + lane;
+        const int q = x2_owner(cc + kmin, p.S, p.S_inv);
+        const bool reg = i >= rlo && i < rhi && cc + kmax < p.N &&
+                         x2_owner(cc + kmax, p.S, p.S_inv) == q;
+        if (__all_sync(0xffffffffu, reg)) {
+            fast(i0, q, L);
+        } else {
+            for (int t0 = 0; t0 < steps; t0 += kX2SlowBatch) {
+                int n = 0;
+#pragma unroll
+                for (int t = 0; t < kX2SlowBatch; ++t) {
+                    const int c = (t0 + t) * L.cpi + L.coff;
+                    const uint64_t ic = i0 + c;
+                    uint64_t s = __shfl_sync(0xffffffffu, cc, c & 31) + L.k;
+                    if (s >= p.N) s -= p.N;
+                    const bool mn = t0 + t < steps && L.on && ic < L.len &&
+                                    L.own + (ic >= L.cut ? 1 : 0) == p.me;
+                    qq[t] = mn ? x2_owner(s, p.S, p.S_inv) : -1;
+                    mine[t] = mn;
+                    grp[t] = __match_any_sync(0xffffffffu, qq[t]);
+                    zz[t] = L.z + ic;
+                    if (t0 + t < steps && i0 + uint64_t(t0 + t) * L.cpi < maxlen) n = t + 1;
+                }
+                if (n) take(n, mine, qq, grp, zz);
+            }
         }
-        take(n, mine, qq, grp, zz);
+        cc = addmod(cc, m32, p.N);
     }
 }
 
@@ -251,8 +293,16 @@ __global__ void __launch_bounds__(kX2Threads) k_x2_count(X2Params p,
                 add(n, live, r, grp);
             });
         else
-            x2_unpack_band(p, b, [&](int n, const bool* mine, const int* q, const unsigned* grp,
-                                     const uint64_t*) { add(n, mine, q, grp); });
+            x2_unpack_band(
+                p, b,
+                [&](uint64_t, int q, const X2Lanes& L) {  // m elements per column from q
+                    const unsigned g = __match_any_sync(0xffffffffu, q);
+                    if ((g & ((1u << lane) - 1)) == 0) atomicAdd(&cnt[warp][q], L.m * __popc(g));
+                    __syncwarp();
+                },
+                [&](int n, const bool* mine, const int* q, const unsigned* grp, const uint64_t*) {
+                    add(n, mine, q, grp);
+                });
         __syncwarp();
         if (lane < p.G) counts[uint64_t(lane) * (nb + 1) + b] = cnt[warp][lane];
         __syncwarp();
@@ -385,7 +435,10 @@ __global__ void __launch_bounds__(kX2Threads) k_x2_pack(X2Params p) {
 }
 
 // unpack: this shard's destination elements of the round's bands from the
-// senders' streams into P (a row's columns of one warp step are contiguous)
+// senders' streams into P (a row's columns of one warp step are contiguous). In
+// a regular chunk each column's m elements are consecutive in one stream: the
+// column's stream pointer is ranked once per chunk, and a step is a shuffle, a
+// load and a store per lane.
 __global__ void __launch_bounds__(kX2Threads) k_x2_unpack(X2Params p) {
     __shared__ unsigned long long pos[kX2Warps][kMaxShards];  // next slot per sender
     __shared__ const double2* srcp[kMaxShards];
@@ -394,6 +447,7 @@ __global__ void __launch_bounds__(kX2Threads) k_x2_unpack(X2Params p) {
     __syncthreads();
     const uint64_t nb = p.tp.ntiles;
     const uint64_t lo = uint64_t(p.me) * p.S;
+    const unsigned lt = (1u << lane) - 1;
     for (uint64_t b = p.b0 + uint64_t(blockIdx.x) * kX2Warps + warp; b < p.b1;
          b += uint64_t(gridDim.x) * kX2Warps) {
         if (lane < p.G) {
@@ -401,26 +455,52 @@ __global__ void __launch_bounds__(kX2Threads) k_x2_unpack(X2Params p) {
             pos[warp][lane] = o[b] - o[p.b0];
         }
         __syncwarp();
-        x2_unpack_band(p, b, [&](int n, const bool* mine, const int* q, const unsigned* grp,
-                                 const uint64_t* z) {
-            unsigned long long at[kX2Batch];
-#pragma unroll
-            for (int t = 0; t < kX2Batch; ++t) {  // stream positions first (counters only) ...
-                if (t < n && mine[t]) {
-                    const unsigned below = grp[t] & ((1u << lane) - 1);
-                    at[t] = pos[warp][q[t]] + __popc(below);
-                    if (!below) pos[warp][q[t]] += __popc(grp[t]);
-                }
+        x2_unpack_band(
+            p, b,
+            [&](uint64_t i0, int q, const X2Lanes& L) {
+                const unsigned g = __match_any_sync(0xffffffffu, q);
+                const unsigned below = g & lt;
+                // lane c: the stream slot of column i0 + c's first element
+                const unsigned long long col = reinterpret_cast<unsigned long long>(
+                    srcp[q] + pos[warp][q] + uint64_t(L.m) * __popc(below));
                 __syncwarp();
-            }
-            double2 v[kX2Batch];
+                if (!below) pos[warp][q] += uint64_t(L.m) * __popc(g);
+                __syncwarp();
+                double2* out = p.P + (L.z + i0 + L.coff - lo);
+                const int steps = kCols / L.cpi;
+                for (int t0 = 0; t0 < steps; t0 += kX2Batch) {
+                    double2 v[kX2Batch];
 #pragma unroll
-            for (int t = 0; t < kX2Batch; ++t)  // ... then every load of the batch in flight
-                if (t < n && mine[t]) v[t] = srcp[q[t]][at[t]];
+                    for (int t = 0; t < kX2Batch; ++t) {
+                        const unsigned long long c = __shfl_sync(
+                            0xffffffffu, col, ((t0 + t) * L.cpi + L.coff) & 31);
+                        if (L.on && t0 + t < steps)
+                            v[t] = reinterpret_cast<const double2*>(c)[L.ri];
+                    }
 #pragma unroll
-            for (int t = 0; t < kX2Batch; ++t)
-                if (t < n && mine[t]) p.P[z[t] - lo] = v[t];
-        });
+                    for (int t = 0; t < kX2Batch; ++t)
+                        if (L.on && t0 + t < steps) out[(t0 + t) * L.cpi] = v[t];
+                }
+            },
+            [&](int n, const bool* mine, const int* q, const unsigned* grp, const uint64_t* z) {
+                unsigned long long at[kX2SlowBatch];
+#pragma unroll
+                for (int t = 0; t < kX2SlowBatch; ++t) {  // stream positions first (counters only) ...
+                    if (t < n && mine[t]) {
+                        const unsigned below = grp[t] & lt;
+                        at[t] = pos[warp][q[t]] + __popc(below);
+                        if (!below) pos[warp][q[t]] += __popc(grp[t]);
+                    }
+                    __syncwarp();
+                }
+                double2 v[kX2SlowBatch];
+#pragma unroll
+                for (int t = 0; t < kX2SlowBatch; ++t)  // ... then every load of the batch in flight
+                    if (t < n && mine[t]) v[t] = srcp[q[t]][at[t]];
+#pragma unroll
+                for (int t = 0; t < kX2SlowBatch; ++t)
+                    if (t < n && mine[t]) p.P[z[t] - lo] = v[t];
+            });
         __syncwarp();
     }
 }
