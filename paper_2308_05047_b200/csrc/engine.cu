@@ -143,6 +143,19 @@ struct shs_engine {
     // shard group driven by this engine (shard.cu); every run / step call below
     // is forwarded to it
     ShardGroup* group = nullptr;
+    // orbit-compressed stages (orbit.cuh): the state holds only the r members of
+    // <a>, in z order. Stages with orb_use[s] run k_tiled<true, false, true>
+    // (both groups written, no collapse pass); each N-amplitude buffer holds a
+    // pair of compressed slots (stride orb_pad), the current pair in X
+    bool orb_want = true;          // SHS_ORBIT=0 / shs_engine_set_orbit(0): dense only
+    bool orb_ready = false;        // rank records built
+    uint64_t orb_r = 0, orb_pad = 0;
+    std::vector<uint8_t> orb_use;  // per stage
+    ulonglong2* orb_rec = nullptr; // [ceil(N / 64) + 2]
+    bool rep_orb = false;          // the current state is compressed (pair in X)
+    int orb_sel = 0;               // its slot when the host knows it ...
+    const DevStage* orb_prev = nullptr;  // ... else the device slot whose sel picks it
+    int64_t orb_stage = -1;        // the stage whose probs pass ran compressed (pending collapse)
 };
 
 namespace {
@@ -446,6 +459,7 @@ void release(shs_engine* e) {
     cudaFree(e->d_out);
     if (e->h_out) cudaFreeHost(e->h_out);
     cudaFree(e->d_slots);
+    cudaFree(e->orb_rec);
     if (e->h_rec) cudaFreeHost(e->h_rec);
     for (auto ev : e->meas_ev)
         if (ev) cudaEventDestroy(ev);
@@ -499,6 +513,7 @@ int carve_sparse(shs_engine* e) {
 // All-or-nothing: a failed allocation frees what this call allocated, so a
 // retry starts clean (and no kernel ever runs with a half-allocated engine).
 int ensure_buffers_once(shs_engine* e);
+int orb_build(shs_engine* e);
 int ensure_buffers(shs_engine* e) {
     if (e->X) return SHS_OK;
     const uint64_t bytes0 = e->device_bytes;
@@ -540,10 +555,119 @@ int ensure_buffers_once(shs_engine* e) {
                             cudaMemcpyHostToDevice));
         e->device_bytes += sizeof(uint32_t) * tab.size();
     }
+    if (e->orb_want && e->orb_r) return orb_build(e);
+    return SHS_OK;
+}
+
+// Rank records of the orbit <a> (orbit.cuh), built once per engine with Y as
+// scratch (called only while Y holds no state): membership bits by
+// enumerating a^x for x < r (r from a baby-step giant-step order search at
+// create), word popcounts, an exclusive scan, the records.
+int orb_build(shs_engine* e) {
+    if (e->orb_ready || !e->orb_r || !e->Y) return SHS_OK;
+    const uint64_t N = e->N, r = e->orb_r, nw = (N + 63) / 64;
+    const uint64_t a = e->prob.a % N;
+    char* scratch = reinterpret_cast<char*>(e->Y);
+    auto* bits = reinterpret_cast<unsigned int*>(scratch);
+    scratch += ((8 * nw + 255) / 256) * 256;
+    auto* counts = reinterpret_cast<unsigned long long*>(scratch);
+    scratch += ((8 * nw + 255) / 256) * 256;
+    auto* bases = reinterpret_cast<unsigned long long*>(scratch);
+    scratch += ((8 * nw + 255) / 256) * 256;
+    const uint64_t T = std::min<uint64_t>(r, uint64_t(e->num_sms) * 2048);
+    const uint64_t B = (r + T - 1) / T;
+    auto* starts = reinterpret_cast<uint64_t*>(scratch);
+    scratch += ((8 * T + 255) / 256) * 256;
+    size_t temp_bytes = 0;
+    SHS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, counts, bases, static_cast<int64_t>(nw),
+                                           e->stream));
+    if (static_cast<uint64_t>(scratch - reinterpret_cast<char*>(e->Y)) + temp_bytes > sizeof(double2) * N)
+        return set_error(SHS_CUDA_ERROR, "orbit index scratch exceeds the state buffer");
+    std::vector<uint64_t> h(T);
+    {
+        uint64_t step = 1, base = a, ex = B;  // a^B
+        while (ex) {
+            if (ex & 1) step = mulmod(step, base, N);
+            base = mulmod(base, base, N);
+            ex >>= 1;
+        }
+        uint64_t v = 1;
+        for (uint64_t k = 0; k < T; ++k) {
+            h[k] = v;
+            v = mulmod(v, step, N);
+        }
+    }
+    if (!e->orb_rec) {
+        SHS_CUDA(cudaMalloc(&e->orb_rec, sizeof(ulonglong2) * (nw + 2)));
+        e->device_bytes += sizeof(ulonglong2) * (nw + 2);
+    }
+    SHS_CUDA(cudaMemcpyAsync(starts, h.data(), 8 * T, cudaMemcpyHostToDevice, e->stream));
+    SHS_CUDA(cudaMemsetAsync(bits, 0, 8 * nw, e->stream));
+    const int grid = static_cast<int>(std::min<uint64_t>((nw + 255) / 256, uint64_t(e->num_sms) * 16));
+    int rc = launch(e, -1, [&] {
+        k_orb_mark<<<static_cast<int>((T + 255) / 256), 256, 0, e->stream>>>(starts, T, B, r, a,
+                                                                            shoup(a, N), N, bits);
+        k_orb_counts<<<grid, 256, 0, e->stream>>>(bits, nw, counts);
+        size_t tb = temp_bytes;
+        cub::DeviceScan::ExclusiveSum(scratch, tb, counts, bases, static_cast<int64_t>(nw), e->stream);
+        k_orb_records<<<grid, 256, 0, e->stream>>>(bits, bases, nw, r, e->orb_rec);
+    });
+    if (rc) return rc;
+    unsigned long long last[2] = {0, 0};
+    SHS_CUDA(cudaMemcpyAsync(&last[0], bases + nw - 1, 8, cudaMemcpyDeviceToHost, e->stream));
+    SHS_CUDA(cudaMemcpyAsync(&last[1], counts + nw - 1, 8, cudaMemcpyDeviceToHost, e->stream));
+    if ((rc = sync(e))) return rc;
+    if (last[0] + last[1] != r)
+        return set_error(SHS_ERROR, "orbit index: " + std::to_string(last[0] + last[1]) +
+                                        " members marked, order " + std::to_string(r));
+    e->orb_ready = true;
+    return SHS_OK;
+}
+
+bool orb_stage_on(const shs_engine* e, uint32_t s) {
+    return e->orb_want && e->orb_ready && e->orb_use[s] && !e->e1;
+}
+
+int orb_grid(const shs_engine* e) { return e->num_sms * 8; }
+
+// dense X -> compressed slot 0 of Y's pair, then swap: the pair is in X
+int orb_enter(shs_engine* e) {
+    int rc = launch(e, -1, [&] {
+        k_orb_compress<<<orb_grid(e), kOrbThreads, 0, e->stream>>>(e->X, e->orb_rec, e->N, e->Y);
+    });
+    if (rc) return rc;
+    std::swap(e->X, e->Y);
+    e->rep_orb = true;
+    e->orb_sel = 0;
+    e->orb_prev = nullptr;
+    return SHS_OK;
+}
+
+OrbSrc orb_src(const shs_engine* e) {
+    return OrbSrc{e->X, e->X + e->orb_pad, e->orb_prev, e->orb_sel};
+}
+
+// compressed pair in X -> dense Y, then swap: the dense state is in X
+int orb_leave(shs_engine* e) {
+    int rc = launch(e, -1, [&] {
+        k_orb_expand<<<orb_grid(e), kOrbThreads, 0, e->stream>>>(orb_src(e), e->orb_rec, e->N, e->Y);
+    });
+    if (rc) return rc;
+    std::swap(e->X, e->Y);
+    e->rep_orb = false;
+    e->orb_prev = nullptr;
     return SHS_OK;
 }
 
 int state_init(shs_engine* e) {
+    e->rep_orb = false;
+    e->orb_prev = nullptr;
+    e->orb_sel = 0;
+    e->orb_stage = -1;
+    if (e->orb_want && !e->orb_ready && e->orb_r && e->X) {
+        int rc = orb_build(e);
+        if (rc) return rc;
+    }
     e->spec_stage = -1;
     e->e1 = true;  // sel = e_1 implicitly: no memset of the N-amplitude buffer
     e->inv = 1.0;
@@ -580,6 +704,37 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
     const bool gather = e->a_pows[s] != 1;
     int rc;
     *nparts = grid_for(e);
+    e->orb_stage = -1;
+    const bool orb = orb_stage_on(e, s);
+    if (orb && !e->rep_orb && (rc = orb_enter(e))) return rc;
+    if (!orb && e->rep_orb && (rc = orb_leave(e))) return rc;
+    if (orb) {
+        // compressed: h0 and h1 of every member into Y's pair (no collapse pass)
+        TileParams tp = tile_params_for(e, s);
+        tp.dev = dev;
+        tp.spec = 0;
+        tp.X1 = e->X + e->orb_pad;
+        tp.prev = e->orb_prev;
+        tp.prev_sel = e->orb_sel;
+        tp.Y1 = e->Y + e->orb_pad;
+        tp.orb = e->orb_rec;
+        tp.write = s + 1 < e->t ? 1 : 0;
+        const TilePlanHost& pl = e->plans[s];
+        const int g1 = static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
+        const int g2 = static_cast<int>(
+            std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
+        rc = launch(e, 0, [&] {
+            k_tiled<true, false, true><<<g1, tile_threads<true, false, true>(), tile_smem_bytes<true, true>(),
+                                         e->stream>>>(tp);
+            e->band_issued += pl.ntiles;
+            k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
+        });
+        e->launches++;
+        *nparts = g1 + g2;
+        e->spec_stage = -1;
+        e->orb_stage = s;
+        return rc;
+    }
     if (e->plans[s].tiled && !e->e1) {
         TileParams tp = tile_params_for(e, s);
         tp.dev = dev;
@@ -627,6 +782,15 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
 int launch_collapse_pass(shs_engine* e, uint32_t s, int src_group, const DevStage* dev) {
     const bool gather = e->a_pows[s] != 1;
     int rc;
+    if (e->orb_stage == static_cast<int64_t>(s)) {
+        // the compressed probs pass wrote both groups into Y's pair: keep one
+        e->orb_stage = -1;
+        std::swap(e->X, e->Y);
+        e->orb_prev = dev;
+        e->orb_sel = dev ? 0 : src_group;
+        e->e1 = false;
+        return SHS_OK;
+    }
     if (e->plans[s].tiled && !e->e1) {
         TileParams tp = tile_params_for(e, s);
         tp.sel = src_group;
@@ -779,9 +943,22 @@ int launch_sparse_collapse(shs_engine* e, uint32_t s, const DevStage* dev) {
     });
 }
 
-// the dense sel (X) from the support entering stage s
+// the dense sel (X) from the support entering stage s (compressed when stage s
+// runs compressed)
 int materialize_sparse(shs_engine* e, uint32_t s) {
     const uint64_t K = uint64_t(1) << s;
+    if (e->orb_want && e->orb_ready && e->orb_use[s]) {
+        SHS_CUDA(cudaMemsetAsync(e->X, 0, sizeof(double2) * e->orb_r, e->stream));
+        int rc = launch(e, -1, [&] {
+            k_orb_scatter<<<sparse_grid(e, K), kSparseThreads, 0, e->stream>>>(
+                e->sZ[s & 1], e->sV[s & 1], K, e->orb_rec, e->X);
+        });
+        e->e1 = false;
+        e->rep_orb = true;
+        e->orb_sel = 0;
+        e->orb_prev = nullptr;
+        return rc;
+    }
     SHS_CUDA(cudaMemsetAsync(e->X, 0, sizeof(double2) * e->N, e->stream));
     int rc = launch(e, -1, [&] {
         k_sparse_scatter<<<sparse_grid(e, K), kSparseThreads, 0, e->stream>>>(e->sZ[s & 1],
@@ -1287,6 +1464,42 @@ const char* shs_build_info(void) {
     return "shorsim_b200: sm_100a, fp64 no-FMA (--fmad=false), nvcc " SHS_NVCC_VERSION;
 }
 
+// Which stages run compressed (orbit.cuh): maximal runs of >= 2 consecutive
+// stages with whole-band tile plans (k_tiled<., false>), on a single-device
+// engine from kOrbitMinN, when the orbit fills at most half of Z_N (2 slots per
+// buffer). The order r comes from a baby-step giant-step search (sparse_plan.hpp).
+namespace {
+void plan_orbit(shs_engine* e) {
+    e->orb_use.assign(e->t, 0);
+    e->orb_r = 0;
+    const char* env = std::getenv("SHS_ORBIT");  // default off until it beats the dense stages
+    e->orb_want = env && env[0] == '1';
+    if (e->group || e->N < kOrbitMinN) return;
+    std::vector<uint8_t> cap(e->t, 0);
+    for (uint32_t s = 1; s < e->t; ++s)
+        cap[s] = e->a_pows[s] != 1 && e->plans[s].tiled && !e->plans[s].split_tail;
+    bool any = false;
+    for (uint32_t s = 1; s < e->t;) {
+        uint32_t s1 = s;
+        while (s1 < e->t && cap[s1]) ++s1;
+        if (s1 - s >= 2) {
+            for (uint32_t k = s; k < s1; ++k) e->orb_use[k] = 1;
+            any = true;
+        }
+        s = s1 + 1;
+    }
+    if (!any) return;
+    const uint64_t r = small_order(e->prob.a % e->N, e->N, e->N);
+    const uint64_t pad = (r + 63) / 64 * 64;
+    if (r == 0 || 2 * pad > e->N) {
+        e->orb_use.assign(e->t, 0);
+        return;
+    }
+    e->orb_r = r;
+    e->orb_pad = pad;
+}
+}  // namespace
+
 int shs_engine_create(const shs_problem* problem, const shs_error* error,
                       const shs_options* options, shs_engine** out) {
     if (!problem || !error || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
@@ -1392,6 +1605,9 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
                                   static_cast<int>(tile_smem_bytes<true>()));
         if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<probs>)");
     }
+    ce = cudaFuncSetAttribute(k_tiled<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(tile_smem_bytes<true, true>()));
+    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<orbit>)");
     for (auto fn : {k_tiled<false, false>, k_tiled<false, true>}) {
         ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tile_smem_bytes<false>()));
@@ -1452,11 +1668,33 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
             e->sparse_n = 0;  // the group runs every stage dense
         }
     }
+    plan_orbit(e);
     *out = e;
     return SHS_OK;
 }
 
 void shs_engine_destroy(shs_engine* e) { release(e); }
+
+int shs_engine_set_orbit(shs_engine* e, int32_t enable) {
+    if (!e) return set_error(SHS_INVALID_ARGUMENT, "null engine");
+    if (e->rep_orb || e->pending) state_init(e);  // takes effect from a fresh state
+    e->orb_want = enable != 0;
+    return SHS_OK;
+}
+
+int shs_engine_orbit_info(const shs_engine* e, uint64_t out[3]) {
+    if (!e || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    out[0] = e->orb_want ? e->orb_r : 0;
+    out[1] = 0;
+    out[2] = 0;
+    if (!out[0]) return SHS_OK;
+    for (uint32_t s = e->t; s-- > 0;)
+        if (e->orb_use[s]) {
+            out[1] += 1;
+            out[2] = s;
+        }
+    return SHS_OK;
+}
 
 uint32_t shs_engine_stages(const shs_engine* e) { return e ? e->t : 0; }
 
@@ -1586,7 +1824,11 @@ int shs_stage_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
         StageParams p = params_for(e, e->ps);
         const bool gather = e->a_pows[e->ps] != 1;
         const int grid = static_cast<int>(std::min<uint64_t>((count + 255) / 256, 4096));
-        int rc = launch(e, -1, [&] {
+        // a compressed probs pass has already swapped nothing: its input pair is X
+        int rc = e->rep_orb ? launch(e, -1, [&] {
+            k_orb_stage_read<<<grid, 256, 0, e->stream>>>(p, orb_src(e), e->orb_rec, x, gather ? 1 : 0,
+                                                          first, count, d);
+        }) : launch(e, -1, [&] {
             if (gather) {
                 if (e->e1) k_stage_read<kSrcGather, true><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
                 else k_stage_read<kSrcGather, false><<<grid, 256, 0, e->stream>>>(p, x, first, count, d);
@@ -1613,7 +1855,10 @@ int shs_state_read(shs_engine* e, int32_t x, uint64_t first, uint64_t count, dou
         SHS_CUDA(cudaMallocAsync(&d, sizeof(double2) * count, e->stream));
         const int grid = static_cast<int>(std::min<uint64_t>((count + 255) / 256, 4096));
         const double wr = e->w[2 * x], wi = e->w[2 * x + 1];
-        int rc = launch(e, -1, [&] {
+        int rc = e->rep_orb ? launch(e, -1, [&] {
+            k_orb_state_read<<<grid, 256, 0, e->stream>>>(orb_src(e), e->orb_rec, e->N, wr, wi, e->inv,
+                                                          nullptr, first, count, d);
+        }) : launch(e, -1, [&] {
             if (e->e1) k_state_read<true><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, first, count, d);
             else k_state_read<false><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, first, count, d);
         });
@@ -1641,7 +1886,10 @@ int shs_state_gather(shs_engine* e, int32_t x, const uint64_t* idx, uint64_t cou
                                  e->stream));
         const int grid = static_cast<int>(std::min<uint64_t>((count + 255) / 256, 4096));
         const double wr = e->w[2 * x], wi = e->w[2 * x + 1];
-        int rc = launch(e, -1, [&] {
+        int rc = e->rep_orb ? launch(e, -1, [&] {
+            k_orb_state_read<<<grid, 256, 0, e->stream>>>(orb_src(e), e->orb_rec, e->N, wr, wi, e->inv,
+                                                          di, 0, count, d);
+        }) : launch(e, -1, [&] {
             if (e->e1) k_state_gather<true><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, di, count, d);
             else k_state_gather<false><<<grid, 256, 0, e->stream>>>(e->X, 0, e->N, wr, wi, e->inv, di, count, d);
         });

@@ -44,6 +44,7 @@
 
 #include "device_math.cuh"
 #include "stage_kernels.cuh"
+#include "orbit.cuh"
 
 namespace shs {
 
@@ -80,12 +81,19 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #ifndef SHS_RR_CONSUMER_WARPS
 #define SHS_RR_CONSUMER_WARPS 16
 #endif
-template <bool kSplit>
+// The orbit variant (kOrb) runs 8 producer warps (its copies need rank
+// arithmetic: 4 warps were issue-bound) and 12 consumer warps (members only).
+template <bool kSplit, bool kOrb = false>
 struct TileCfg {
-    static constexpr int kCW = kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
+    static constexpr int kCW = kOrb ? 12 : kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
     static constexpr int kCons = 32 * kCW;
+    static constexpr int kPW = kOrb ? 8 : kProducerWarps;   // producer warps
+    static constexpr int kProds = 32 * kPW;
+    static constexpr int kCopies = kRows * kCols / kProds;  // copies per side per producer
+    static constexpr int kColStep = kProds / kRows;         // columns between a thread's copies
+    static constexpr int kRowStep = kProds / kCols;         // rows between a thread's copies
     static constexpr int kProdWarp = kCW;                   // first producer warp
-    static constexpr int kChainWarp0 = kCW + kProducerWarps;  // first chain warp (probs only)
+    static constexpr int kChainWarp0 = kCW + kPW;           // first chain warp (probs only)
     static constexpr int kRowsPerCons = kRows * kCols / kCons;
     static constexpr int kNSync = kCons + 32 * kChainWarps;   // norm named-barrier thread count
     static_assert(kCons % kCols == 0 && kRowsPerCons >= 1, "consumer layout");
@@ -122,6 +130,16 @@ struct TileParams {
     // of a stage whose probs pass did so returns at once when group 0 is kept
     int spec;
     const DevStage* dev;  // device-resident run: sc / sel from this slot instead
+    // orbit-compressed state (orbit.cuh, k_tiled<true, false, true>): the source
+    // is slot X or X1 of a pair, picked by prev->sel (device-resident run) or
+    // prev_sel; both groups are written, h0 to Y and h1 to Y1, at the members'
+    // ranks unless `write` is 0 (the run's last stage); rec: the rank records
+    const double2* X1;
+    double2* Y1;
+    const ulonglong2* orb;
+    const DevStage* prev;
+    int prev_sel;
+    int write;
 };
 
 __device__ __forceinline__ uint64_t tile_row_len(uint64_t j, const TileParams& p) {
@@ -195,23 +213,51 @@ struct __align__(16) TileStage {
     uint64_t last;  // 1 on the last chunk of the CTA's sequence
 };
 
-template <bool kProbs>
+// orbit variant: rank records of the chunk's 32 column runs (items 0..31) and
+// 32 row runs (items 32..63), two consecutive 64-index records each, loaded
+// into registers kOrbAhead chunks ahead
+constexpr int kOrbAhead = 3;
+// an item's 32-index window of one chunk: membership bits (row items: cut at the
+// row's end), rank of its first index, its start and whether it wraps past N - 1
+struct OrbWin {
+    uint64_t rank, start;
+    uint32_t bits, wrap;
+};
+
+template <bool kProbs, bool kOrb = false>
 struct TileSmem {
     TileStage stage[kStages];
     double nrm[kProbs ? kNormBufs : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
     uint64_t full[kStages], empty[kStages];
     unsigned long long digits[2][kDigits];
     uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
+    // orbit variant: each ring slot's rows as (membership bits of its 32 columns,
+    // rank of its first column), and the record ring
+    uint64_t row_rank[kOrb ? kStages : 1][kRows];
+    uint32_t row_bits[kOrb ? kStages : 1][kRows];
+    // the slot's members in row-major order: (row << 5 | column), and each row's
+    // first member (row_off[32] = the count)
+    uint16_t memb[kOrb ? kStages : 1][kOrb ? kRows * kCols : 1];
+    uint32_t row_off[kOrb ? kStages : 1][kRows + 1];
+    uint32_t nrm_bits[kOrb ? kNormBufs : 1][kRows];  // members of each norm tile row
 };
 
-template <bool kProbs, bool kSplit>
+template <bool kProbs, bool kSplit, bool kOrb = false>
 constexpr int tile_threads() {
-    return 32 * (TileCfg<kSplit>::kCW + kProducerWarps + (kProbs ? kChainWarps : 0));
+    return 32 * (TileCfg<kSplit, kOrb>::kCW + TileCfg<kSplit, kOrb>::kPW + (kProbs ? kChainWarps : 0));
 }
 
-template <bool kProbs>
+template <bool kProbs, bool kOrb = false>
 constexpr size_t tile_smem_bytes() {
-    return sizeof(TileSmem<kProbs>);
+    return sizeof(TileSmem<kProbs, kOrb>);
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int kN>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
 }
 
 // The tile's row table, spread over a warp: lane l holds rows l + 32 h
@@ -304,18 +350,21 @@ struct CtaWork<false> {
     uint32_t* q;
     uint64_t b, nt, k;
     bool producer, p0;
+    int nprod;  // producer threads (named barrier count)
     __device__ __forceinline__ uint64_t fetch(const TileParams& p) const {
         return gridDim.x + (atomicAdd(p.band_ctr, 1ull) - p.band_base);
     }
-    __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t* queue, bool is_producer)
-        : q(queue), b(blockIdx.x), nt(p.ntiles), k(0), producer(is_producer) {
-        p0 = producer && threadIdx.x == 32 * TileCfg<false>::kProdWarp;
+    __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t* queue, bool is_producer,
+                                       int prod_warp0 = TileCfg<false>::kProdWarp,
+                                       int nprod_ = kProducers)
+        : q(queue), b(blockIdx.x), nt(p.ntiles), k(0), producer(is_producer), nprod(nprod_) {
+        p0 = producer && threadIdx.x == 32 * prod_warp0;
         if (p0) {
             q[0] = static_cast<uint32_t>(b);
             const uint64_t b1 = fetch(p);
             q[1] = static_cast<uint32_t>(b1 < nt ? b1 : nt);
         }
-        if (producer) named_sync(kProducerBar, kProducers);
+        if (producer) named_sync(kProducerBar, nprod);
     }
     __device__ __forceinline__ bool valid() const { return b < nt; }
     __device__ __forceinline__ void next(const TileParams& p) {
@@ -326,7 +375,7 @@ struct CtaWork<false> {
                 q[(k + 2) % kBandQ] = static_cast<uint32_t>(b2 < nt ? b2 : nt);
             }
         }
-        if (producer) named_sync(kProducerBar, kProducers);
+        if (producer) named_sync(kProducerBar, nprod);
         ++k;
         b = q[k % kBandQ];
     }
@@ -340,7 +389,7 @@ template <>
 struct CtaWork<true> {
     uint64_t k, K, b, b_first, b_last, lo_col, hi_col, nt;
     bool bulk, tail_empty;
-    __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t*, bool) {
+    __device__ __forceinline__ CtaWork(const TileParams& p, uint32_t*, bool, int = 0, int = 0) {
         const uint2 s0 = p.split[blockIdx.x], s1 = p.split[blockIdx.x + 1];
         b_first = s0.x;
         lo_col = uint64_t(s0.y) * kCols;
@@ -440,13 +489,15 @@ __device__ __forceinline__ void store_rows(const LaneRows& lr, int lane, uint64_
     }
 }
 
-template <bool kProbs, bool kSplit>
-__global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(TileParams p) {
+template <bool kProbs, bool kSplit, bool kOrb = false>
+__global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_tiled(TileParams p) {
+    static_assert(!kOrb || (kProbs && !kSplit && kRows == 32 && kCols == 32),
+                  "orbit variant: probs pass, whole bands, 32 x 32 chunks");
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    TileSmem<kProbs>& sm = *reinterpret_cast<TileSmem<kProbs>*>(smem_raw);
+    TileSmem<kProbs, kOrb>& sm = *reinterpret_cast<TileSmem<kProbs, kOrb>*>(smem_raw);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    using Cfg = TileCfg<kSplit>;
+    using Cfg = TileCfg<kSplit, kOrb>;
     constexpr int kConsumerWarps = Cfg::kCW, kConsumers = Cfg::kCons;
     constexpr int kProducerWarp = Cfg::kProdWarp, kChainWarp = Cfg::kChainWarp0;
     constexpr int kRowsPerConsumer = Cfg::kRowsPerCons, kNormSync = Cfg::kNSync;
@@ -467,7 +518,8 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&sm.full[s], kProducers + 1);  // copies of every producer + header
+            // copies of every producer + header
+            mbar_init(&sm.full[s], Cfg::kProds + 1);
             mbar_init(&sm.empty[s], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -476,7 +528,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
         for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&sm.digits[0][0])[i] = 0ull;
     __syncthreads();
 
-    if (warp >= kProducerWarp && warp < kProducerWarp + kProducerWarps) {
+    if (warp >= kProducerWarp && warp < kProducerWarp + Cfg::kPW) {
         // ------------------------------------------------------------ producers
         // gathered side: element e = pt + kProducers * k is (column e / kRows,
         // row e % kRows = pt % kRows): kRows consecutive threads copy one
@@ -488,8 +540,160 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
         const int r_src = pt & (kRows - 1);
         const int src_c0 = pt / kRows;
         const int dst_r0 = pt / kCols, dst_c = pt % kCols;
+        constexpr int kOC = Cfg::kCopies, kOCS = Cfg::kColStep, kORS = Cfg::kRowStep;
         int stage = 0;
         uint32_t phase = 0;
+        if constexpr (kOrb) {
+            // Orbit variant. Element (row r, column c) of a chunk is an orbit member
+            // on the direct side (z_j + c) iff its gathered source (j + c m) is one
+            // (m is a power of a), so both copies are skipped for non-members and
+            // the rest are read at their ranks, from 32-index windows (membership
+            // bits, rank of the first index) built from two 64-index records.
+            // Producer warp w copies columns w + 8k (lanes = rows) and rows w + 8k
+            // (lanes = columns); its lanes 0..7 hold those 8 windows, loaded two
+            // chunks ahead into registers, so the warps never wait on each other
+            // (a cp.async group would also wait for the data copies). Warp 0 also
+            // builds the consumers' row table: all 32 row windows (lane = row),
+            // the row offsets and the chunk's member list.
+            static_assert(Cfg::kPW == 8 && Cfg::kColStep == 8 && Cfg::kRowStep == 8, "orbit layout");
+            const int pw = warp - kProducerWarp;
+            const double2* Xs = (p.prev ? p.prev->sel : p.prev_sel) ? p.X1 : p.X;
+            const uint32_t lt_lane = (1u << lane) - 1u;
+            const int itk = lane & 3;
+            const bool icol = lane < 4, irow = lane >= 4 && lane < 8;
+            for (CtaWork<kSplit> wk(p, sm.bandq, true, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
+                const uint64_t j0 = wk.band() * kRows;
+                LaneRows lr;
+                const uint64_t tend = tile_rows_split(p, j0, lane, lr, 0, ~0ull);
+                const uint64_t nch = (tend + kCols - 1) / kCols;  // >= 1 (rows are >= 512 long)
+                const uint64_t rlen = lr.len[0];  // row `lane`
+                // item of lanes 0..7: column pw + 8 itk (lanes 0..3) / row pw + 8 itk (4..7)
+                uint64_t iws, ilen;
+                {
+                    uint64_t z, len;
+                    row_from_lanes(lr, pw + 8 * itk, z, len);
+                    if (icol) {
+                        iws = addmod(j0, mulmod_shoup(pw + 8 * itk, p.m, p.m_sh, p.N), p.N);
+                        ilen = ~0ull;
+                    } else {
+                        iws = z;
+                        ilen = irow ? len : 0;
+                    }
+                }
+                uint64_t rws = lr.z[0];  // warp 0: row `lane`'s window start
+                // records: [chunk n, n + 1][item / row][lo, hi]
+                uint64_t lws = iws, lrws = rws;  // load positions (chunk n + 2)
+                auto load_item = [&](uint64_t n, ulonglong2& lo, ulonglong2& hi) {
+                    lo = hi = make_ulonglong2(0ull, 0ull);
+                    if ((icol || irow) && n < nch && n * kCols < ilen) {
+                        lo = __ldg(p.orb + (lws >> 6));
+                        hi = __ldg(p.orb + (lws >> 6) + 1);
+                    }
+                    lws = icol ? addmod(lws, p.m_chunk, p.N) : lws + kCols;
+                };
+                auto load_row = [&](uint64_t n, ulonglong2& lo, ulonglong2& hi) {
+                    lo = hi = make_ulonglong2(0ull, 0ull);
+                    if (pw == 0 && n < nch && n * kCols < rlen) {
+                        lo = __ldg(p.orb + (lrws >> 6));
+                        hi = __ldg(p.orb + (lrws >> 6) + 1);
+                    }
+                    lrws += kCols;
+                };
+                ulonglong2 i0l, i0h, i1l, i1h, r0l, r0h, r1l, r1h;
+                load_item(0, i0l, i0h);
+                load_item(1, i1l, i1h);
+                load_row(0, r0l, r0h);
+                load_row(1, r1l, r1h);
+                for (uint64_t n = 0; n < nch; ++n) {
+                    const uint64_t i0 = n * kCols;
+                    // window of this lane's item at chunk n
+                    uint32_t ib = 0, iwrap = 0;
+                    uint64_t irank = 0;
+                    {
+                        const unsigned o = static_cast<unsigned>(iws & 63);
+                        if (i0 < ilen) {
+                            ib = static_cast<uint32_t>(o ? (i0l.x >> o) | (i0h.x << (64 - o)) : i0l.x);
+                            irank = i0l.y + __popcll(i0l.x & lowmask64(o));
+                            if (irow && ilen - i0 < 32) ib &= (1u << (ilen - i0)) - 1u;
+                            if (icol && iws + (kRows - 1) >= p.N) iwrap = 1;
+                        }
+                    }
+                    const uint64_t iws_n = iws;
+                    iws = icol ? addmod(iws, p.m_chunk, p.N) : iws + kCols;
+                    i0l = i1l;
+                    i0h = i1h;
+                    load_item(n + 2, i1l, i1h);
+                    mbar_wait(&sm.empty[stage], phase ^ 1);
+                    TileStage& st = sm.stage[stage];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {  // gathered side: column pw + 8k, row `lane`
+                        const int cc = pw + 8 * k;
+                        const uint32_t cb = __shfl_sync(0xffffffffu, ib, k);
+                        const uint64_t crank = __shfl_sync(0xffffffffu, irank, k);
+                        const uint32_t cwrap = __shfl_sync(0xffffffffu, iwrap, k);
+                        const uint64_t cstart = __shfl_sync(0xffffffffu, iws_n, k);
+                        if (((cb >> lane) & 1u) && i0 + cc < rlen) {
+                            uint64_t rank = crank + __popc(cb & lt_lane);
+                            if (cwrap && cstart + lane >= p.N)  // the run wraps past N - 1 (rare)
+                                orb_lookup(p.orb, cstart + lane - p.N, rank);
+                            cp_async16(&st.src[cc][lane], Xs + rank);
+                        } else if (cwrap && i0 + cc < rlen && cstart + lane >= p.N) {
+                            uint64_t rank;
+                            if (orb_lookup(p.orb, cstart + lane - p.N, rank))
+                                cp_async16(&st.src[cc][lane], Xs + rank);
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {  // direct side: row pw + 8k, column `lane`
+                        const int rr = pw + 8 * k;
+                        const uint32_t rb = __shfl_sync(0xffffffffu, ib, 4 + k);
+                        const uint64_t rrank = __shfl_sync(0xffffffffu, irank, 4 + k);
+                        if ((rb >> lane) & 1u)
+                            cp_async16(&st.dst[rr][lane], Xs + (rrank + __popc(rb & lt_lane)));
+                    }
+                    cp_async_arrive(&sm.full[stage]);
+                    if (pw == 0) {  // the consumers' row table, lane = row
+                        uint32_t rb = 0;
+                        uint64_t rrank = 0;
+                        const unsigned o = static_cast<unsigned>(rws & 63);
+                        if (i0 < rlen) {
+                            rb = static_cast<uint32_t>(o ? (r0l.x >> o) | (r0h.x << (64 - o)) : r0l.x);
+                            rrank = r0l.y + __popcll(r0l.x & lowmask64(o));
+                            if (rlen - i0 < 32) rb &= (1u << (rlen - i0)) - 1u;
+                        }
+                        rws += kCols;
+                        r0l = r1l;
+                        r0h = r1h;
+                        load_row(n + 2, r1l, r1h);
+                        const uint32_t cnt = __popc(rb);
+                        uint32_t incl = cnt;
+#pragma unroll
+                        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o2);
+                            if (lane >= o2) incl += v;
+                        }
+                        uint32_t e = incl - cnt;
+                        sm.row_off[stage][lane] = e;
+                        if (lane == 31) sm.row_off[stage][kRows] = incl;
+                        sm.row_bits[stage][lane] = rb;
+                        sm.row_rank[stage][lane] = rrank;
+                        for (uint32_t m = rb; m; m &= m - 1)
+                            sm.memb[stage][e++] = static_cast<uint16_t>((lane << 5) | (__ffs(m) - 1));
+                        store_row_spans(lr, lane, st.row_z, st.row_lo, st.row_n);
+                        if (lane == 0) {
+                            st.i0 = i0;
+                            st.last = (wk.last() && n + 1 == nch) ? 1 : 0;
+                        }
+                        __syncwarp();  // row table and member list ordered before lane 0's release
+                        if (lane == 0) mbar_arrive(&sm.full[stage]);
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        } else
         for (CtaWork<kSplit> wk(p, sm.bandq, true); wk.valid(); wk.next(p)) {
             const uint64_t j0 = wk.band() * kRows;
             const uint64_t lo_col = wk.lo();
@@ -580,6 +784,25 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
             more = st.last == 0;
             const int b = static_cast<int>(k % kNormBufs);
             if (kProbs && k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
+            if constexpr (kOrb) {
+                // only the chunk's members (about half of its 1024 positions): the
+                // e-th in row-major order; the chains skip the other positions
+                const uint32_t M = sm.row_off[stage][kRows];
+                for (uint32_t e = tid; e < M; e += kConsumers) {
+                    const uint32_t rc = sm.memb[stage][e];
+                    const int r = static_cast<int>(rc >> 5), cc = static_cast<int>(rc & 31);
+                    double h0r, h0i, h1r, h1i;
+                    stage_pair(sc, st.dst[r][cc], st.src[cc][r], h0r, h0i, h1r, h1i);
+                    sm.nrm[b][0][r][cc] = cnorm(h0r, h0i);
+                    sm.nrm[b][1][r][cc] = cnorm(h1r, h1i);
+                    if (p.write) {  // both groups at the member's rank
+                        const uint64_t at = sm.row_rank[stage][r] + (e - sm.row_off[stage][r]);
+                        p.Y[at] = make_double2(h0r, h0i);
+                        p.Y1[at] = make_double2(h1r, h1i);
+                    }
+                }
+                if (tid < kRows) sm.nrm_bits[b][tid] = sm.row_bits[stage][tid];
+            } else
 #pragma unroll
             for (int q = 0; q < kRowsPerConsumer; ++q) {
                 const int r = rg * kRowsPerConsumer + q;
@@ -646,7 +869,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
         DigitWindow win;
         window_reset(win);
         uint64_t k = 0;
-        for (CtaWork<kSplit> wk(p, sm.bandq, false); wk.valid(); wk.next(p)) {
+        for (CtaWork<kSplit> wk(p, sm.bandq, false, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
             const uint64_t j0 = wk.band() * kRows;
             const uint64_t lo_col = wk.lo();
             LaneRows lr;
@@ -664,6 +887,9 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
                 const int b = static_cast<int>(k % kNormBufs);
                 named_sync(kNormFull0 + b, kNormSync);
                 const double* row = &sm.nrm[b][cg][cr][0];
+                // orbit variant: positions off the orbit hold stale norms, read as +0.0
+                const uint32_t mb = kOrb ? sm.nrm_bits[kOrb ? b : 0][cr] : ~0u;
+                auto nv = [&](int cc) { return ((mb >> cc) & 1u) ? row[cc] : 0.0; };
                 if (i0 >= c_fast && i0 + kCols <= c_hi) {
                     // interior chunk (the common case): 64 in-order adds, branch-free.
                     // At most one block ends inside the chunk (kCols <= 256), at
@@ -675,7 +901,11 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
                     double a = c_s, nb = 0.0;
 #pragma unroll
                     for (int cc = 0; cc < kCols; cc += 2) {
-                        const double2 x = *reinterpret_cast<const double2*>(row + cc);
+                        double2 x = *reinterpret_cast<const double2*>(row + cc);
+                        if (kOrb) {
+                            x.x = ((mb >> cc) & 1u) ? x.x : 0.0;
+                            x.y = ((mb >> (cc + 1)) & 1u) ? x.y : 0.0;
+                        }
                         const bool lo0 = cc <= qb, lo1 = cc + 1 <= qb;
                         a = __dadd_rn(a, lo0 ? x.x : 0.0);
                         nb = __dadd_rn(nb, lo0 ? 0.0 : x.x);
@@ -697,19 +927,19 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit>()), 1) k_tiled(T
                     if (i0 + qa < c_head) {
                         const int qh = static_cast<int>(min(c_head - i0, uint64_t(q1)));
                         double* head = p.head + ((j0 + cr) * 2 + cg) * 256 + i0;
-                        for (int cc = qa; cc < qh; ++cc) head[cc] = row[cc];
+                        for (int cc = qa; cc < qh; ++cc) head[cc] = nv(cc);
                         qa = qh;
                     }
                     while (qa < q1) {
                         const int qb = qa + static_cast<int>(255 - ((c_z + i0 + qa) & 255));
                         if (qb < q1) {
-                            for (int cc = qa; cc <= qb; ++cc) c_s = __dadd_rn(c_s, row[cc]);
+                            for (int cc = qa; cc <= qb; ++cc) c_s = __dadd_rn(c_s, nv(cc));
                             p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = c_s;
                             window_add(win, c_s, sm.digits[cg]);
                             c_s = 0.0;
                             qa = qb + 1;
                         } else {
-                            for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, row[cc]);
+                            for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, nv(cc));
                             qa = q1;
                         }
                     }

@@ -431,6 +431,18 @@ class IterativeShorEngine:
     def sparse_stages(self) -> int:
         return self._lib.shs_engine_sparse_stages(self._h)
 
+    def set_orbit(self, enable: bool) -> None:
+        """Orbit-compressed stages (from N >= 2^26; off by default): stages with
+        whole-band tile plans store and sweep only the r = ord_N(a) members of
+        <a>, bit-identical results. Toggling resets the state."""
+        _raise(self._lib.shs_engine_set_orbit(self._h, 1 if enable else 0))
+
+    def orbit_info(self) -> dict:
+        """{"r": orbit size (0: off), "stages": stages run compressed, "first": the first}"""
+        out = (C.c_uint64 * 3)()
+        _raise(self._lib.shs_engine_orbit_info(self._h, out))
+        return {"r": int(out[0]), "stages": int(out[1]), "first": int(out[2])}
+
     def launch_count(self) -> int:
         return self._lib.shs_engine_launch_count(self._h)
 
