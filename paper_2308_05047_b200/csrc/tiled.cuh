@@ -42,6 +42,9 @@
 //                        predecessor's tail partial and the row's stored head.
 #pragma once
 
+#include <type_traits>
+
+
 #include "device_math.cuh"
 #include "stage_kernels.cuh"
 #include "orbit.cuh"
@@ -81,13 +84,13 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #ifndef SHS_RR_CONSUMER_WARPS
 #define SHS_RR_CONSUMER_WARPS 16
 #endif
-// The orbit variant (kOrb) runs 8 producer warps (its copies need rank
-// arithmetic: 4 warps were issue-bound) and 12 consumer warps (members only).
+// The orbit variant (kOrb) runs 14 consumer warps (members only, each found by a
+// search of its slot's row offsets).
 template <bool kSplit, bool kOrb = false>
 struct TileCfg {
-    static constexpr int kCW = kOrb ? 12 : kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
+    static constexpr int kCW = kOrb ? 14 : kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
     static constexpr int kCons = 32 * kCW;
-    static constexpr int kPW = kOrb ? 8 : kProducerWarps;   // producer warps
+    static constexpr int kPW = kProducerWarps;              // producer warps
     static constexpr int kProds = 32 * kPW;
     static constexpr int kCopies = kRows * kCols / kProds;  // copies per side per producer
     static constexpr int kColStep = kProds / kRows;         // columns between a thread's copies
@@ -140,6 +143,8 @@ struct TileParams {
     const DevStage* prev;
     int prev_sel;
     int write;
+    const struct OrbPlan* plan;  // k_orb_plan output: band b's sub-chunk n at plan[band_off[b] + n]
+    const uint32_t* band_off;
 };
 
 __device__ __forceinline__ uint64_t tile_row_len(uint64_t j, const TileParams& p) {
@@ -184,6 +189,22 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
                  : "memory");
 }
+// predicated 16-byte cp.async (no branch around it)
+__device__ __forceinline__ void cp_async16_if(bool pred, void* dst, const void* src) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(static_cast<uint32_t>(pred))
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA), completing `bytes` on bar's transaction count
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
 // arrive on bar once all of this thread's prior cp.async copies have landed
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar))
@@ -213,34 +234,49 @@ struct __align__(16) TileStage {
     uint64_t last;  // 1 on the last chunk of the CTA's sequence
 };
 
-// orbit variant: rank records of the chunk's 32 column runs (items 0..31) and
-// 32 row runs (items 32..63), two consecutive 64-index records each, loaded
-// into registers kOrbAhead chunks ahead
-constexpr int kOrbAhead = 3;
-// an item's 32-index window of one chunk: membership bits (row items: cut at the
-// row's end), rank of its first index, its start and whether it wraps past N - 1
-struct OrbWin {
-    uint64_t rank, start;
-    uint32_t bits, wrap;
+// Orbit variant (kOrb). A per-stage pre-pass (k_orb_plan) turns the rank
+// records into one OrbPlan per band and 32-column sub-chunk: the rank base and
+// membership window of each gathered column run and of each row run. The
+// producers prefetch plans with 1-D bulk copies (TMA) kOrbPlanRing entries
+// ahead, so no record lookup sits on their path, and pack the members of up to
+// kOrbSub consecutive sub-chunks of a band into one compact slot (up to
+// kOrbCap members per side: a slot holds as many live amplitudes as a dense
+// 32 x 32 chunk would, so as many bytes are in flight per SM).
+struct OrbPlan {
+    uint64_t crank[kCols];  // rank of column run c's first source; bit 63: the run wraps past N - 1
+    uint64_t rrank[kRows];  // rank of row r's first index of the sub-chunk
+    uint32_t cbits[kCols];  // membership of the run's kRows sources
+    uint32_t rbits[kRows];  // membership of the row's kCols indices (0 past the row's end)
+};
+constexpr int kOrbCap = 1088;
+constexpr int kOrbSub = 4;
+constexpr int kOrbPlanRing = 8;
+constexpr uint64_t kOrbWrap = 1ull << 63;
+
+struct __align__(16) OrbSlot {
+    double2 src[kOrbCap];  // gathered values of the slot's members (member order)
+    double2 dst[kOrbCap];  // direct values
+    uint64_t rrank[kOrbSub][kRows];
+    uint32_t rbits[kOrbSub][kRows];
+    uint16_t roff[kOrbSub][kRows];  // row r's first member within sub-chunk j
+    uint16_t moff[kOrbSub + 1];     // sub-chunk j's first member in the slot
+    uint16_t nsub;
+    uint32_t i0, last;              // (i0 unused: kept for the shared consumer prologue)
 };
 
 template <bool kProbs, bool kOrb = false>
 struct TileSmem {
-    TileStage stage[kStages];
+    std::conditional_t<kOrb, OrbSlot, TileStage> stage[kStages];
     double nrm[kProbs ? kNormBufs : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
     uint64_t full[kStages], empty[kStages];
     unsigned long long digits[2][kDigits];
     uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
-    // orbit variant: each ring slot's rows as (membership bits of its 32 columns,
-    // rank of its first column), and the record ring
-    uint64_t row_rank[kOrb ? kStages : 1][kRows];
-    uint32_t row_bits[kOrb ? kStages : 1][kRows];
-    // the slot's members in row-major order: (row << 5 | column), and each row's
-    // first member (row_off[32] = the count)
-    uint16_t memb[kOrb ? kStages : 1][kOrb ? kRows * kCols : 1];
-    uint32_t row_off[kOrb ? kStages : 1][kRows + 1];
-    uint32_t nrm_bits[kOrb ? kNormBufs : 1][kRows];  // members of each norm tile row
+    uint32_t nrm_bits[kOrb ? kNormBufs : 1][kRows];  // orbit: members of each norm tile row
+    uint64_t planfull[kOrb ? kOrbPlanRing : 1], planempty[kOrb ? kOrbPlanRing : 1];
+    OrbPlan plan[kOrb ? kOrbPlanRing : 1];
 };
+
+static_assert(sizeof(TileSmem<true, true>) <= 232448, "orbit variant: shared memory per CTA");
 
 template <bool kProbs, bool kSplit, bool kOrb = false>
 constexpr int tile_threads() {
@@ -252,13 +288,7 @@ constexpr size_t tile_smem_bytes() {
     return sizeof(TileSmem<kProbs, kOrb>);
 }
 
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int kN>
-__device__ __forceinline__ void cp_async_wait_group() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
-}
+
 
 // The tile's row table, spread over a warp: lane l holds rows l + 32 h
 // (h < kRowsPerLane), or row l & (kRows - 1) when kRows < 32. Returns the tile
@@ -344,6 +374,7 @@ struct CtaWork;
 // acquire -> named barrier).
 constexpr int kBandQ = 16;  // > kStages + kNormBufs: the chain lags <= 8 chunks (bands)
 constexpr int kProducerBar = 1 + 2 * kNormBufs;  // named barrier of the producer warps
+constexpr int kConsumerBar = kProducerBar + 1;   // orbit variant: consumers released together
 
 template <>
 struct CtaWork<false> {
@@ -522,6 +553,11 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             mbar_init(&sm.full[s], Cfg::kProds + 1);
             mbar_init(&sm.empty[s], kConsumerWarps);
         }
+        if constexpr (kOrb)
+            for (int s = 0; s < kOrbPlanRing; ++s) {
+                mbar_init(&sm.planfull[s], 1);
+                mbar_init(&sm.planempty[s], Cfg::kPW);
+            }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (kProbs)
@@ -540,151 +576,135 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
         const int r_src = pt & (kRows - 1);
         const int src_c0 = pt / kRows;
         const int dst_r0 = pt / kCols, dst_c = pt % kCols;
-        constexpr int kOC = Cfg::kCopies, kOCS = Cfg::kColStep, kORS = Cfg::kRowStep;
         int stage = 0;
         uint32_t phase = 0;
         if constexpr (kOrb) {
-            // Orbit variant. Element (row r, column c) of a chunk is an orbit member
-            // on the direct side (z_j + c) iff its gathered source (j + c m) is one
-            // (m is a power of a), so both copies are skipped for non-members and
-            // the rest are read at their ranks, from 32-index windows (membership
-            // bits, rank of the first index) built from two 64-index records.
-            // Producer warp w copies columns w + 8k (lanes = rows) and rows w + 8k
-            // (lanes = columns); its lanes 0..7 hold those 8 windows, loaded two
-            // chunks ahead into registers, so the warps never wait on each other
-            // (a cp.async group would also wait for the data copies). Warp 0 also
-            // builds the consumers' row table: all 32 row windows (lane = row),
-            // the row offsets and the chunk's member list.
-            static_assert(Cfg::kPW == 8 && Cfg::kColStep == 8 && Cfg::kRowStep == 8, "orbit layout");
+            // Orbit variant. Element (row r, column c) of a sub-chunk is an orbit
+            // member on the direct side (z_j + c) iff its gathered source (j + c m)
+            // is one (m is a power of a); members are copied into the slot in
+            // row-major member order, each side from its rank. Warp w copies the
+            // gathered columns w + 4k (lanes = rows) and the direct rows w + 4k
+            // (lanes = columns). Every warp evaluates the same packing decision
+            // from the same plan; warp 0 also writes the slot's tables, and its
+            // lane 0 issues the plan prefetches.
             const int pw = warp - kProducerWarp;
+            const bool issuer = pw == 0 && lane == 0;
             const double2* Xs = (p.prev ? p.prev->sel : p.prev_sel) ? p.X1 : p.X;
             const uint32_t lt_lane = (1u << lane) - 1u;
-            const int itk = lane & 3;
-            const bool icol = lane < 4, irow = lane >= 4 && lane < 8;
+            uint64_t gc = 0;  // plan entries consumed
+            // issuer walk: band index ik of the CTA's band sequence, sub-chunk in of in_n
+            uint64_t gi = 0, ik = 0, in = 0, in_n = 0, iband = ~0ull;
+            bool idone = false;
+            auto band_nch = [&](uint64_t bb) {
+                uint64_t mx = 0;
+                for (int r = 0; r < kRows; ++r) {
+                    const uint64_t l = tile_row_len(bb * kRows + r, p);
+                    mx = l > mx ? l : mx;
+                }
+                return (mx + kCols - 1) / kCols;
+            };
+            auto issue = [&]() {  // the next plan entry, kOrbPlanRing - 1 ahead of the consumers
+                while (in == in_n) {
+                    if (idone) return;
+                    if (iband != ~0ull) ++ik;
+                    const uint64_t bb = ik == 0 ? blockIdx.x : sm.bandq[ik % kBandQ];
+                    if (bb >= p.ntiles) {
+                        idone = true;
+                        return;
+                    }
+                    iband = bb;
+                    in = 0;
+                    in_n = band_nch(bb);
+                }
+                const int ps = static_cast<int>(gi % kOrbPlanRing);
+                mbar_wait(&sm.planempty[ps], static_cast<uint32_t>((gi / kOrbPlanRing) & 1) ^ 1);
+                mbar_arrive_expect_tx(&sm.planfull[ps], sizeof(OrbPlan));
+                bulk_g2s(&sm.plan[ps], p.plan + (p.band_off[iband] + in), sizeof(OrbPlan),
+                         &sm.planfull[ps]);
+                ++in;
+                ++gi;
+            };
             for (CtaWork<kSplit> wk(p, sm.bandq, true, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
+                if (issuer && wk.k == 0)
+                    for (int q = 0; q < kOrbPlanRing - 1; ++q) issue();
                 const uint64_t j0 = wk.band() * kRows;
                 LaneRows lr;
                 const uint64_t tend = tile_rows_split(p, j0, lane, lr, 0, ~0ull);
-                const uint64_t nch = (tend + kCols - 1) / kCols;  // >= 1 (rows are >= 512 long)
-                const uint64_t rlen = lr.len[0];  // row `lane`
-                // item of lanes 0..7: column pw + 8 itk (lanes 0..3) / row pw + 8 itk (4..7)
-                uint64_t iws, ilen;
-                {
-                    uint64_t z, len;
-                    row_from_lanes(lr, pw + 8 * itk, z, len);
-                    if (icol) {
-                        iws = addmod(j0, mulmod_shoup(pw + 8 * itk, p.m, p.m_sh, p.N), p.N);
-                        ilen = ~0ull;
-                    } else {
-                        iws = z;
-                        ilen = irow ? len : 0;
-                    }
-                }
-                uint64_t rws = lr.z[0];  // warp 0: row `lane`'s window start
-                // records: [chunk n, n + 1][item / row][lo, hi]
-                uint64_t lws = iws, lrws = rws;  // load positions (chunk n + 2)
-                auto load_item = [&](uint64_t n, ulonglong2& lo, ulonglong2& hi) {
-                    lo = hi = make_ulonglong2(0ull, 0ull);
-                    if ((icol || irow) && n < nch && n * kCols < ilen) {
-                        lo = __ldg(p.orb + (lws >> 6));
-                        hi = __ldg(p.orb + (lws >> 6) + 1);
-                    }
-                    lws = icol ? addmod(lws, p.m_chunk, p.N) : lws + kCols;
-                };
-                auto load_row = [&](uint64_t n, ulonglong2& lo, ulonglong2& hi) {
-                    lo = hi = make_ulonglong2(0ull, 0ull);
-                    if (pw == 0 && n < nch && n * kCols < rlen) {
-                        lo = __ldg(p.orb + (lrws >> 6));
-                        hi = __ldg(p.orb + (lrws >> 6) + 1);
-                    }
-                    lrws += kCols;
-                };
-                ulonglong2 i0l, i0h, i1l, i1h, r0l, r0h, r1l, r1h;
-                load_item(0, i0l, i0h);
-                load_item(1, i1l, i1h);
-                load_row(0, r0l, r0h);
-                load_row(1, r1l, r1h);
-                for (uint64_t n = 0; n < nch; ++n) {
-                    const uint64_t i0 = n * kCols;
-                    // window of this lane's item at chunk n
-                    uint32_t ib = 0, iwrap = 0;
-                    uint64_t irank = 0;
-                    {
-                        const unsigned o = static_cast<unsigned>(iws & 63);
-                        if (i0 < ilen) {
-                            ib = static_cast<uint32_t>(o ? (i0l.x >> o) | (i0h.x << (64 - o)) : i0l.x);
-                            irank = i0l.y + __popcll(i0l.x & lowmask64(o));
-                            if (irow && ilen - i0 < 32) ib &= (1u << (ilen - i0)) - 1u;
-                            if (icol && iws + (kRows - 1) >= p.N) iwrap = 1;
-                        }
-                    }
-                    const uint64_t iws_n = iws;
-                    iws = icol ? addmod(iws, p.m_chunk, p.N) : iws + kCols;
-                    i0l = i1l;
-                    i0h = i1h;
-                    load_item(n + 2, i1l, i1h);
+                const uint64_t nch = (tend + kCols - 1) / kCols;
+                uint64_t n = 0;
+                while (n < nch) {
                     mbar_wait(&sm.empty[stage], phase ^ 1);
-                    TileStage& st = sm.stage[stage];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {  // gathered side: column pw + 8k, row `lane`
-                        const int cc = pw + 8 * k;
-                        const uint32_t cb = __shfl_sync(0xffffffffu, ib, k);
-                        const uint64_t crank = __shfl_sync(0xffffffffu, irank, k);
-                        const uint32_t cwrap = __shfl_sync(0xffffffffu, iwrap, k);
-                        const uint64_t cstart = __shfl_sync(0xffffffffu, iws_n, k);
-                        if (((cb >> lane) & 1u) && i0 + cc < rlen) {
-                            uint64_t rank = crank + __popc(cb & lt_lane);
-                            if (cwrap && cstart + lane >= p.N)  // the run wraps past N - 1 (rare)
-                                orb_lookup(p.orb, cstart + lane - p.N, rank);
-                            cp_async16(&st.src[cc][lane], Xs + rank);
-                        } else if (cwrap && i0 + cc < rlen && cstart + lane >= p.N) {
-                            uint64_t rank;
-                            if (orb_lookup(p.orb, cstart + lane - p.N, rank))
-                                cp_async16(&st.src[cc][lane], Xs + rank);
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {  // direct side: row pw + 8k, column `lane`
-                        const int rr = pw + 8 * k;
-                        const uint32_t rb = __shfl_sync(0xffffffffu, ib, 4 + k);
-                        const uint64_t rrank = __shfl_sync(0xffffffffu, irank, 4 + k);
-                        if ((rb >> lane) & 1u)
-                            cp_async16(&st.dst[rr][lane], Xs + (rrank + __popc(rb & lt_lane)));
-                    }
-                    cp_async_arrive(&sm.full[stage]);
-                    if (pw == 0) {  // the consumers' row table, lane = row
-                        uint32_t rb = 0;
-                        uint64_t rrank = 0;
-                        const unsigned o = static_cast<unsigned>(rws & 63);
-                        if (i0 < rlen) {
-                            rb = static_cast<uint32_t>(o ? (r0l.x >> o) | (r0h.x << (64 - o)) : r0l.x);
-                            rrank = r0l.y + __popcll(r0l.x & lowmask64(o));
-                            if (rlen - i0 < 32) rb &= (1u << (rlen - i0)) - 1u;
-                        }
-                        rws += kCols;
-                        r0l = r1l;
-                        r0h = r1h;
-                        load_row(n + 2, r1l, r1h);
+                    OrbSlot& st = sm.stage[stage];
+                    uint32_t M = 0;
+                    int j = 0;
+                    while (j < kOrbSub && n < nch) {
+                        const int ps = static_cast<int>(gc % kOrbPlanRing);
+                        mbar_wait(&sm.planfull[ps], static_cast<uint32_t>((gc / kOrbPlanRing) & 1));
+                        const OrbPlan& E = sm.plan[ps];
+                        const uint32_t rb = E.rbits[lane];  // row `lane`
                         const uint32_t cnt = __popc(rb);
                         uint32_t incl = cnt;
 #pragma unroll
-                        for (int o2 = 1; o2 < 32; o2 <<= 1) {
-                            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o2);
-                            if (lane >= o2) incl += v;
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += v;
                         }
-                        uint32_t e = incl - cnt;
-                        sm.row_off[stage][lane] = e;
-                        if (lane == 31) sm.row_off[stage][kRows] = incl;
-                        sm.row_bits[stage][lane] = rb;
-                        sm.row_rank[stage][lane] = rrank;
-                        for (uint32_t m = rb; m; m &= m - 1)
-                            sm.memb[stage][e++] = static_cast<uint16_t>((lane << 5) | (__ffs(m) - 1));
-                        store_row_spans(lr, lane, st.row_z, st.row_lo, st.row_n);
-                        if (lane == 0) {
-                            st.i0 = i0;
-                            st.last = (wk.last() && n + 1 == nch) ? 1 : 0;
+                        const uint32_t off = incl - cnt;
+                        const uint32_t Mn = __shfl_sync(0xffffffffu, incl, 31);
+                        if (j > 0 && M + Mn > kOrbCap) break;  // the next slot starts with it
+                        const uint64_t i0 = n * kCols;
+                        // column runs wrapping past N - 1 (rare): this warp's columns, lane bits
+                        const uint32_t wrapc = __ballot_sync(0xffffffffu, (E.crank[lane] & kOrbWrap) != 0) &
+                                               (0x11111111u << pw);
+                        const uint32_t mo = M + off;
+#pragma unroll
+                        for (int k = 0; k < kCols / Cfg::kPW; ++k) {  // gathered: column pw + 4k, row `lane`
+                            const int cc = pw + Cfg::kPW * k;
+                            const uint64_t rank = (E.crank[cc] & ~kOrbWrap) + __popc(E.cbits[cc] & lt_lane);
+                            cp_async16_if(((rb & ~wrapc) >> cc) & 1u,
+                                          &st.src[mo + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
                         }
-                        __syncwarp();  // row table and member list ordered before lane 0's release
+                        if (wrapc) {  // wrapped columns: every element by lookup
+                            for (uint32_t wm = wrapc; wm; wm &= wm - 1) {
+                                const int cc = __ffs(wm) - 1;
+                                const uint64_t cs = addmod(j0, mulmod_shoup(i0 + cc, p.m, p.m_sh, p.N), p.N);
+                                const uint64_t src = cs + lane >= p.N ? cs + lane - p.N : cs + lane;
+                                uint64_t rank;
+                                orb_lookup(p.orb, src, rank);
+                                if ((rb >> cc) & 1u)
+                                    cp_async16(&st.src[mo + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < kRows / Cfg::kPW; ++k) {  // direct: row pw + 4k, column `lane`
+                            const int rr = pw + Cfg::kPW * k;
+                            const uint32_t rbr = __shfl_sync(0xffffffffu, rb, rr);
+                            const uint32_t offr = __shfl_sync(0xffffffffu, off, rr);
+                            const uint32_t below = __popc(rbr & lt_lane);
+                            cp_async16_if((rbr >> lane) & 1u, &st.dst[M + offr + below], Xs + (E.rrank[rr] + below));
+                        }
+                        if (pw == 0) {
+                            st.rbits[j][lane] = rb;
+                            st.rrank[j][lane] = E.rrank[lane];
+                            st.roff[j][lane] = static_cast<uint16_t>(off);
+                            if (lane == 0) st.moff[j] = static_cast<uint16_t>(M);
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&sm.planempty[ps]);
+                        if (issuer) issue();
+                        ++gc;
+                        M += Mn;
+                        ++j;
+                        ++n;
+                    }
+                    if (pw == 0 && lane == 0) {
+                        st.nsub = static_cast<uint16_t>(j);
+                        st.moff[j] = static_cast<uint16_t>(M);
+                        st.last = (wk.last() && n == nch) ? 1u : 0u;
+                    }
+                    cp_async_arrive(&sm.full[stage]);
+                    if (pw == 0) {
+                        __syncwarp();  // slot tables ordered before lane 0's release
                         if (lane == 0) mbar_arrive(&sm.full[stage]);
                     }
                     if (++stage == kStages) {
@@ -777,32 +797,57 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
         for (int q = 0; q < kRowsPerConsumer; ++q) carry[q] = make_double2(0.0, 0.0);
         bool more = true;  // every CTA has >= 1 item, every item >= 1 chunk
         while (more) {
-            mbar_wait(&sm.full[stage], phase);
-            TileStage& st = sm.stage[stage];
+            if constexpr (kOrb) {
+                // one warp polls the slot's barrier, the others sleep on a named
+                // barrier (14 spinning warps took issue slots from the producers)
+                if (warp == 0) mbar_wait(&sm.full[stage], phase);
+                named_sync(kConsumerBar, kConsumers);
+            } else {
+                mbar_wait(&sm.full[stage], phase);
+            }
+            auto& st = sm.stage[stage];
             const uint32_t i0 = static_cast<uint32_t>(st.i0);
             const uint32_t pos = i0 + c;
             more = st.last == 0;
+            if constexpr (kOrb) {
+                // the slot's sub-chunks: one norm tile each; a member e of sub-chunk
+                // j is row r (the last with roff <= e - moff) and the (e - moff -
+                // roff)-th member column of that row
+                const int nsub = st.nsub;
+                for (int j = 0; j < nsub; ++j, ++k) {
+                    const int b = static_cast<int>(k % kNormBufs);
+                    if (k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
+                    const uint32_t m0 = st.moff[j], m1 = st.moff[j + 1];
+                    for (uint32_t e = m0 + tid; e < m1; e += kConsumers) {
+                        const uint32_t kk = e - m0;
+                        int r = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1)
+                            if (st.roff[j][r + step] <= kk) r += step;
+                        const uint32_t nin = kk - st.roff[j][r];
+                        const int cc = static_cast<int>(__fns(st.rbits[j][r], 0, static_cast<int>(nin) + 1));
+                        double h0r, h0i, h1r, h1i;
+                        stage_pair(sc, st.dst[e], st.src[e], h0r, h0i, h1r, h1i);
+                        sm.nrm[b][0][r][cc] = cnorm(h0r, h0i);
+                        sm.nrm[b][1][r][cc] = cnorm(h1r, h1i);
+                        if (p.write) {  // both groups at the member's rank
+                            const uint64_t at = st.rrank[j][r] + nin;
+                            p.Y[at] = make_double2(h0r, h0i);
+                            p.Y1[at] = make_double2(h1r, h1i);
+                        }
+                    }
+                    if (tid < kRows) sm.nrm_bits[b][tid] = st.rbits[j][tid];
+                    named_arrive(kNormFull0 + b, kNormSync);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[stage]);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            } else {
             const int b = static_cast<int>(k % kNormBufs);
             if (kProbs && k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
-            if constexpr (kOrb) {
-                // only the chunk's members (about half of its 1024 positions): the
-                // e-th in row-major order; the chains skip the other positions
-                const uint32_t M = sm.row_off[stage][kRows];
-                for (uint32_t e = tid; e < M; e += kConsumers) {
-                    const uint32_t rc = sm.memb[stage][e];
-                    const int r = static_cast<int>(rc >> 5), cc = static_cast<int>(rc & 31);
-                    double h0r, h0i, h1r, h1i;
-                    stage_pair(sc, st.dst[r][cc], st.src[cc][r], h0r, h0i, h1r, h1i);
-                    sm.nrm[b][0][r][cc] = cnorm(h0r, h0i);
-                    sm.nrm[b][1][r][cc] = cnorm(h1r, h1i);
-                    if (p.write) {  // both groups at the member's rank
-                        const uint64_t at = sm.row_rank[stage][r] + (e - sm.row_off[stage][r]);
-                        p.Y[at] = make_double2(h0r, h0i);
-                        p.Y1[at] = make_double2(h1r, h1i);
-                    }
-                }
-                if (tid < kRows) sm.nrm_bits[b][tid] = sm.row_bits[stage][tid];
-            } else
 #pragma unroll
             for (int q = 0; q < kRowsPerConsumer; ++q) {
                 const int r = rg * kRowsPerConsumer + q;
@@ -857,6 +902,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 stage = 0;
                 phase ^= 1;
             }
+            }  // dense slot
         }
         if (kProbs) {  // match the chain's releases of the last kNormBufs norm tiles
             for (uint64_t q = (k > kNormBufs ? k - kNormBufs : 0); q < k; ++q)
@@ -1042,6 +1088,44 @@ static __global__ void __launch_bounds__(32 * kFixWarps, 2) k_tile_fixup(TilePar
     window_flush(win, digits[g]);
     __syncthreads();
     write_partials(digits, slots + uint64_t(blockIdx.x) * 2 * kDigits, tid);
+}
+
+// Per-stage pre-pass of the orbit variant: the OrbPlan of band b, sub-chunk n
+// (one warp each, lane = column run / row) into plan[band_off[b] + n].
+__device__ __forceinline__ void orb_window(const ulonglong2* __restrict__ rec, uint64_t s,
+                                           uint32_t& bits, uint64_t& rank) {
+    const ulonglong2 R0 = __ldg(rec + (s >> 6)), R1 = __ldg(rec + (s >> 6) + 1);
+    const unsigned o = static_cast<unsigned>(s & 63);
+    bits = static_cast<uint32_t>(o ? (R0.x >> o) | (R1.x << (64 - o)) : R0.x);
+    rank = R0.y + __popcll(R0.x & lowmask64(o));
+}
+
+static __global__ void __launch_bounds__(256) k_orb_plan(TileParams p, uint64_t nch_max,
+                                                         const uint32_t* __restrict__ band_off,
+                                                         OrbPlan* __restrict__ plan) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x / 32) + threadIdx.x / 32; w < p.ntiles * nch_max;
+         w += nwarps) {
+        const uint64_t b = w / nch_max, n = w - b * nch_max;
+        if (n >= band_off[b + 1] - band_off[b]) continue;  // warp-uniform
+        const uint64_t j0 = b * kRows, i0 = n * kCols, j = j0 + lane;
+        const uint64_t len = tile_row_len(j, p);
+        const uint64_t cs = addmod(j0, mulmod_shoup(i0 + lane, p.m, p.m_sh, p.N), p.N);
+        uint32_t cb, rb = 0;
+        uint64_t cr, rr = 0;
+        orb_window(p.orb, cs, cb, cr);
+        if (cs + (kRows - 1) >= p.N) cr |= kOrbWrap;
+        if (i0 < len) {
+            orb_window(p.orb, mulmod_shoup(j, p.A, p.A_sh, p.N) + i0, rb, rr);
+            if (len - i0 < kCols) rb &= (1u << (len - i0)) - 1u;
+        }
+        OrbPlan& e = plan[band_off[b] + n];
+        e.crank[lane] = cr;
+        e.rrank[lane] = rr;
+        e.cbits[lane] = cb;
+        e.rbits[lane] = rb;
+    }
 }
 
 }  // namespace shs
