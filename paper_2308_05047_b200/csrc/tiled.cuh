@@ -86,11 +86,18 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #endif
 // The orbit variant (kOrb) runs 14 consumer warps (members only, each found by a
 // search of its slot's row offsets).
+#ifndef SHS_ORB_PRODUCER_WARPS
+#define SHS_ORB_PRODUCER_WARPS 8
+#endif
+#ifndef SHS_ORB_CONSUMER_WARPS
+#define SHS_ORB_CONSUMER_WARPS (18 - SHS_ORB_PRODUCER_WARPS)
+#endif
 template <bool kSplit, bool kOrb = false>
 struct TileCfg {
-    static constexpr int kCW = kOrb ? 14 : kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
+    static constexpr int kCW = kOrb ? SHS_ORB_CONSUMER_WARPS : kSplit ? kConsumerWarps : SHS_RR_CONSUMER_WARPS;
     static constexpr int kCons = 32 * kCW;
-    static constexpr int kPW = kProducerWarps;              // producer warps
+    static constexpr int kPW = kOrb ? SHS_ORB_PRODUCER_WARPS : kProducerWarps;  // producer warps
+    static_assert(kRows % kPW == 0 && kCols % kPW == 0, "producer warps split the rows / columns");
     static constexpr int kProds = 32 * kPW;
     static constexpr int kCopies = kRows * kCols / kProds;  // copies per side per producer
     static constexpr int kColStep = kProds / kRows;         // columns between a thread's copies
@@ -172,6 +179,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
@@ -248,20 +259,31 @@ struct OrbPlan {
     uint32_t cbits[kCols];  // membership of the run's kRows sources
     uint32_t rbits[kRows];  // membership of the row's kCols indices (0 past the row's end)
 };
-constexpr int kOrbCap = 1088;
+constexpr int kOrbCap = 1088;  // members per slot: a compact norm tile per group fills a dense one
+static_assert(kOrbCap == kRows * kNrmStride, "compact norm tile = dense norm tile");
 constexpr int kOrbSub = 4;
 constexpr int kOrbPlanRing = 8;
 constexpr uint64_t kOrbWrap = 1ull << 63;
 
+// A slot: the members of nsub consecutive sub-chunks of one band, row-major over
+// the slot's columns (row r's members, all its sub-chunks, in z order, are
+// rank-contiguous), so the consumers store them as runs and the chains fold them
+// from a compact norm tile.
 struct __align__(16) OrbSlot {
-    double2 src[kOrbCap];  // gathered values of the slot's members (member order)
-    double2 dst[kOrbCap];  // direct values
-    uint64_t rrank[kOrbSub][kRows];
-    uint32_t rbits[kOrbSub][kRows];
-    uint16_t roff[kOrbSub][kRows];  // row r's first member within sub-chunk j
-    uint16_t moff[kOrbSub + 1];     // sub-chunk j's first member in the slot
+    double2 src[kOrbCap];            // gathered values of the slot's members (member order)
+    double2 dst[kOrbCap];            // direct values
+    uint64_t rrank[kRows];           // rank of row r's first position in the slot
+    uint32_t rbits[kOrbSub][kRows];  // row r's members among sub-chunk j's 32 columns
+    uint16_t soff[kRows + 1];        // row r's first member in the slot; soff[32] = members
     uint16_t nsub;
-    uint32_t i0, last;              // (i0 unused: kept for the shared consumer prologue)
+    uint32_t i0, last;               // (i0: band column of the slot's first sub-chunk)
+};
+// what the chains need of a slot, kept with its norm tile (the slot itself is
+// recycled as soon as the consumers are done)
+struct OrbMeta {
+    uint32_t rbits[kOrbSub][kRows];
+    uint16_t soff[kRows];
+    uint16_t nsub;
 };
 
 template <bool kProbs, bool kOrb = false>
@@ -271,7 +293,7 @@ struct TileSmem {
     uint64_t full[kStages], empty[kStages];
     unsigned long long digits[2][kDigits];
     uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
-    uint32_t nrm_bits[kOrb ? kNormBufs : 1][kRows];  // orbit: members of each norm tile row
+    OrbMeta meta[kOrb ? kNormBufs : 1];  // orbit: the slot of each norm tile
     uint64_t planfull[kOrb ? kOrbPlanRing : 1], planempty[kOrb ? kOrbPlanRing : 1];
     OrbPlan plan[kOrb ? kOrbPlanRing : 1];
 };
@@ -591,6 +613,11 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             const bool issuer = pw == 0 && lane == 0;
             const double2* Xs = (p.prev ? p.prev->sel : p.prev_sel) ? p.X1 : p.X;
             const uint32_t lt_lane = (1u << lane) - 1u;
+            constexpr uint32_t kOrbWarpCols = [] {  // columns 0, kPW, 2 kPW, ...
+                uint32_t m = 0;
+                for (int c = 0; c < kCols; c += Cfg::kPW) m |= 1u << c;
+                return m;
+            }();
             uint64_t gc = 0;  // plan entries consumed
             // issuer walk: band index ik of the CTA's band sequence, sub-chunk in of in_n
             uint64_t gi = 0, ik = 0, in = 0, in_n = 0, iband = ~0ull;
@@ -635,34 +662,69 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 while (n < nch) {
                     mbar_wait(&sm.empty[stage], phase ^ 1);
                     OrbSlot& st = sm.stage[stage];
+                    // pass 1: how many sub-chunks fit (identical in every warp)
+                    uint32_t rbj[kOrbSub], cntj[kOrbSub];
+                    int K = 0;
                     uint32_t M = 0;
-                    int j = 0;
-                    while (j < kOrbSub && n < nch) {
-                        const int ps = static_cast<int>(gc % kOrbPlanRing);
-                        mbar_wait(&sm.planfull[ps], static_cast<uint32_t>((gc / kOrbPlanRing) & 1));
-                        const OrbPlan& E = sm.plan[ps];
-                        const uint32_t rb = E.rbits[lane];  // row `lane`
-                        const uint32_t cnt = __popc(rb);
-                        uint32_t incl = cnt;
+                    bool stop = false;
 #pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += v;
+                    for (int jj = 0; jj < kOrbSub; ++jj) {
+                        rbj[jj] = cntj[jj] = 0;
+                        if (!stop && n + jj < nch) {
+                            const uint64_t g = gc + jj;
+                            const int ps = static_cast<int>(g % kOrbPlanRing);
+                            mbar_wait(&sm.planfull[ps], static_cast<uint32_t>((g / kOrbPlanRing) & 1));
+                            const uint32_t rb = sm.plan[ps].rbits[lane];  // row `lane`
+                            const uint32_t c = __popc(rb);
+                            const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
+                            if (jj > 0 && M + tot > kOrbCap) {
+                                stop = true;
+                            } else {
+                                rbj[jj] = rb;
+                                cntj[jj] = c;
+                                M += tot;
+                                K = jj + 1;
+                            }
                         }
-                        const uint32_t off = incl - cnt;
-                        const uint32_t Mn = __shfl_sync(0xffffffffu, incl, 31);
-                        if (j > 0 && M + Mn > kOrbCap) break;  // the next slot starts with it
-                        const uint64_t i0 = n * kCols;
-                        // column runs wrapping past N - 1 (rare): this warp's columns, lane bits
-                        const uint32_t wrapc = __ballot_sync(0xffffffffu, (E.crank[lane] & kOrbWrap) != 0) &
-                                               (0x11111111u << pw);
-                        const uint32_t mo = M + off;
+                    }
+                    // row offsets over the slot: row-major, all sub-chunks of a row together
+                    uint32_t rowc = 0;
 #pragma unroll
-                        for (int k = 0; k < kCols / Cfg::kPW; ++k) {  // gathered: column pw + 4k, row `lane`
+                    for (int jj = 0; jj < kOrbSub; ++jj) rowc += cntj[jj];
+                    uint32_t incl = rowc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    uint32_t base = incl - rowc;  // this row's next member slot index
+                    // (one bulk copy per row for the direct side measured slower:
+                    // 13.1 vs 11.8 ms at n30, TMA-issue bound)
+                    // pass 2: copies, sub-chunk by sub-chunk
+#pragma unroll
+                    for (int jj = 0; jj < kOrbSub; ++jj) {
+                        if (jj >= K) break;
+                        const uint64_t g = gc + jj;
+                        const int ps = static_cast<int>(g % kOrbPlanRing);
+                        const OrbPlan& E = sm.plan[ps];
+                        const uint32_t rb = rbj[jj];
+                        const uint64_t i0 = (n + jj) * kCols;
+                        const uint32_t wrapc = __ballot_sync(0xffffffffu, (E.crank[lane] & kOrbWrap) != 0) &
+                                               (kOrbWarpCols << pw);
+#pragma unroll
+                        for (int k = 0; k < kCols / Cfg::kPW; ++k) {  // gathered: column pw + kPW k, row `lane`
                             const int cc = pw + Cfg::kPW * k;
                             const uint64_t rank = (E.crank[cc] & ~kOrbWrap) + __popc(E.cbits[cc] & lt_lane);
                             cp_async16_if(((rb & ~wrapc) >> cc) & 1u,
-                                          &st.src[mo + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
+                                          &st.src[base + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
+                        }
+#pragma unroll
+                        for (int k = 0; k < kRows / Cfg::kPW; ++k) {  // direct: row pw + kPW k, column `lane`
+                            const int rr = pw + Cfg::kPW * k;
+                            const uint32_t rbr = __shfl_sync(0xffffffffu, rb, rr);
+                            const uint32_t br = __shfl_sync(0xffffffffu, base, rr);
+                            const uint32_t below = __popc(rbr & lt_lane);
+                            cp_async16_if((rbr >> lane) & 1u, &st.dst[br + below], Xs + (E.rrank[rr] + below));
                         }
                         if (wrapc) {  // wrapped columns: every element by lookup
                             for (uint32_t wm = wrapc; wm; wm &= wm - 1) {
@@ -672,36 +734,29 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                                 uint64_t rank;
                                 orb_lookup(p.orb, src, rank);
                                 if ((rb >> cc) & 1u)
-                                    cp_async16(&st.src[mo + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
+                                    cp_async16(&st.src[base + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
                             }
                         }
-#pragma unroll
-                        for (int k = 0; k < kRows / Cfg::kPW; ++k) {  // direct: row pw + 4k, column `lane`
-                            const int rr = pw + Cfg::kPW * k;
-                            const uint32_t rbr = __shfl_sync(0xffffffffu, rb, rr);
-                            const uint32_t offr = __shfl_sync(0xffffffffu, off, rr);
-                            const uint32_t below = __popc(rbr & lt_lane);
-                            cp_async16_if((rbr >> lane) & 1u, &st.dst[M + offr + below], Xs + (E.rrank[rr] + below));
-                        }
                         if (pw == 0) {
-                            st.rbits[j][lane] = rb;
-                            st.rrank[j][lane] = E.rrank[lane];
-                            st.roff[j][lane] = static_cast<uint16_t>(off);
-                            if (lane == 0) st.moff[j] = static_cast<uint16_t>(M);
+                            st.rbits[jj][lane] = rb;
+                            if (jj == 0) st.rrank[lane] = E.rrank[lane];
                         }
+                        base += cntj[jj];
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&sm.planempty[ps]);
                         if (issuer) issue();
-                        ++gc;
-                        M += Mn;
-                        ++j;
-                        ++n;
                     }
-                    if (pw == 0 && lane == 0) {
-                        st.nsub = static_cast<uint16_t>(j);
-                        st.moff[j] = static_cast<uint16_t>(M);
-                        st.last = (wk.last() && n == nch) ? 1u : 0u;
+                    if (pw == 0) {
+                        st.soff[lane] = static_cast<uint16_t>(incl - rowc);
+                        if (lane == 31) st.soff[kRows] = static_cast<uint16_t>(incl);
+                        if (lane == 0) {
+                            st.nsub = static_cast<uint16_t>(K);
+                            st.i0 = static_cast<uint32_t>(n * kCols);
+                        }
                     }
+                    gc += K;
+                    n += K;
+                    if (pw == 0 && lane == 0) st.last = (wk.last() && n == nch) ? 1u : 0u;
                     cp_async_arrive(&sm.full[stage]);
                     if (pw == 0) {
                         __syncwarp();  // slot tables ordered before lane 0's release
@@ -810,35 +865,37 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             const uint32_t pos = i0 + c;
             more = st.last == 0;
             if constexpr (kOrb) {
-                // the slot's sub-chunks: one norm tile each; a member e of sub-chunk
-                // j is row r (the last with roff <= e - moff) and the (e - moff -
-                // roff)-th member column of that row
-                const int nsub = st.nsub;
-                for (int j = 0; j < nsub; ++j, ++k) {
-                    const int b = static_cast<int>(k % kNormBufs);
-                    if (k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
-                    const uint32_t m0 = st.moff[j], m1 = st.moff[j + 1];
-                    for (uint32_t e = m0 + tid; e < m1; e += kConsumers) {
-                        const uint32_t kk = e - m0;
-                        int r = 0;
+                // the slot's members -> one compact norm tile (member order) and
+                // both groups' stores; member e is row r, the last with soff <= e
+                const int b = static_cast<int>(k % kNormBufs);
+                if (k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
+                const uint32_t M = st.soff[kRows];
+                double* n0 = &sm.nrm[b][0][0][0];
+                double* n1 = &sm.nrm[b][1][0][0];
+                for (uint32_t e = tid; e < M; e += kConsumers) {
+                    int r = 0;
 #pragma unroll
-                        for (int step = 16; step > 0; step >>= 1)
-                            if (st.roff[j][r + step] <= kk) r += step;
-                        const uint32_t nin = kk - st.roff[j][r];
-                        const int cc = static_cast<int>(__fns(st.rbits[j][r], 0, static_cast<int>(nin) + 1));
-                        double h0r, h0i, h1r, h1i;
-                        stage_pair(sc, st.dst[e], st.src[e], h0r, h0i, h1r, h1i);
-                        sm.nrm[b][0][r][cc] = cnorm(h0r, h0i);
-                        sm.nrm[b][1][r][cc] = cnorm(h1r, h1i);
-                        if (p.write) {  // both groups at the member's rank
-                            const uint64_t at = st.rrank[j][r] + nin;
-                            p.Y[at] = make_double2(h0r, h0i);
-                            p.Y1[at] = make_double2(h1r, h1i);
-                        }
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (st.soff[r + step] <= e) r += step;
+                    double h0r, h0i, h1r, h1i;
+                    stage_pair(sc, st.dst[e], st.src[e], h0r, h0i, h1r, h1i);
+                    n0[e] = cnorm(h0r, h0i);
+                    n1[e] = cnorm(h1r, h1i);
+                    if (p.write) {  // both groups at the member's rank
+                        const uint64_t at = st.rrank[r] + (e - st.soff[r]);
+                        p.Y[at] = make_double2(h0r, h0i);
+                        p.Y1[at] = make_double2(h1r, h1i);
                     }
-                    if (tid < kRows) sm.nrm_bits[b][tid] = st.rbits[j][tid];
-                    named_arrive(kNormFull0 + b, kNormSync);
                 }
+                const int K = st.nsub;
+                if (tid < kRows) {
+                    OrbMeta& mt = sm.meta[b];
+                    mt.soff[tid] = st.soff[tid];
+                    for (int j = 0; j < K; ++j) mt.rbits[j][tid] = st.rbits[j][tid];
+                    if (tid == 0) mt.nsub = static_cast<uint16_t>(K);
+                }
+                named_arrive(kNormFull0 + b, kNormSync);
+                ++k;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[stage]);
                 if (++stage == kStages) {
@@ -929,13 +986,52 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             const uint64_t c_head = (256 - (c_z & 255)) & 255;
             const uint64_t c_fast = c_lo > c_head ? c_lo : c_head;
             double c_s = 0.0;
+            if constexpr (kOrb) {
+                // Orbit variant: per slot, this row's members (compact, in z order)
+                // sub-chunk by sub-chunk; positions off the orbit add +0.0 in the
+                // reference, so skipping them leaves every fold unchanged. The head
+                // positions (k_tile_fixup) are stored with zeros off the orbit.
+                const uint64_t nch = (tend + kCols - 1) / kCols;
+                for (uint64_t n = 0; n < nch; ++k) {
+                    const int b = static_cast<int>(k % kNormBufs);
+                    named_sync(kNormFull0 + b, kNormSync);
+                    const OrbMeta& mt = sm.meta[b];
+                    const int K = mt.nsub;
+                    const double* nv = &sm.nrm[b][cg][0][0];
+                    uint32_t e = mt.soff[cr];
+                    for (int j = 0; j < K; ++j) {
+                        const uint64_t i0 = (n + j) * kCols;
+                        if (i0 >= c_len) break;
+                        uint32_t bits = mt.rbits[j][cr];
+                        const int end = static_cast<int>(min(c_len - i0, uint64_t(kCols)));
+                        int start = 0;
+                        if (i0 < c_head) {
+                            const int qh = static_cast<int>(min(c_head - i0, uint64_t(end)));
+                            double* head = p.head + ((j0 + cr) * 2 + cg) * 256 + i0;
+                            for (int cc = 0; cc < qh; ++cc) head[cc] = ((bits >> cc) & 1u) ? nv[e++] : 0.0;
+                            start = qh;
+                            bits &= qh >= 32 ? 0u : ~((1u << qh) - 1u);
+                        }
+                        const int qb = static_cast<int>(255 - ((c_z + i0) & 255));
+                        if (qb >= start && qb < end) {  // a block ends at column qb
+                            uint32_t lo = bits & (qb >= 31 ? ~0u : ((2u << qb) - 1u));
+                            bits &= ~lo;
+                            for (; lo; lo &= lo - 1) c_s = __dadd_rn(c_s, nv[e++]);
+                            p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = c_s;
+                            window_add(win, c_s, sm.digits[cg]);
+                            c_s = 0.0;
+                        }
+                        for (; bits; bits &= bits - 1) c_s = __dadd_rn(c_s, nv[e++]);
+                    }
+                    n += K;
+                    __syncwarp();
+                    named_arrive(kNormEmpty0 + b, kNormSync);
+                }
+            } else
             for (uint64_t i0 = lo_col; i0 < iend; i0 += kCols, ++k) {
                 const int b = static_cast<int>(k % kNormBufs);
                 named_sync(kNormFull0 + b, kNormSync);
                 const double* row = &sm.nrm[b][cg][cr][0];
-                // orbit variant: positions off the orbit hold stale norms, read as +0.0
-                const uint32_t mb = kOrb ? sm.nrm_bits[kOrb ? b : 0][cr] : ~0u;
-                auto nv = [&](int cc) { return ((mb >> cc) & 1u) ? row[cc] : 0.0; };
                 if (i0 >= c_fast && i0 + kCols <= c_hi) {
                     // interior chunk (the common case): 64 in-order adds, branch-free.
                     // At most one block ends inside the chunk (kCols <= 256), at
@@ -947,11 +1043,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                     double a = c_s, nb = 0.0;
 #pragma unroll
                     for (int cc = 0; cc < kCols; cc += 2) {
-                        double2 x = *reinterpret_cast<const double2*>(row + cc);
-                        if (kOrb) {
-                            x.x = ((mb >> cc) & 1u) ? x.x : 0.0;
-                            x.y = ((mb >> (cc + 1)) & 1u) ? x.y : 0.0;
-                        }
+                        const double2 x = *reinterpret_cast<const double2*>(row + cc);
                         const bool lo0 = cc <= qb, lo1 = cc + 1 <= qb;
                         a = __dadd_rn(a, lo0 ? x.x : 0.0);
                         nb = __dadd_rn(nb, lo0 ? 0.0 : x.x);
@@ -973,19 +1065,19 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                     if (i0 + qa < c_head) {
                         const int qh = static_cast<int>(min(c_head - i0, uint64_t(q1)));
                         double* head = p.head + ((j0 + cr) * 2 + cg) * 256 + i0;
-                        for (int cc = qa; cc < qh; ++cc) head[cc] = nv(cc);
+                        for (int cc = qa; cc < qh; ++cc) head[cc] = row[cc];
                         qa = qh;
                     }
                     while (qa < q1) {
                         const int qb = qa + static_cast<int>(255 - ((c_z + i0 + qa) & 255));
                         if (qb < q1) {
-                            for (int cc = qa; cc <= qb; ++cc) c_s = __dadd_rn(c_s, nv(cc));
+                            for (int cc = qa; cc <= qb; ++cc) c_s = __dadd_rn(c_s, row[cc]);
                             p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = c_s;
                             window_add(win, c_s, sm.digits[cg]);
                             c_s = 0.0;
                             qa = qb + 1;
                         } else {
-                            for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, nv(cc));
+                            for (int cc = qa; cc < q1; ++cc) c_s = __dadd_rn(c_s, row[cc]);
                             qa = q1;
                         }
                     }
