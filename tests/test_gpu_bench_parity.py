@@ -10,7 +10,8 @@ u64 index range just above 2^32 that config 5 depends on).
   (proj/src/statevector.cpp:32-40) and ``==`` the oracle's exact combine (the
   engine's AUTO mode above 1024 blocks).
 * Config 4 (N = 4294967213, t = 64, 2 x 68.7 GB): the dense round-robin tiled
-  kernels (k_tiled<., false>) under a seeded forced sequence, stages 0..22,
+  kernels (k_tiled<., false>; and the opt-in orbit-compressed stages,
+  k_tiled<true, false, true>) under a seeded forced sequence, stages 0..22,
   against the sparse-support oracle (oracle/shor_oracle.c so_sparse_*, itself
   pinned to the dense oracle in tests/test_oracle_pinned.py): p0/p1 ``==`` per
   stage (they sum every one of the 16.7 M block partials), every support
@@ -99,13 +100,17 @@ def test_c3_full_runs_vs_live_reference(cuda_ok, oracle, reference, a):
         gc.collect()
 
 
-def _forced_dense_vs_sparse_oracle(oracle, N, a, t, stages, err_name, seed=7, idx=3):
-    """Dense step API (tiled kernels) vs the sparse-support oracle on a seeded
-    forced sequence (the reference's own sampling decides every bit)."""
+def _forced_dense_vs_sparse_oracle(oracle, N, a, t, stages, err_name, seed=7, idx=3, orbit=False):
+    """Dense step API (tiled kernels; orbit=True: the orbit-compressed stages) vs the
+    sparse-support oracle on a seeded forced sequence (the reference's own sampling
+    decides every bit)."""
     err = ERRORS[err_name]
     oe = oracle_err(err)
     eng = _engine(N, a, t, err)
     eng.set_sparse(False)
+    eng.set_orbit(orbit)
+    if orbit:
+        assert eng.orbit_info()["stages"] > 0
     so = oracle.sparse(N, a, N.bit_length(), t, oe)
     rng = np.random.default_rng(N % 1000003)
     eng.state_init()
@@ -142,13 +147,14 @@ def _forced_dense_vs_sparse_oracle(oracle, N, a, t, stages, err_name, seed=7, id
 
 
 @pytest.mark.slow
-def test_c4_dense_stages_vs_sparse_support_oracle(cuda_ok, oracle):
+@pytest.mark.parametrize("orbit", [False, True])
+def test_c4_dense_stages_vs_sparse_support_oracle(cuda_ok, oracle, orbit):
     N, a, t = 4294967213, 5, 64
     eng = _engine(N, a, t, ERRORS["none"])
     plans = [eng.tile_plan(s) for s in range(1, 23)]
     eng.close()
     assert all(p["tiled"] for p in plans)  # the round-robin tiled kernels are what runs
-    kept = _forced_dense_vs_sparse_oracle(oracle, N, a, t, 23, "phase_init")
+    kept = _forced_dense_vs_sparse_oracle(oracle, N, a, t, 23, "phase_init", orbit=orbit)
     assert 0 < sum(kept) < len(kept)  # both collapse paths (speculative h0 and h1) ran
 
 
