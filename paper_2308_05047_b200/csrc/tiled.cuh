@@ -200,7 +200,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
                  : "memory");
 }
-// predicated 16-byte cp.async (no branch around it)
+// predicated 16-byte cp.async (no branch around it). No "memory" clobber: the
+// producers never read the slot they fill, and their barrier arrives order the
+// copies; without it the compiler can batch the plan reads ahead of the copies.
 __device__ __forceinline__ void cp_async16_if(bool pred, void* dst, const void* src) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(
@@ -301,8 +303,9 @@ struct TileSmem {
 static_assert(sizeof(TileSmem<true, true>) <= 232448, "orbit variant: shared memory per CTA");
 
 template <bool kProbs, bool kSplit, bool kOrb = false>
-constexpr int tile_threads() {
-    return 32 * (TileCfg<kSplit, kOrb>::kCW + TileCfg<kSplit, kOrb>::kPW + (kProbs ? kChainWarps : 0));
+constexpr int tile_threads() {  // (+ the orbit variant's plan warp)
+    return 32 * (TileCfg<kSplit, kOrb>::kCW + TileCfg<kSplit, kOrb>::kPW + (kProbs ? kChainWarps : 0) +
+                 (kOrb ? 1 : 0));
 }
 
 template <bool kProbs, bool kOrb = false>
@@ -607,10 +610,9 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             // row-major member order, each side from its rank. Warp w copies the
             // gathered columns w + 4k (lanes = rows) and the direct rows w + 4k
             // (lanes = columns). Every warp evaluates the same packing decision
-            // from the same plan; warp 0 also writes the slot's tables, and its
-            // lane 0 issues the plan prefetches.
+            // from the same plan; warp 0 also writes the slot's tables. The plan
+            // entries come from the plan warp (below).
             const int pw = warp - kProducerWarp;
-            const bool issuer = pw == 0 && lane == 0;
             const double2* Xs = (p.prev ? p.prev->sel : p.prev_sel) ? p.X1 : p.X;
             const uint32_t lt_lane = (1u << lane) - 1u;
             constexpr uint32_t kOrbWarpCols = [] {  // columns 0, kPW, 2 kPW, ...
@@ -619,41 +621,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 return m;
             }();
             uint64_t gc = 0;  // plan entries consumed
-            // issuer walk: band index ik of the CTA's band sequence, sub-chunk in of in_n
-            uint64_t gi = 0, ik = 0, in = 0, in_n = 0, iband = ~0ull;
-            bool idone = false;
-            auto band_nch = [&](uint64_t bb) {
-                uint64_t mx = 0;
-                for (int r = 0; r < kRows; ++r) {
-                    const uint64_t l = tile_row_len(bb * kRows + r, p);
-                    mx = l > mx ? l : mx;
-                }
-                return (mx + kCols - 1) / kCols;
-            };
-            auto issue = [&]() {  // the next plan entry, kOrbPlanRing - 1 ahead of the consumers
-                while (in == in_n) {
-                    if (idone) return;
-                    if (iband != ~0ull) ++ik;
-                    const uint64_t bb = ik == 0 ? blockIdx.x : sm.bandq[ik % kBandQ];
-                    if (bb >= p.ntiles) {
-                        idone = true;
-                        return;
-                    }
-                    iband = bb;
-                    in = 0;
-                    in_n = band_nch(bb);
-                }
-                const int ps = static_cast<int>(gi % kOrbPlanRing);
-                mbar_wait(&sm.planempty[ps], static_cast<uint32_t>((gi / kOrbPlanRing) & 1) ^ 1);
-                mbar_arrive_expect_tx(&sm.planfull[ps], sizeof(OrbPlan));
-                bulk_g2s(&sm.plan[ps], p.plan + (p.band_off[iband] + in), sizeof(OrbPlan),
-                         &sm.planfull[ps]);
-                ++in;
-                ++gi;
-            };
             for (CtaWork<kSplit> wk(p, sm.bandq, true, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
-                if (issuer && wk.k == 0)
-                    for (int q = 0; q < kOrbPlanRing - 1; ++q) issue();
                 const uint64_t j0 = wk.band() * kRows;
                 LaneRows lr;
                 const uint64_t tend = tile_rows_split(p, j0, lane, lr, 0, ~0ull);
@@ -711,20 +679,31 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         const uint64_t i0 = (n + jj) * kCols;
                         const uint32_t wrapc = __ballot_sync(0xffffffffu, (E.crank[lane] & kOrbWrap) != 0) &
                                                (kOrbWarpCols << pw);
+                        constexpr int kG = kCols / Cfg::kPW, kD = kRows / Cfg::kPW;
+                        uint64_t crk[kG], rrk[kD];
+                        uint32_t cbt[kG], rbr[kD], brr[kD];
 #pragma unroll
-                        for (int k = 0; k < kCols / Cfg::kPW; ++k) {  // gathered: column pw + kPW k, row `lane`
+                        for (int k = 0; k < kG; ++k) {  // this warp's plan fields first, all in flight
+                            crk[k] = E.crank[pw + Cfg::kPW * k];
+                            cbt[k] = E.cbits[pw + Cfg::kPW * k];
+                        }
+#pragma unroll
+                        for (int k = 0; k < kD; ++k) {
+                            rrk[k] = E.rrank[pw + Cfg::kPW * k];
+                            rbr[k] = __shfl_sync(0xffffffffu, rb, pw + Cfg::kPW * k);
+                            brr[k] = __shfl_sync(0xffffffffu, base, pw + Cfg::kPW * k);
+                        }
+#pragma unroll
+                        for (int k = 0; k < kG; ++k) {  // gathered: column pw + kPW k, row `lane`
                             const int cc = pw + Cfg::kPW * k;
-                            const uint64_t rank = (E.crank[cc] & ~kOrbWrap) + __popc(E.cbits[cc] & lt_lane);
+                            const uint64_t rank = (crk[k] & ~kOrbWrap) + __popc(cbt[k] & lt_lane);
                             cp_async16_if(((rb & ~wrapc) >> cc) & 1u,
                                           &st.src[base + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
                         }
 #pragma unroll
-                        for (int k = 0; k < kRows / Cfg::kPW; ++k) {  // direct: row pw + kPW k, column `lane`
-                            const int rr = pw + Cfg::kPW * k;
-                            const uint32_t rbr = __shfl_sync(0xffffffffu, rb, rr);
-                            const uint32_t br = __shfl_sync(0xffffffffu, base, rr);
-                            const uint32_t below = __popc(rbr & lt_lane);
-                            cp_async16_if((rbr >> lane) & 1u, &st.dst[br + below], Xs + (E.rrank[rr] + below));
+                        for (int k = 0; k < kD; ++k) {  // direct: row pw + kPW k, column `lane`
+                            const uint32_t below = __popc(rbr[k] & lt_lane);
+                            cp_async16_if((rbr[k] >> lane) & 1u, &st.dst[brr[k] + below], Xs + (rrk[k] + below));
                         }
                         if (wrapc) {  // wrapped columns: every element by lookup
                             for (uint32_t wm = wrapc; wm; wm &= wm - 1) {
@@ -744,7 +723,6 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         base += cntj[jj];
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&sm.planempty[ps]);
-                        if (issuer) issue();
                     }
                     if (pw == 0) {
                         st.soff[lane] = static_cast<uint16_t>(incl - rowc);
@@ -866,25 +844,25 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             more = st.last == 0;
             if constexpr (kOrb) {
                 // the slot's members -> one compact norm tile (member order) and
-                // both groups' stores; member e is row r, the last with soff <= e
+                // both groups' stores: warp w takes rows w, w + kCW, ...; lane i
+                // the row's members i, i + 32, ... (consecutive smem and ranks)
                 const int b = static_cast<int>(k % kNormBufs);
                 if (k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
-                const uint32_t M = st.soff[kRows];
                 double* n0 = &sm.nrm[b][0][0][0];
                 double* n1 = &sm.nrm[b][1][0][0];
-                for (uint32_t e = tid; e < M; e += kConsumers) {
-                    int r = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1)
-                        if (st.soff[r + step] <= e) r += step;
-                    double h0r, h0i, h1r, h1i;
-                    stage_pair(sc, st.dst[e], st.src[e], h0r, h0i, h1r, h1i);
-                    n0[e] = cnorm(h0r, h0i);
-                    n1[e] = cnorm(h1r, h1i);
-                    if (p.write) {  // both groups at the member's rank
-                        const uint64_t at = st.rrank[r] + (e - st.soff[r]);
-                        p.Y[at] = make_double2(h0r, h0i);
-                        p.Y1[at] = make_double2(h1r, h1i);
+                for (int r = warp; r < kRows; r += kConsumerWarps) {
+                    const uint32_t e0 = st.soff[r], e1 = st.soff[r + 1];
+                    const uint64_t rk = st.rrank[r];
+                    for (uint32_t e = e0 + lane; e < e1; e += 32) {
+                        double h0r, h0i, h1r, h1i;
+                        stage_pair(sc, st.dst[e], st.src[e], h0r, h0i, h1r, h1i);
+                        n0[e] = cnorm(h0r, h0i);
+                        n1[e] = cnorm(h1r, h1i);
+                        if (p.write) {  // both groups at the member's rank
+                            const uint64_t at = rk + (e - e0);
+                            p.Y[at] = make_double2(h0r, h0i);
+                            p.Y1[at] = make_double2(h1r, h1i);
+                        }
                     }
                 }
                 const int K = st.nsub;
@@ -965,6 +943,32 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             for (uint64_t q = (k > kNormBufs ? k - kNormBufs : 0); q < k; ++q)
                 named_sync(kNormEmpty0 + static_cast<int>(q % kNormBufs), kNormSync);
         }
+    } else if (kOrb && warp == kChainWarp + kChainWarps) {
+        // ------------------------------------------------------------ plan warp
+        // lane 0 walks the CTA's band sequence (band k from bandq, written by the
+        // first producer thread one band ahead) and prefetches every sub-chunk's
+        // OrbPlan into the ring as soon as its entry is free
+        if (lane == 0) {
+            uint64_t gi = 0;
+            for (uint64_t ik = 0;; ++ik) {
+                const uint64_t bb = ik == 0 ? blockIdx.x : sm.bandq[ik % kBandQ];
+                if (bb >= p.ntiles) break;
+                uint64_t mx = 0;
+                for (int r = 0; r < kRows; ++r) {
+                    const uint64_t l = tile_row_len(bb * kRows + r, p);
+                    mx = l > mx ? l : mx;
+                }
+                const uint64_t nch = (mx + kCols - 1) / kCols;
+                const OrbPlan* src = p.plan + p.band_off[bb];
+                for (uint64_t n = 0; n < nch; ++n, ++gi) {
+                    const int ps = static_cast<int>(gi % kOrbPlanRing);
+                    mbar_wait(&sm.planempty[ps], static_cast<uint32_t>((gi / kOrbPlanRing) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&sm.planfull[ps], sizeof(OrbPlan));
+                    bulk_g2s(&sm.plan[ps], src + n, sizeof(OrbPlan), &sm.planfull[ps]);
+                }
+            }
+        }
+        __syncwarp();
     } else if (kProbs && warp >= kChainWarp && warp < kChainWarp + kChainWarps) {
         // ------------------------------------------------------------ chains
         const int ct = tid - 32 * kChainWarp;  // one lane per (row, group)
