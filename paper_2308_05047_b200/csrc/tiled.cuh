@@ -86,6 +86,15 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #endif
 // The orbit variant (kOrb) runs 14 consumer warps (members only, each found by a
 // search of its slot's row offsets).
+#ifndef SHS_NORM_BUFS
+#define SHS_NORM_BUFS 4
+#endif
+#ifndef SHS_ORB_SLOTS
+#define SHS_ORB_SLOTS 5
+#endif
+#ifndef SHS_ORB_NORM_BUFS
+#define SHS_ORB_NORM_BUFS 2
+#endif
 #ifndef SHS_ORB_PRODUCER_WARPS
 #define SHS_ORB_PRODUCER_WARPS 8
 #endif
@@ -102,15 +111,16 @@ struct TileCfg {
     static constexpr int kCopies = kRows * kCols / kProds;  // copies per side per producer
     static constexpr int kColStep = kProds / kRows;         // columns between a thread's copies
     static constexpr int kRowStep = kProds / kCols;         // rows between a thread's copies
+    // orbit: 5 slots and 2 norm tiles (a compact norm tile holds a slot's norms;
+    // the slots are what keeps bytes in flight)
+    static constexpr int kST = kOrb ? SHS_ORB_SLOTS : kStages;
+    static constexpr int kNB = kOrb ? SHS_ORB_NORM_BUFS : SHS_NORM_BUFS;
     static constexpr int kProdWarp = kCW;                   // first producer warp
     static constexpr int kChainWarp0 = kCW + kPW;           // first chain warp (probs only)
     static constexpr int kRowsPerCons = kRows * kCols / kCons;
     static constexpr int kNSync = kCons + 32 * kChainWarps;   // norm named-barrier thread count
     static_assert(kCons % kCols == 0 && kRowsPerCons >= 1, "consumer layout");
 };
-#ifndef SHS_NORM_BUFS
-#define SHS_NORM_BUFS 4
-#endif
 constexpr int kNormBufs = SHS_NORM_BUFS;           // norm tiles in flight (chain slack)
 constexpr int kNormFull0 = 1, kNormEmpty0 = 1 + kNormBufs;  // named barrier ids
 constexpr int kNrmStride = kCols + 2;              // 16 B-aligned rows, conflict-free LDS.128
@@ -290,14 +300,16 @@ struct OrbMeta {
 
 template <bool kProbs, bool kOrb = false>
 struct TileSmem {
-    std::conditional_t<kOrb, OrbSlot, TileStage> stage[kStages];
-    double nrm[kProbs ? kNormBufs : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
-    uint64_t full[kStages], empty[kStages];
+    static constexpr int kST = kOrb ? SHS_ORB_SLOTS : kStages;
+    static constexpr int kNB = kOrb ? SHS_ORB_NORM_BUFS : kNormBufs;
+    std::conditional_t<kOrb, OrbSlot, TileStage> stage[kST];
+    double nrm[kProbs ? kNB : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
+    uint64_t full[kST], empty[kST];
     unsigned long long digits[2][kDigits];
     uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
-    OrbMeta meta[kOrb ? kNormBufs : 1];  // orbit: the slot of each norm tile
+    OrbMeta meta[kOrb ? kNB : 1];  // orbit: the slot of each norm tile
     uint64_t planfull[kOrb ? kOrbPlanRing : 1], planempty[kOrb ? kOrbPlanRing : 1];
-    OrbPlan plan[kOrb ? kOrbPlanRing : 1];
+    alignas(128) OrbPlan plan[kOrb ? kOrbPlanRing : 1];  // bulk-copy destinations: 16 B aligned at least
 };
 
 static_assert(sizeof(TileSmem<true, true>) <= 232448, "orbit variant: shared memory per CTA");
@@ -554,6 +566,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     using Cfg = TileCfg<kSplit, kOrb>;
+    constexpr int kStages = Cfg::kST, kNormBufs = Cfg::kNB;
     constexpr int kConsumerWarps = Cfg::kCW, kConsumers = Cfg::kCons;
     constexpr int kProducerWarp = Cfg::kProdWarp, kChainWarp = Cfg::kChainWarp0;
     constexpr int kRowsPerConsumer = Cfg::kRowsPerCons, kNormSync = Cfg::kNSync;
@@ -1003,6 +1016,18 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                     const int K = mt.nsub;
                     const double* nv = &sm.nrm[b][cg][0][0];
                     uint32_t e = mt.soff[cr];
+                    // fold the next cnt members in order, 8 loads in flight at a time
+                    // (padding adds +0.0, which leaves the non-negative sum unchanged)
+                    auto fold = [&](uint32_t cnt) {
+                        for (uint32_t t = 0; t < cnt; t += 8) {
+                            double v[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) v[u] = t + u < cnt ? nv[e + t + u] : 0.0;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) c_s = __dadd_rn(c_s, v[u]);
+                        }
+                        e += cnt;
+                    };
                     for (int j = 0; j < K; ++j) {
                         const uint64_t i0 = (n + j) * kCols;
                         if (i0 >= c_len) break;
@@ -1018,14 +1043,14 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         }
                         const int qb = static_cast<int>(255 - ((c_z + i0) & 255));
                         if (qb >= start && qb < end) {  // a block ends at column qb
-                            uint32_t lo = bits & (qb >= 31 ? ~0u : ((2u << qb) - 1u));
+                            const uint32_t lo = bits & (qb >= 31 ? ~0u : ((2u << qb) - 1u));
                             bits &= ~lo;
-                            for (; lo; lo &= lo - 1) c_s = __dadd_rn(c_s, nv[e++]);
+                            fold(__popc(lo));
                             p.S[cg * p.nb + ((c_z + i0 + qb) >> 8)] = c_s;
                             window_add(win, c_s, sm.digits[cg]);
                             c_s = 0.0;
                         }
-                        for (; bits; bits &= bits - 1) c_s = __dadd_rn(c_s, nv[e++]);
+                        fold(__popc(bits));
                     }
                     n += K;
                     __syncwarp();
