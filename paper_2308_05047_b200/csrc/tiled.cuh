@@ -217,8 +217,7 @@ __device__ __forceinline__ void cp_async16_if(bool pred, void* dst, const void* 
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(
             smem_addr(dst)),
-        "l"(src), "r"(static_cast<uint32_t>(pred))
-        : "memory");
+        "l"(src), "r"(static_cast<uint32_t>(pred)));
 }
 // 1-D bulk copy global -> shared (TMA), completing `bytes` on bar's transaction count
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -271,6 +270,7 @@ struct OrbPlan {
     uint32_t cbits[kCols];  // membership of the run's kRows sources
     uint32_t rbits[kRows];  // membership of the row's kCols indices (0 past the row's end)
 };
+constexpr int kOrbGroups = 2;  // producer groups filling alternate slots
 constexpr int kOrbCap = 1088;  // members per slot: a compact norm tile per group fills a dense one
 static_assert(kOrbCap == kRows * kNrmStride, "compact norm tile = dense norm tile");
 constexpr int kOrbSub = 4;
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             // copies of every producer + header
-            mbar_init(&sm.full[s], Cfg::kProds + 1);
+            mbar_init(&sm.full[s], Cfg::kProds / (kOrb ? kOrbGroups : 1) + 1);
             mbar_init(&sm.empty[s], kConsumerWarps);
         }
         if constexpr (kOrb)
@@ -625,14 +625,21 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             // (lanes = columns). Every warp evaluates the same packing decision
             // from the same plan; warp 0 also writes the slot's tables. The plan
             // entries come from the plan warp (below).
-            const int pw = warp - kProducerWarp;
+            // The producer warps form kOrbGroups groups that fill alternate slots
+            // (a slot's copies are a long dependent chain per warp: one group at a
+            // time left the slot period set by it); every group evaluates every
+            // slot's packing, so all agree on where each slot starts.
+            constexpr int kGW = Cfg::kPW / kOrbGroups;  // warps per group
+            const int grp = (warp - kProducerWarp) / kGW;
+            const int pw = (warp - kProducerWarp) % kGW;  // warp within the group
             const double2* Xs = (p.prev ? p.prev->sel : p.prev_sel) ? p.X1 : p.X;
             const uint32_t lt_lane = (1u << lane) - 1u;
-            constexpr uint32_t kOrbWarpCols = [] {  // columns 0, kPW, 2 kPW, ...
+            constexpr uint32_t kOrbWarpCols = [] {  // columns 0, kGW, 2 kGW, ...
                 uint32_t m = 0;
-                for (int c = 0; c < kCols; c += Cfg::kPW) m |= 1u << c;
+                for (int c = 0; c < kCols; c += kGW) m |= 1u << c;
                 return m;
             }();
+            uint64_t qs = 0;  // slots of this CTA so far (slot qs goes to group qs % kOrbGroups)
             uint64_t gc = 0;  // plan entries consumed
             for (CtaWork<kSplit> wk(p, sm.bandq, true, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
                 const uint64_t j0 = wk.band() * kRows;
@@ -641,7 +648,8 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 const uint64_t nch = (tend + kCols - 1) / kCols;
                 uint64_t n = 0;
                 while (n < nch) {
-                    mbar_wait(&sm.empty[stage], phase ^ 1);
+                    const bool mine = static_cast<int>(qs % kOrbGroups) == grp;
+                    if (mine) mbar_wait(&sm.empty[stage], phase ^ 1);
                     OrbSlot& st = sm.stage[stage];
                     // pass 1: how many sub-chunks fit (identical in every warp)
                     uint32_t rbj[kOrbSub], cntj[kOrbSub];
@@ -687,36 +695,31 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         if (jj >= K) break;
                         const uint64_t g = gc + jj;
                         const int ps = static_cast<int>(g % kOrbPlanRing);
+                        if (!mine) {  // the other group's slot: release the entry only
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&sm.planempty[ps]);
+                            continue;
+                        }
                         const OrbPlan& E = sm.plan[ps];
                         const uint32_t rb = rbj[jj];
                         const uint64_t i0 = (n + jj) * kCols;
                         const uint32_t wrapc = __ballot_sync(0xffffffffu, (E.crank[lane] & kOrbWrap) != 0) &
                                                (kOrbWarpCols << pw);
-                        constexpr int kG = kCols / Cfg::kPW, kD = kRows / Cfg::kPW;
-                        uint64_t crk[kG], rrk[kD];
-                        uint32_t cbt[kG], rbr[kD], brr[kD];
+                        constexpr int kG = kCols / kGW, kD = kRows / kGW;
 #pragma unroll
-                        for (int k = 0; k < kG; ++k) {  // this warp's plan fields first, all in flight
-                            crk[k] = E.crank[pw + Cfg::kPW * k];
-                            cbt[k] = E.cbits[pw + Cfg::kPW * k];
-                        }
-#pragma unroll
-                        for (int k = 0; k < kD; ++k) {
-                            rrk[k] = E.rrank[pw + Cfg::kPW * k];
-                            rbr[k] = __shfl_sync(0xffffffffu, rb, pw + Cfg::kPW * k);
-                            brr[k] = __shfl_sync(0xffffffffu, base, pw + Cfg::kPW * k);
-                        }
-#pragma unroll
-                        for (int k = 0; k < kG; ++k) {  // gathered: column pw + kPW k, row `lane`
-                            const int cc = pw + Cfg::kPW * k;
-                            const uint64_t rank = (crk[k] & ~kOrbWrap) + __popc(cbt[k] & lt_lane);
+                        for (int k = 0; k < kG; ++k) {  // gathered: column pw + kGW k, row `lane`
+                            const int cc = pw + kGW * k;
+                            const uint64_t rank = (E.crank[cc] & ~kOrbWrap) + __popc(E.cbits[cc] & lt_lane);
                             cp_async16_if(((rb & ~wrapc) >> cc) & 1u,
                                           &st.src[base + __popc(rb & ((1u << cc) - 1u))], Xs + rank);
                         }
 #pragma unroll
-                        for (int k = 0; k < kD; ++k) {  // direct: row pw + kPW k, column `lane`
-                            const uint32_t below = __popc(rbr[k] & lt_lane);
-                            cp_async16_if((rbr[k] >> lane) & 1u, &st.dst[brr[k] + below], Xs + (rrk[k] + below));
+                        for (int k = 0; k < kD; ++k) {  // direct: row pw + kGW k, column `lane`
+                            const int rr = pw + kGW * k;
+                            const uint32_t rbr = __shfl_sync(0xffffffffu, rb, rr);
+                            const uint32_t brr = __shfl_sync(0xffffffffu, base, rr);
+                            const uint32_t below = __popc(rbr & lt_lane);
+                            cp_async16_if((rbr >> lane) & 1u, &st.dst[brr + below], Xs + (E.rrank[rr] + below));
                         }
                         if (wrapc) {  // wrapped columns: every element by lookup
                             for (uint32_t wm = wrapc; wm; wm &= wm - 1) {
@@ -737,7 +740,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&sm.planempty[ps]);
                     }
-                    if (pw == 0) {
+                    if (mine && pw == 0) {
                         st.soff[lane] = static_cast<uint16_t>(incl - rowc);
                         if (lane == 31) st.soff[kRows] = static_cast<uint16_t>(incl);
                         if (lane == 0) {
@@ -747,11 +750,14 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                     }
                     gc += K;
                     n += K;
-                    if (pw == 0 && lane == 0) st.last = (wk.last() && n == nch) ? 1u : 0u;
-                    cp_async_arrive(&sm.full[stage]);
-                    if (pw == 0) {
-                        __syncwarp();  // slot tables ordered before lane 0's release
-                        if (lane == 0) mbar_arrive(&sm.full[stage]);
+                    ++qs;
+                    if (mine) {
+                        if (pw == 0 && lane == 0) st.last = (wk.last() && n == nch) ? 1u : 0u;
+                        cp_async_arrive(&sm.full[stage]);
+                        if (pw == 0) {
+                            __syncwarp();  // slot tables ordered before lane 0's release
+                            if (lane == 0) mbar_arrive(&sm.full[stage]);
+                        }
                     }
                     if (++stage == kStages) {
                         stage = 0;
