@@ -275,9 +275,21 @@ def run_ours(args):
 
     def spec_at(s):
         return spec_on and s + 1 < t
-    per_amp = {"probs": 48 if spec_at(timed_stages[-1]) else 32, "combine": 0, "collapse": 48}
-    step_bytes = [N * ((48 if spec_at(s) else 32) + (0 if spec_at(s) and b == 0 else 48))
-                  for s, b in zip(timed_stages, timed_bits)]
+    # orbit-compressed stages (the default from N >= 2^26): the
+    # probs pass reads both sides of the r = ord(a) members and writes both
+    # groups (64 B per member; 32 on a run's last stage), no collapse pass
+    orb = eng.orbit_info()
+    r_orb = orb["r"]
+    orb_st = eng.orbit_stages()
+    orbit_timed = r_orb > 0 and all(orb_st[s] for s in timed_stages)
+    if orbit_timed:
+        per_amp = {"probs": (64 if timed_stages[-1] + 1 < t else 32) * r_orb / N, "combine": 0,
+                   "collapse": 0}
+        step_bytes = [r_orb * (64 if s + 1 < t else 32) for s in timed_stages]
+    else:
+        per_amp = {"probs": 48 if spec_at(timed_stages[-1]) else 32, "combine": 0, "collapse": 48}
+        step_bytes = [N * ((48 if spec_at(s) else 32) + (0 if spec_at(s) and b == 0 else 48))
+                      for s, b in zip(timed_stages, timed_bits)]
     step_bpa = sum(step_bytes) / len(step_bytes) / N  # average algorithmic B/amp per timed stage
     kernels = {}
     for k, (tot, n) in kt.items():
@@ -287,13 +299,14 @@ def run_ours(args):
                       "achieved_gbs": (b / (avg * 1e-3) / 1e9) if avg > 0 and b else None}
     # device time of an average timed stage: probs + combine, plus the collapse
     # on the stages that run it (the speculative write skips it when group 0 is kept)
-    ran = [not (spec_at(s) and b == 0) for s, b in zip(timed_stages, timed_bits)]
+    ran = [not orbit_timed and not (spec_at(s) and b == 0) for s, b in zip(timed_stages, timed_bits)]
     stage_dev_ms = (kernels["probs"]["avg_ms"] + kernels["combine"]["avg_ms"] +
                     kernels["collapse"]["avg_ms"] * sum(ran) / len(ran))
     dom = max(("probs", "collapse"), key=lambda k: kernels[k]["avg_ms"])
     achieved = kernels[dom]["achieved_gbs"]
     tiled = eng.tile_plan(timed_stages[-1])["tiled"]
-    kname = {"probs": "k_tiled<1>" if tiled else "k_stage_probs<1,0>",
+    kname = {"probs": ("k_tiled<1,0,1>" if orbit_timed else "k_tiled<1>") if tiled
+             else "k_stage_probs<1,0>",
              "collapse": "k_tiled<0>" if tiled else "k_stage_collapse<1,0>"}[dom]
     traffic, traffic_src = None, None
     try:  # DRAM bytes per launch of this kernel from the committed ncu capture at this N
@@ -312,6 +325,47 @@ def run_ours(args):
                 "peak_source": peak_src, "traffic": traffic, "traffic_source": traffic_src,
                 "share_of_step": kernels[dom]["avg_ms"] / ms_per_step,
                 "bytes_per_amp": per_amp[dom]}
+    if orbit_timed:
+        roofline["orbit"] = {"members": r_orb, "member_fraction": r_orb / N,
+                             "bytes_per_member": 64,
+                             "what": "k_orb_plan + k_tiled<true,false,true> + k_tile_fixup: both sides "
+                                     "of every member read, both groups written, no collapse pass"}
+
+    # the same stages with orbit compression off (the dense kernels), for scale
+    dense_stages = None
+    if orbit_timed and not args.no_dense_compare:
+        eng.set_orbit(False)
+        state["s"], state["prefix"] = 0, 0
+        eng.state_init()
+        for _ in range(max(args.warmup, 1)):
+            step()
+        nd = max(3, min(args.steps, 10))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        dbits, dst = [], []
+        for _ in range(nd):
+            s_, b_ = step()
+            dst.append(s_)
+            dbits.append(b_)
+        e1.record(stream)
+        e1.synchronize()
+        dms = e0.elapsed_time(e1) / nd
+        eng.set_timing(True)
+        for _ in range(3):
+            step()
+        dkt = eng.kernel_times()
+        eng.set_timing(False)
+        pavg = dkt["probs"][0] / max(dkt["probs"][1], 1)
+        dense_stages = {
+            "ms_per_step": dms, "value": ws * N / (dms * 1e-3), "steps": nd,
+            "probs_ms": pavg, "probs_frac_of_hbm": 48 * N / (pavg * 1e-3) / 1e9 / hbm_peak,
+            "collapse_ms": dkt["collapse"][0] / max(dkt["collapse"][1], 1),
+            "bits_1": sum(dbits),
+            "what": "the same step loop from stage 1 with orbit compression off (dense tiled "
+                    "kernels, speculative group-0 write); not the headline"}
+        eng.set_orbit(True)
 
     # end to end: the public call a user makes (C ABI, host results), full run.
     # e2e.value: every stage dense over all N amplitudes (the reference's work,
@@ -358,7 +412,7 @@ def run_ours(args):
                                                        if spec_at(s) and b == 0)},
         "wall_ms_per_step": 1e3 * wall / args.steps,
         "device_ms_per_stage_kernels": stage_dev_ms,
-        "roofline": roofline, "kernels": kernels,
+        "roofline": roofline, "kernels": kernels, "dense_stages": dense_stages,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 16,
                 "what": "IterativeShorEngine.run(seed, idx) through the C ABI with every stage "
@@ -708,6 +762,8 @@ def main():
     ap.add_argument("--e2e-runs", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the configs 1-2 batched line")
+    ap.add_argument("--no-dense-compare", action="store_true",
+                    help="skip timing the same stages with orbit compression off")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -148,6 +148,7 @@ SIGNATURES = [
     ("shs_engine_sparse_stages", u32, [C.c_void_p]),
     ("shs_engine_set_orbit", C.c_int, [C.c_void_p, i32]),
     ("shs_engine_orbit_info", C.c_int, [C.c_void_p, C.POINTER(u64)]),
+    ("shs_engine_orbit_stages", C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
     ("shs_shor_postprocess", C.c_int, [C.POINTER(u64), u32, u32, u64, u64, u64, i32, i32,
                                        C.c_void_p]),
     ("shs_ekera_postprocess", C.c_int, [C.POINTER(u64), u32, u32, u64, u64, C.c_void_p, u64,

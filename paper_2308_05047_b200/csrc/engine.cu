@@ -1513,12 +1513,15 @@ namespace {
 void plan_orbit(shs_engine* e) {
     e->orb_use.assign(e->t, 0);
     e->orb_r = 0;
-    const char* env = std::getenv("SHS_ORBIT");  // default off until it beats the dense stages
-    e->orb_want = env && env[0] == '1';
+    const char* env = std::getenv("SHS_ORBIT");  // SHS_ORBIT=0: dense stages only
+    e->orb_want = !(env && env[0] == '0');
     if (e->group || e->N < kOrbitMinN) return;
     std::vector<uint8_t> cap(e->t, 0);
     for (uint32_t s = 1; s < e->t; ++s)
-        cap[s] = e->a_pows[s] != 1 && e->plans[s].tiled && !e->plans[s].split_tail;
+        // whole bands: the round-robin plans, and split-tail plans with enough
+        // bands for the dynamic band counter to balance (their rows are long)
+        cap[s] = e->a_pows[s] != 1 && e->plans[s].tiled &&
+                 (!e->plans[s].split_tail || e->plans[s].ntiles >= 4 * static_cast<uint64_t>(e->num_sms));
     bool any = false;
     for (uint32_t s = 1; s < e->t;) {
         uint32_t s1 = s;
@@ -1720,6 +1723,12 @@ int shs_engine_set_orbit(shs_engine* e, int32_t enable) {
     if (!e) return set_error(SHS_INVALID_ARGUMENT, "null engine");
     if (e->rep_orb || e->pending) state_init(e);  // takes effect from a fresh state
     e->orb_want = enable != 0;
+    return SHS_OK;
+}
+
+int shs_engine_orbit_stages(const shs_engine* e, uint8_t* out) {
+    if (!e || !out) return set_error(SHS_INVALID_ARGUMENT, "null argument");
+    for (uint32_t s = 0; s < e->t; ++s) out[s] = e->orb_want && e->orb_r && e->orb_use[s] ? 1 : 0;
     return SHS_OK;
 }
 

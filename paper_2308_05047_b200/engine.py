@@ -432,10 +432,16 @@ class IterativeShorEngine:
         return self._lib.shs_engine_sparse_stages(self._h)
 
     def set_orbit(self, enable: bool) -> None:
-        """Orbit-compressed stages (from N >= 2^26; off by default): stages with
+        """Orbit-compressed stages (on by default from N >= 2^26): stages with
         whole-band tile plans store and sweep only the r = ord_N(a) members of
         <a>, bit-identical results. Toggling resets the state."""
         _raise(self._lib.shs_engine_set_orbit(self._h, 1 if enable else 0))
+
+    def orbit_stages(self) -> List[int]:
+        """1 for every stage that runs compressed"""
+        out = (C.c_uint8 * self.problem.t)()
+        _raise(self._lib.shs_engine_orbit_stages(self._h, out))
+        return list(out)
 
     def orbit_info(self) -> dict:
         """{"r": orbit size (0: off), "stages": stages run compressed, "first": the first}"""
