@@ -99,7 +99,7 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #define SHS_ORB_PRODUCER_WARPS 8
 #endif
 #ifndef SHS_ORB_CONSUMER_WARPS
-#define SHS_ORB_CONSUMER_WARPS (18 - SHS_ORB_PRODUCER_WARPS)
+#define SHS_ORB_CONSUMER_WARPS 8
 #endif
 template <bool kSplit, bool kOrb = false>
 struct TileCfg {
@@ -869,9 +869,13 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 if (k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
                 double* n0 = &sm.nrm[b][0][0][0];
                 double* n1 = &sm.nrm[b][1][0][0];
+                const int K = st.nsub;
                 for (int r = warp; r < kRows; r += kConsumerWarps) {
                     const uint32_t e0 = st.soff[r], e1 = st.soff[r + 1];
                     const uint64_t rk = st.rrank[r];
+                    // the chains' copy of this row's slot table
+                    if (lane < K) sm.meta[b].rbits[lane][r] = st.rbits[lane][r];
+                    if (lane == 31) sm.meta[b].soff[r] = static_cast<uint16_t>(e0);
                     for (uint32_t e = e0 + lane; e < e1; e += 32) {
                         double h0r, h0i, h1r, h1i;
                         stage_pair(sc, st.dst[e], st.src[e], h0r, h0i, h1r, h1i);
@@ -884,13 +888,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         }
                     }
                 }
-                const int K = st.nsub;
-                if (tid < kRows) {
-                    OrbMeta& mt = sm.meta[b];
-                    mt.soff[tid] = st.soff[tid];
-                    for (int j = 0; j < K; ++j) mt.rbits[j][tid] = st.rbits[j][tid];
-                    if (tid == 0) mt.nsub = static_cast<uint16_t>(K);
-                }
+                if (tid == 0) sm.meta[b].nsub = static_cast<uint16_t>(K);
                 named_arrive(kNormFull0 + b, kNormSync);
                 ++k;
                 __syncwarp();
