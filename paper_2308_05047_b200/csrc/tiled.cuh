@@ -1225,31 +1225,63 @@ __device__ __forceinline__ void orb_window(const ulonglong2* __restrict__ rec, u
     rank = R0.y + __popcll(R0.x & lowmask64(o));
 }
 
-static __global__ void __launch_bounds__(256) k_orb_plan(TileParams p, uint64_t nch_max,
+// One warp per band, walking its sub-chunks in order: lane c's column run
+// jumps by kCols m per sub-chunk (a random pair of records, loaded one sub-chunk
+// ahead), lane r's row window advances along the row (each record read once).
+static __global__ void __launch_bounds__(256) k_orb_plan(TileParams p, uint64_t /*nch_max*/,
                                                          const uint32_t* __restrict__ band_off,
                                                          OrbPlan* __restrict__ plan) {
     const int lane = threadIdx.x & 31;
     const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x / 32);
-    for (uint64_t w = blockIdx.x * uint64_t(blockDim.x / 32) + threadIdx.x / 32; w < p.ntiles * nch_max;
-         w += nwarps) {
-        const uint64_t b = w / nch_max, n = w - b * nch_max;
-        if (n >= band_off[b + 1] - band_off[b]) continue;  // warp-uniform
-        const uint64_t j0 = b * kRows, i0 = n * kCols, j = j0 + lane;
+    for (uint64_t b = blockIdx.x * uint64_t(blockDim.x / 32) + threadIdx.x / 32; b < p.ntiles; b += nwarps) {
+        const uint64_t j0 = b * kRows, j = j0 + lane;
         const uint64_t len = tile_row_len(j, p);
-        const uint64_t cs = addmod(j0, mulmod_shoup(i0 + lane, p.m, p.m_sh, p.N), p.N);
-        uint32_t cb, rb = 0;
-        uint64_t cr, rr = 0;
-        orb_window(p.orb, cs, cb, cr);
-        if (cs + (kRows - 1) >= p.N) cr |= kOrbWrap;
-        if (i0 < len) {
-            orb_window(p.orb, mulmod_shoup(j, p.A, p.A_sh, p.N) + i0, rb, rr);
-            if (len - i0 < kCols) rb &= (1u << (len - i0)) - 1u;
+        const uint64_t z = len ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
+        const uint64_t e0 = band_off[b], nch = band_off[b + 1] - e0;
+        uint64_t cs = addmod(j0, mulmod_shoup(lane, p.m, p.m_sh, p.N), p.N);
+        ulonglong2 c0 = __ldg(p.orb + (cs >> 6)), c1 = __ldg(p.orb + (cs >> 6) + 1);
+        uint64_t wcur = z >> 6;
+        ulonglong2 r0 = make_ulonglong2(0ull, 0ull), r1 = r0;
+        if (len) {
+            r0 = __ldg(p.orb + wcur);
+            r1 = __ldg(p.orb + wcur + 1);
         }
-        OrbPlan& e = plan[band_off[b] + n];
-        e.crank[lane] = cr;
-        e.rrank[lane] = rr;
-        e.cbits[lane] = cb;
-        e.rbits[lane] = rb;
+        for (uint64_t n = 0; n < nch; ++n) {
+            const uint64_t i0 = n * kCols;
+            // next sub-chunk's column records, in flight while this one is written
+            const uint64_t csn = addmod(cs, p.m_chunk, p.N);
+            ulonglong2 d0 = c0, d1 = c1;
+            if (n + 1 < nch) {
+                d0 = __ldg(p.orb + (csn >> 6));
+                d1 = __ldg(p.orb + (csn >> 6) + 1);
+            }
+            const unsigned oc = static_cast<unsigned>(cs & 63);
+            const uint32_t cb = static_cast<uint32_t>(oc ? (c0.x >> oc) | (c1.x << (64 - oc)) : c0.x);
+            uint64_t cr = c0.y + __popcll(c0.x & lowmask64(oc));
+            if (cs + (kRows - 1) >= p.N) cr |= kOrbWrap;
+            uint32_t rb = 0;
+            uint64_t rr = 0;
+            if (i0 < len) {
+                const uint64_t s0 = z + i0;
+                if ((s0 >> 6) != wcur) {  // the row moved to the next record
+                    wcur = s0 >> 6;
+                    r0 = r1;
+                    r1 = __ldg(p.orb + wcur + 1);
+                }
+                const unsigned o = static_cast<unsigned>(s0 & 63);
+                rb = static_cast<uint32_t>(o ? (r0.x >> o) | (r1.x << (64 - o)) : r0.x);
+                rr = r0.y + __popcll(r0.x & lowmask64(o));
+                if (len - i0 < kCols) rb &= (1u << (len - i0)) - 1u;
+            }
+            OrbPlan& e = plan[e0 + n];
+            e.crank[lane] = cr;
+            e.rrank[lane] = rr;
+            e.cbits[lane] = cb;
+            e.rbits[lane] = rb;
+            cs = csn;
+            c0 = d0;
+            c1 = d1;
+        }
     }
 }
 
