@@ -99,7 +99,7 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #define SHS_ORB_PRODUCER_WARPS 8
 #endif
 #ifndef SHS_ORB_CONSUMER_WARPS
-#define SHS_ORB_CONSUMER_WARPS 8
+#define SHS_ORB_CONSUMER_WARPS 6
 #endif
 template <bool kSplit, bool kOrb = false>
 struct TileCfg {
@@ -270,7 +270,10 @@ struct OrbPlan {
     uint32_t cbits[kCols];  // membership of the run's kRows sources
     uint32_t rbits[kRows];  // membership of the row's kCols indices (0 past the row's end)
 };
-constexpr int kOrbGroups = 2;  // producer groups filling alternate slots
+#ifndef SHS_ORB_GROUPS
+#define SHS_ORB_GROUPS 1
+#endif
+constexpr int kOrbGroups = SHS_ORB_GROUPS;  // producer groups filling alternate slots
 constexpr int kOrbCap = 1088;  // members per slot: a compact norm tile per group fills a dense one
 static_assert(kOrbCap == kRows * kNrmStride, "compact norm tile = dense norm tile");
 constexpr int kOrbSub = 4;
