@@ -572,6 +572,48 @@ int ensure_buffers_once(shs_engine* e) {
 int orb_build(shs_engine* e) {
     if (e->orb_ready || !e->orb_r || !e->Y) return SHS_OK;
     const uint64_t N = e->N, r = e->orb_r, nw = (N + 63) / 64;
+    // plan layout per orbit stage: band b's sub-chunks at [boff[b], boff[b + 1])
+    std::vector<uint32_t> boff;
+    e->orb_boff_at.assign(e->t, 0);
+    e->orb_nch_max.assign(e->t, 0);
+    uint64_t most = 0;
+    for (uint32_t s = 0; s < e->t; ++s) {
+        if (!e->orb_use[s]) continue;
+        const TilePlanHost& pl = e->plans[s];
+        e->orb_boff_at[s] = boff.size();
+        uint64_t acc = 0, mx = 0;
+        auto len = [&](uint64_t j) -> uint64_t {
+            if (j >= pl.H) return 0;
+            if (j + pl.u < pl.H) return pl.du;
+            if (j >= pl.v) return pl.dv;
+            return pl.du + pl.dv;
+        };
+        for (uint64_t b = 0; b < pl.ntiles; ++b) {
+            boff.push_back(static_cast<uint32_t>(acc));
+            uint64_t m = 0;
+            for (uint64_t j = b * kRows; j < (b + 1) * kRows; ++j) m = std::max(m, len(j));
+            const uint64_t nch = (m + kCols - 1) / kCols;
+            acc += nch;
+            mx = std::max(mx, nch);
+        }
+        boff.push_back(static_cast<uint32_t>(acc));
+        e->orb_nch_max[s] = mx;
+        most = std::max(most, acc);
+    }
+    // the compressed stages need the rank records and the largest stage's plans
+    // beside the state: without room for them (plus 1 GB of slack) the engine
+    // runs every stage dense, with identical results
+    {
+        const size_t need = sizeof(ulonglong2) * (nw + 2) + sizeof(uint32_t) * boff.size() +
+                            sizeof(OrbPlan) * most + (size_t(1) << 30);
+        size_t free_b = 0, total_b = 0;
+        if (!e->orb_rec && (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || free_b < need)) {
+            cudaGetLastError();
+            e->orb_want = false;
+            e->orb_r = 0;
+            return SHS_OK;
+        }
+    }
     const uint64_t a = e->prob.a % N;
     char* scratch = reinterpret_cast<char*>(e->Y);
     auto* bits = reinterpret_cast<unsigned int*>(scratch);
@@ -626,34 +668,6 @@ int orb_build(shs_engine* e) {
     if (last[0] + last[1] != r)
         return set_error(SHS_ERROR, "orbit index: " + std::to_string(last[0] + last[1]) +
                                         " members marked, order " + std::to_string(r));
-    // plan layout per orbit stage: band b's sub-chunks at [boff[b], boff[b + 1])
-    std::vector<uint32_t> boff;
-    e->orb_boff_at.assign(e->t, 0);
-    e->orb_nch_max.assign(e->t, 0);
-    uint64_t most = 0;
-    for (uint32_t s = 0; s < e->t; ++s) {
-        if (!e->orb_use[s]) continue;
-        const TilePlanHost& pl = e->plans[s];
-        e->orb_boff_at[s] = boff.size();
-        uint64_t acc = 0, mx = 0;
-        auto len = [&](uint64_t j) -> uint64_t {
-            if (j >= pl.H) return 0;
-            if (j + pl.u < pl.H) return pl.du;
-            if (j >= pl.v) return pl.dv;
-            return pl.du + pl.dv;
-        };
-        for (uint64_t b = 0; b < pl.ntiles; ++b) {
-            boff.push_back(static_cast<uint32_t>(acc));
-            uint64_t m = 0;
-            for (uint64_t j = b * kRows; j < (b + 1) * kRows; ++j) m = std::max(m, len(j));
-            const uint64_t nch = (m + kCols - 1) / kCols;
-            acc += nch;
-            mx = std::max(mx, nch);
-        }
-        boff.push_back(static_cast<uint32_t>(acc));
-        e->orb_nch_max[s] = mx;
-        most = std::max(most, acc);
-    }
     SHS_CUDA(cudaMalloc(&e->orb_boff, sizeof(uint32_t) * boff.size()));
     SHS_CUDA(cudaMemcpy(e->orb_boff, boff.data(), sizeof(uint32_t) * boff.size(), cudaMemcpyHostToDevice));
     SHS_CUDA(cudaMalloc(&e->orb_plan, sizeof(OrbPlan) * most));
