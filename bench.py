@@ -368,8 +368,8 @@ def run_ours(args):
         eng.set_orbit(True)
 
     # end to end: the public call a user makes (C ABI, host results), full run.
-    # e2e.value: every stage dense over all N amplitudes (the reference's work,
-    # apples to apples with the kernel numbers); s_per_run: the default run()
+    # e2e.value: every stage swept, no sparse prefix (N amplitude updates per
+    # stage, the reference's work, comparable with value); s_per_run: the default run()
     # with its sparse prefix (the first stages on the support of the state,
     # bit-identical results), the "s per full iterative-Shor run" metric.
     def timed_runs(sparse):
@@ -416,10 +416,11 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 16,
                 "what": "IterativeShorEngine.run(seed, idx) through the C ABI with every stage "
-                        "dense (set_sparse(False)): t stages, p0/p1 decided on the device, "
-                        "bit string returned to the host; inputs are the problem scalars "
-                        "(kernel arguments). The default run() (sparse prefix) is s_per_run, "
-                        "same bit string",
+                        "swept (set_sparse(False): no sparse prefix; the stages with whole-band "
+                        "plans orbit-compressed, the rest dense): t stages, p0/p1 decided on "
+                        "the device, bit string returned to the host; inputs are the problem "
+                        "scalars (kernel arguments). The default run() (sparse prefix) is "
+                        "s_per_run, same bit string",
                 "s_per_run_default": run_s,
                 "last_j": str(res.bits.j)},
         "gpu_launches": launches, "clocks": clock_info,
