@@ -604,6 +604,7 @@ int orb_build(shs_engine* e) {
     // beside the state: without room for them (plus 1 GB of slack) the engine
     // runs every stage dense, with identical results
     {
+        if (SHS_ORB_FUSED_PLAN) most = 0;  // the kernel's plan warps compute the entries
         const size_t need = sizeof(ulonglong2) * (nw + 2) + sizeof(uint32_t) * boff.size() +
                             sizeof(OrbPlan) * most + (size_t(1) << 30);
         size_t free_b = 0, total_b = 0;
@@ -670,7 +671,7 @@ int orb_build(shs_engine* e) {
                                         " members marked, order " + std::to_string(r));
     SHS_CUDA(cudaMalloc(&e->orb_boff, sizeof(uint32_t) * boff.size()));
     SHS_CUDA(cudaMemcpy(e->orb_boff, boff.data(), sizeof(uint32_t) * boff.size(), cudaMemcpyHostToDevice));
-    SHS_CUDA(cudaMalloc(&e->orb_plan, sizeof(OrbPlan) * most));
+    if (most) SHS_CUDA(cudaMalloc(&e->orb_plan, sizeof(OrbPlan) * most));
     e->device_bytes += sizeof(uint32_t) * boff.size() + sizeof(OrbPlan) * most;
     e->orb_ready = true;
     return SHS_OK;
@@ -778,7 +779,8 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         const int g2 = static_cast<int>(
             std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
-            k_orb_plan<<<e->num_sms * 8, 256, 0, e->stream>>>(tp, e->orb_nch_max[s], tp.band_off, e->orb_plan);
+            if (!SHS_ORB_FUSED_PLAN)
+                k_orb_plan<<<e->num_sms * 8, 256, 0, e->stream>>>(tp, e->orb_nch_max[s], tp.band_off, e->orb_plan);
             k_tiled<true, false, true><<<g1, tile_threads<true, false, true>(), tile_smem_bytes<true, true>(),
                                          e->stream>>>(tp);
             e->band_issued += pl.ntiles;

@@ -89,6 +89,12 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #ifndef SHS_NORM_BUFS
 #define SHS_NORM_BUFS 4
 #endif
+#ifndef SHS_ORB_FUSED_PLAN
+#define SHS_ORB_FUSED_PLAN 1  // plan entries computed by plan warps in the kernel (0: k_orb_plan + TMA)
+#endif
+#ifndef SHS_ORB_PLAN_WARPS
+#define SHS_ORB_PLAN_WARPS 2
+#endif
 #ifndef SHS_ORB_SLOTS
 #define SHS_ORB_SLOTS 5
 #endif
@@ -210,6 +216,14 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
                  : "memory");
 }
+__device__ __forceinline__ void orb_window(const ulonglong2* __restrict__ rec, uint64_t s,
+                                           uint32_t& bits, uint64_t& rank) {
+    const ulonglong2 R0 = __ldg(rec + (s >> 6)), R1 = __ldg(rec + (s >> 6) + 1);
+    const unsigned o = static_cast<unsigned>(s & 63);
+    bits = static_cast<uint32_t>(o ? (R0.x >> o) | (R1.x << (64 - o)) : R0.x);
+    rank = R0.y + __popcll(R0.x & lowmask64(o));
+}
+
 // predicated 16-byte cp.async (no branch around it). No "memory" clobber: the
 // producers never read the slot they fill, and their barrier arrives order the
 // copies; without it the compiler can batch the plan reads ahead of the copies.
@@ -317,10 +331,11 @@ struct TileSmem {
 
 static_assert(sizeof(TileSmem<true, true>) <= 232448, "orbit variant: shared memory per CTA");
 
+constexpr int kOrbPlanWarps = SHS_ORB_FUSED_PLAN ? SHS_ORB_PLAN_WARPS : 1;
 template <bool kProbs, bool kSplit, bool kOrb = false>
-constexpr int tile_threads() {  // (+ the orbit variant's plan warp)
+constexpr int tile_threads() {  // (+ the orbit variant's plan warps)
     return 32 * (TileCfg<kSplit, kOrb>::kCW + TileCfg<kSplit, kOrb>::kPW + (kProbs ? kChainWarps : 0) +
-                 (kOrb ? 1 : 0));
+                 (kOrb ? kOrbPlanWarps : 0));
 }
 
 template <bool kProbs, bool kOrb = false>
@@ -963,7 +978,47 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             for (uint64_t q = (k > kNormBufs ? k - kNormBufs : 0); q < k; ++q)
                 named_sync(kNormEmpty0 + static_cast<int>(q % kNormBufs), kNormSync);
         }
-    } else if (kOrb && warp == kChainWarp + kChainWarps) {
+    } else if (kOrb && SHS_ORB_FUSED_PLAN && warp >= kChainWarp + kChainWarps) {
+        // ------------------------------------------------------------ plan warps
+        // kOrbPlanWarps warps compute the plan entries in the kernel (no plan
+        // pre-pass): entry g of the CTA's sub-chunk sequence by warp g mod
+        // kOrbPlanWarps, lane c / r: column run c / row r of the sub-chunk, each
+        // window from two rank records
+        const int pwi = warp - (kChainWarp + kChainWarps);
+        uint64_t g = 0;
+        for (uint64_t ik = 0;; ++ik) {
+            const uint64_t bb = ik == 0 ? blockIdx.x : sm.bandq[ik % kBandQ];
+            if (bb >= p.ntiles) break;
+            const uint64_t j0 = bb * kRows, j = j0 + lane;
+            const uint64_t len = tile_row_len(j, p);
+            const uint64_t z = len ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
+            const uint64_t nch = (__reduce_max_sync(0xffffffffu, static_cast<uint32_t>(len)) + kCols - 1) / kCols;
+            uint64_t n = (pwi + kOrbPlanWarps - g % kOrbPlanWarps) % kOrbPlanWarps;  // first of mine
+            for (; n < nch; n += kOrbPlanWarps) {
+                const uint64_t ge = g + n;  // this entry's index in the CTA's sequence
+                const uint64_t i0 = n * kCols;
+                const uint64_t cs = addmod(j0, mulmod_shoup(i0 + lane, p.m, p.m_sh, p.N), p.N);
+                uint32_t cb, rb = 0;
+                uint64_t cr, rr = 0;
+                orb_window(p.orb, cs, cb, cr);
+                if (cs + (kRows - 1) >= p.N) cr |= kOrbWrap;
+                if (i0 < len) {
+                    orb_window(p.orb, z + i0, rb, rr);
+                    if (len - i0 < kCols) rb &= (1u << (len - i0)) - 1u;
+                }
+                const int ps = static_cast<int>(ge % kOrbPlanRing);
+                mbar_wait(&sm.planempty[ps], static_cast<uint32_t>((ge / kOrbPlanRing) & 1) ^ 1);
+                OrbPlan& e = sm.plan[ps];
+                e.crank[lane] = cr;
+                e.rrank[lane] = rr;
+                e.cbits[lane] = cb;
+                e.rbits[lane] = rb;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.planfull[ps]);
+            }
+            g += nch;
+        }
+    } else if (kOrb && !SHS_ORB_FUSED_PLAN && warp == kChainWarp + kChainWarps) {
         // ------------------------------------------------------------ plan warp
         // lane 0 walks the CTA's band sequence (band k from bandq, written by the
         // first producer thread one band ahead) and prefetches every sub-chunk's
@@ -1220,13 +1275,6 @@ static __global__ void __launch_bounds__(32 * kFixWarps, 2) k_tile_fixup(TilePar
 
 // Per-stage pre-pass of the orbit variant: the OrbPlan of band b, sub-chunk n
 // (one warp each, lane = column run / row) into plan[band_off[b] + n].
-__device__ __forceinline__ void orb_window(const ulonglong2* __restrict__ rec, uint64_t s,
-                                           uint32_t& bits, uint64_t& rank) {
-    const ulonglong2 R0 = __ldg(rec + (s >> 6)), R1 = __ldg(rec + (s >> 6) + 1);
-    const unsigned o = static_cast<unsigned>(s & 63);
-    bits = static_cast<uint32_t>(o ? (R0.x >> o) | (R1.x << (64 - o)) : R0.x);
-    rank = R0.y + __popcll(R0.x & lowmask64(o));
-}
 
 // One warp per band, walking its sub-chunks in order: lane c's column run
 // jumps by kCols m per sub-chunk (a random pair of records, loaded one sub-chunk
