@@ -328,8 +328,9 @@ def run_ours(args):
     if orbit_timed:
         roofline["orbit"] = {"members": r_orb, "member_fraction": r_orb / N,
                              "bytes_per_member": 64,
-                             "what": "k_orb_plan + k_tiled<true,false,true> + k_tile_fixup: both sides "
-                                     "of every member read, both groups written, no collapse pass"}
+                             "what": "k_tiled<true,false,true> (plan warps, producers, consumers, "
+                                     "chains) + k_tile_fixup: both sides of every member read, both "
+                                     "groups written, no collapse pass"}
 
     # the same stages with orbit compression off (the dense kernels), for scale
     dense_stages = None

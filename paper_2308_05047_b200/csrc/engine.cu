@@ -156,10 +156,6 @@ struct shs_engine {
     int orb_sel = 0;               // its slot when the host knows it ...
     const DevStage* orb_prev = nullptr;  // ... else the device slot whose sel picks it
     int64_t orb_stage = -1;        // the stage whose probs pass ran compressed (pending collapse)
-    // per orbit stage: band offsets of its plan entries (k_orb_plan), into one array
-    std::vector<uint64_t> orb_boff_at, orb_nch_max;  // [t]: offset into orb_boff, longest band
-    uint32_t* orb_boff = nullptr;
-    OrbPlan* orb_plan = nullptr;   // entries of the largest orbit stage
 };
 
 namespace {
@@ -464,8 +460,6 @@ void release(shs_engine* e) {
     if (e->h_out) cudaFreeHost(e->h_out);
     cudaFree(e->d_slots);
     cudaFree(e->orb_rec);
-    cudaFree(e->orb_boff);
-    cudaFree(e->orb_plan);
     if (e->h_rec) cudaFreeHost(e->h_rec);
     for (auto ev : e->meas_ev)
         if (ev) cudaEventDestroy(ev);
@@ -572,41 +566,11 @@ int ensure_buffers_once(shs_engine* e) {
 int orb_build(shs_engine* e) {
     if (e->orb_ready || !e->orb_r || !e->Y) return SHS_OK;
     const uint64_t N = e->N, r = e->orb_r, nw = (N + 63) / 64;
-    // plan layout per orbit stage: band b's sub-chunks at [boff[b], boff[b + 1])
-    std::vector<uint32_t> boff;
-    e->orb_boff_at.assign(e->t, 0);
-    e->orb_nch_max.assign(e->t, 0);
-    uint64_t most = 0;
-    for (uint32_t s = 0; s < e->t; ++s) {
-        if (!e->orb_use[s]) continue;
-        const TilePlanHost& pl = e->plans[s];
-        e->orb_boff_at[s] = boff.size();
-        uint64_t acc = 0, mx = 0;
-        auto len = [&](uint64_t j) -> uint64_t {
-            if (j >= pl.H) return 0;
-            if (j + pl.u < pl.H) return pl.du;
-            if (j >= pl.v) return pl.dv;
-            return pl.du + pl.dv;
-        };
-        for (uint64_t b = 0; b < pl.ntiles; ++b) {
-            boff.push_back(static_cast<uint32_t>(acc));
-            uint64_t m = 0;
-            for (uint64_t j = b * kRows; j < (b + 1) * kRows; ++j) m = std::max(m, len(j));
-            const uint64_t nch = (m + kCols - 1) / kCols;
-            acc += nch;
-            mx = std::max(mx, nch);
-        }
-        boff.push_back(static_cast<uint32_t>(acc));
-        e->orb_nch_max[s] = mx;
-        most = std::max(most, acc);
-    }
-    // the compressed stages need the rank records and the largest stage's plans
-    // beside the state: without room for them (plus 1 GB of slack) the engine
-    // runs every stage dense, with identical results
+    // the compressed stages need the rank records beside the state: without
+    // room for them (plus 1 GB of slack) the engine runs every stage dense, with
+    // identical results
     {
-        if (SHS_ORB_FUSED_PLAN) most = 0;  // the kernel's plan warps compute the entries
-        const size_t need = sizeof(ulonglong2) * (nw + 2) + sizeof(uint32_t) * boff.size() +
-                            sizeof(OrbPlan) * most + (size_t(1) << 30);
+        const size_t need = sizeof(ulonglong2) * (nw + 2) + (size_t(1) << 30);
         size_t free_b = 0, total_b = 0;
         if (!e->orb_rec && (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || free_b < need)) {
             cudaGetLastError();
@@ -669,10 +633,6 @@ int orb_build(shs_engine* e) {
     if (last[0] + last[1] != r)
         return set_error(SHS_ERROR, "orbit index: " + std::to_string(last[0] + last[1]) +
                                         " members marked, order " + std::to_string(r));
-    SHS_CUDA(cudaMalloc(&e->orb_boff, sizeof(uint32_t) * boff.size()));
-    SHS_CUDA(cudaMemcpy(e->orb_boff, boff.data(), sizeof(uint32_t) * boff.size(), cudaMemcpyHostToDevice));
-    if (most) SHS_CUDA(cudaMalloc(&e->orb_plan, sizeof(OrbPlan) * most));
-    e->device_bytes += sizeof(uint32_t) * boff.size() + sizeof(OrbPlan) * most;
     e->orb_ready = true;
     return SHS_OK;
 }
@@ -772,21 +732,17 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         tp.Y1 = e->Y + e->orb_pad;
         tp.orb = e->orb_rec;
         tp.write = s + 1 < e->t ? 1 : 0;
-        tp.plan = e->orb_plan;
-        tp.band_off = e->orb_boff + e->orb_boff_at[s];
         const TilePlanHost& pl = e->plans[s];
         const int g1 = static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         const int g2 = static_cast<int>(
             std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
-            if (!SHS_ORB_FUSED_PLAN)
-                k_orb_plan<<<e->num_sms * 8, 256, 0, e->stream>>>(tp, e->orb_nch_max[s], tp.band_off, e->orb_plan);
             k_tiled<true, false, true><<<g1, tile_threads<true, false, true>(), tile_smem_bytes<true, true>(),
                                          e->stream>>>(tp);
             e->band_issued += pl.ntiles;
             k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
-        e->launches += 2;  // plan + k_tiled + k_tile_fixup in one launch group
+        e->launches++;  // k_tiled + k_tile_fixup in one launch group
         *nparts = g1 + g2;
         e->spec_stage = -1;
         e->orb_stage = s;

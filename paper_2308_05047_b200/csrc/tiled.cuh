@@ -89,9 +89,6 @@ static_assert(kCols <= 256 && kProducers % kCols == 0 && kConsumers % kCols == 0
 #ifndef SHS_NORM_BUFS
 #define SHS_NORM_BUFS 4
 #endif
-#ifndef SHS_ORB_FUSED_PLAN
-#define SHS_ORB_FUSED_PLAN 1  // plan entries computed by plan warps in the kernel (0: k_orb_plan + TMA)
-#endif
 #ifndef SHS_ORB_PLAN_WARPS
 #define SHS_ORB_PLAN_WARPS 2
 #endif
@@ -166,8 +163,6 @@ struct TileParams {
     const DevStage* prev;
     int prev_sel;
     int write;
-    const struct OrbPlan* plan;  // k_orb_plan output: band b's sub-chunk n at plan[band_off[b] + n]
-    const uint32_t* band_off;
 };
 
 __device__ __forceinline__ uint64_t tile_row_len(uint64_t j, const TileParams& p) {
@@ -193,10 +188,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                  "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -233,14 +224,6 @@ __device__ __forceinline__ void cp_async16_if(bool pred, void* dst, const void* 
             smem_addr(dst)),
         "l"(src), "r"(static_cast<uint32_t>(pred)));
 }
-// 1-D bulk copy global -> shared (TMA), completing `bytes` on bar's transaction count
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
 // arrive on bar once all of this thread's prior cp.async copies have landed
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar))
@@ -270,14 +253,13 @@ struct __align__(16) TileStage {
     uint64_t last;  // 1 on the last chunk of the CTA's sequence
 };
 
-// Orbit variant (kOrb). A per-stage pre-pass (k_orb_plan) turns the rank
-// records into one OrbPlan per band and 32-column sub-chunk: the rank base and
-// membership window of each gathered column run and of each row run. The
-// producers prefetch plans with 1-D bulk copies (TMA) kOrbPlanRing entries
-// ahead, so no record lookup sits on their path, and pack the members of up to
-// kOrbSub consecutive sub-chunks of a band into one compact slot (up to
-// kOrbCap members per side: a slot holds as many live amplitudes as a dense
-// 32 x 32 chunk would, so as many bytes are in flight per SM).
+// Orbit variant (kOrb). Plan warps turn the rank records into one OrbPlan per
+// band and 32-column sub-chunk (the rank base and membership window of each
+// gathered column run and of each row run) in a shared-memory ring ahead of the
+// producers, so no record lookup sits on their path; the producers pack the
+// members of up to kOrbSub consecutive sub-chunks of a band into one compact
+// slot (up to kOrbCap members per side: a slot holds as many live amplitudes as
+// a dense 32 x 32 chunk would, so as many bytes are in flight per SM).
 struct OrbPlan {
     uint64_t crank[kCols];  // rank of column run c's first source; bit 63: the run wraps past N - 1
     uint64_t rrank[kRows];  // rank of row r's first index of the sub-chunk
@@ -331,7 +313,7 @@ struct TileSmem {
 
 static_assert(sizeof(TileSmem<true, true>) <= 232448, "orbit variant: shared memory per CTA");
 
-constexpr int kOrbPlanWarps = SHS_ORB_FUSED_PLAN ? SHS_ORB_PLAN_WARPS : 1;
+constexpr int kOrbPlanWarps = SHS_ORB_PLAN_WARPS;
 template <bool kProbs, bool kSplit, bool kOrb = false>
 constexpr int tile_threads() {  // (+ the orbit variant's plan warps)
     return 32 * (TileCfg<kSplit, kOrb>::kCW + TileCfg<kSplit, kOrb>::kPW + (kProbs ? kChainWarps : 0) +
@@ -978,7 +960,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             for (uint64_t q = (k > kNormBufs ? k - kNormBufs : 0); q < k; ++q)
                 named_sync(kNormEmpty0 + static_cast<int>(q % kNormBufs), kNormSync);
         }
-    } else if (kOrb && SHS_ORB_FUSED_PLAN && warp >= kChainWarp + kChainWarps) {
+    } else if (kOrb && warp >= kChainWarp + kChainWarps) {
         // ------------------------------------------------------------ plan warps
         // kOrbPlanWarps warps compute the plan entries in the kernel (no plan
         // pre-pass): entry g of the CTA's sub-chunk sequence by warp g mod
@@ -1018,32 +1000,6 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             }
             g += nch;
         }
-    } else if (kOrb && !SHS_ORB_FUSED_PLAN && warp == kChainWarp + kChainWarps) {
-        // ------------------------------------------------------------ plan warp
-        // lane 0 walks the CTA's band sequence (band k from bandq, written by the
-        // first producer thread one band ahead) and prefetches every sub-chunk's
-        // OrbPlan into the ring as soon as its entry is free
-        if (lane == 0) {
-            uint64_t gi = 0;
-            for (uint64_t ik = 0;; ++ik) {
-                const uint64_t bb = ik == 0 ? blockIdx.x : sm.bandq[ik % kBandQ];
-                if (bb >= p.ntiles) break;
-                uint64_t mx = 0;
-                for (int r = 0; r < kRows; ++r) {
-                    const uint64_t l = tile_row_len(bb * kRows + r, p);
-                    mx = l > mx ? l : mx;
-                }
-                const uint64_t nch = (mx + kCols - 1) / kCols;
-                const OrbPlan* src = p.plan + p.band_off[bb];
-                for (uint64_t n = 0; n < nch; ++n, ++gi) {
-                    const int ps = static_cast<int>(gi % kOrbPlanRing);
-                    mbar_wait(&sm.planempty[ps], static_cast<uint32_t>((gi / kOrbPlanRing) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&sm.planfull[ps], sizeof(OrbPlan));
-                    bulk_g2s(&sm.plan[ps], src + n, sizeof(OrbPlan), &sm.planfull[ps]);
-                }
-            }
-        }
-        __syncwarp();
     } else if (kProbs && warp >= kChainWarp && warp < kChainWarp + kChainWarps) {
         // ------------------------------------------------------------ chains
         const int ct = tid - 32 * kChainWarp;  // one lane per (row, group)
@@ -1271,69 +1227,6 @@ static __global__ void __launch_bounds__(32 * kFixWarps, 2) k_tile_fixup(TilePar
     window_flush(win, digits[g]);
     __syncthreads();
     write_partials(digits, slots + uint64_t(blockIdx.x) * 2 * kDigits, tid);
-}
-
-// Per-stage pre-pass of the orbit variant: the OrbPlan of band b, sub-chunk n
-// (one warp each, lane = column run / row) into plan[band_off[b] + n].
-
-// One warp per band, walking its sub-chunks in order: lane c's column run
-// jumps by kCols m per sub-chunk (a random pair of records, loaded one sub-chunk
-// ahead), lane r's row window advances along the row (each record read once).
-static __global__ void __launch_bounds__(256) k_orb_plan(TileParams p, uint64_t /*nch_max*/,
-                                                         const uint32_t* __restrict__ band_off,
-                                                         OrbPlan* __restrict__ plan) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x / 32);
-    for (uint64_t b = blockIdx.x * uint64_t(blockDim.x / 32) + threadIdx.x / 32; b < p.ntiles; b += nwarps) {
-        const uint64_t j0 = b * kRows, j = j0 + lane;
-        const uint64_t len = tile_row_len(j, p);
-        const uint64_t z = len ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
-        const uint64_t e0 = band_off[b], nch = band_off[b + 1] - e0;
-        uint64_t cs = addmod(j0, mulmod_shoup(lane, p.m, p.m_sh, p.N), p.N);
-        ulonglong2 c0 = __ldg(p.orb + (cs >> 6)), c1 = __ldg(p.orb + (cs >> 6) + 1);
-        uint64_t wcur = z >> 6;
-        ulonglong2 r0 = make_ulonglong2(0ull, 0ull), r1 = r0;
-        if (len) {
-            r0 = __ldg(p.orb + wcur);
-            r1 = __ldg(p.orb + wcur + 1);
-        }
-        for (uint64_t n = 0; n < nch; ++n) {
-            const uint64_t i0 = n * kCols;
-            // next sub-chunk's column records, in flight while this one is written
-            const uint64_t csn = addmod(cs, p.m_chunk, p.N);
-            ulonglong2 d0 = c0, d1 = c1;
-            if (n + 1 < nch) {
-                d0 = __ldg(p.orb + (csn >> 6));
-                d1 = __ldg(p.orb + (csn >> 6) + 1);
-            }
-            const unsigned oc = static_cast<unsigned>(cs & 63);
-            const uint32_t cb = static_cast<uint32_t>(oc ? (c0.x >> oc) | (c1.x << (64 - oc)) : c0.x);
-            uint64_t cr = c0.y + __popcll(c0.x & lowmask64(oc));
-            if (cs + (kRows - 1) >= p.N) cr |= kOrbWrap;
-            uint32_t rb = 0;
-            uint64_t rr = 0;
-            if (i0 < len) {
-                const uint64_t s0 = z + i0;
-                if ((s0 >> 6) != wcur) {  // the row moved to the next record
-                    wcur = s0 >> 6;
-                    r0 = r1;
-                    r1 = __ldg(p.orb + wcur + 1);
-                }
-                const unsigned o = static_cast<unsigned>(s0 & 63);
-                rb = static_cast<uint32_t>(o ? (r0.x >> o) | (r1.x << (64 - o)) : r0.x);
-                rr = r0.y + __popcll(r0.x & lowmask64(o));
-                if (len - i0 < kCols) rb &= (1u << (len - i0)) - 1u;
-            }
-            OrbPlan& e = plan[e0 + n];
-            e.crank[lane] = cr;
-            e.rrank[lane] = rr;
-            e.cbits[lane] = cb;
-            e.rbits[lane] = rb;
-            cs = csn;
-            c0 = d0;
-            c1 = d1;
-        }
-    }
 }
 
 }  // namespace shs
