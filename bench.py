@@ -46,6 +46,9 @@ WORKLOADS = {
     # profiling size for the round-robin tiled variant (config 4's): 17 GB per buffer
     "n30": dict(N=1073217479, a=2, p=32749, q=32771,
                 desc="30-qubit profiling size: N=1073217479=32749*32771, a=2 (order 536575980), t=60"),
+    # an orbit of N / 6 (p - 1, q - 1 share 2 * 3 * ...): the compressed stages at low density
+    "n30r6": dict(N=1087482493, a=2, p=32971, q=32983,
+                  desc="30-qubit size with a small orbit: N=1087482493=32971*32983, a=2 (order 181236090 = N/6)"),
     # profiling size: 4.3 GB per buffer (34x L2), fast ncu replays
     "n29": dict(N=268435247, a=3, p=12589, q=21323,
                 desc="29-qubit profiling size: N=268435247=12589*21323, a=3 (order 67100334), t=56"),

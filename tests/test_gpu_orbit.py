@@ -109,3 +109,31 @@ def test_orbit_step_api_states_equal_dense_n30(cuda_ok, oracle):
         a_eng.close()
         b_eng.close()
         gc.collect()
+
+
+@pytest.mark.parametrize("N,a,r", [
+    (1087482493, 2, 181236090),  # 32971 * 32983: the orbit is N / 6
+    (1074262927, 2, 523488),     # 32719 * 32833: N / 2052 (slots pack 4 near-empty sub-chunks)
+])
+def test_orbit_low_density_runs_equal_dense(cuda_ok, N, a, r):
+    """Orbits much smaller than N / 2: the compressed stages pack up to four
+    sub-chunks per slot; runs with and without the sparse prefix equal the
+    dense engine's."""
+    import paper_2308_05047_b200 as shs
+    err = shs.ErrorConfig(shs.ErrorKind.phase_init, 0.1)
+    eng = _engine(N, a, err)
+    assert eng.orbit_info()["r"] == r and eng.orbit_info()["stages"] > 0
+    got = []
+    for sparse in (True, False):
+        eng.set_sparse(sparse)
+        got.append(eng.run(5, 1))
+    eng.set_orbit(False)
+    want = []
+    for sparse in (True, False):
+        eng.set_sparse(sparse)
+        want.append(eng.run(5, 1))
+    eng.close()
+    gc.collect()
+    for g, w in zip(got, want):
+        assert g.bits.j == w.bits.j and g.j_sampled == w.j_sampled
+        assert [x.p1 for x in g.trace] == [x.p1 for x in w.trace]
