@@ -270,8 +270,10 @@ struct OrbPlan {
 #define SHS_ORB_GROUPS 1
 #endif
 constexpr int kOrbGroups = SHS_ORB_GROUPS;  // producer groups filling alternate slots
-constexpr int kOrbCap = 1088;  // members per slot: a compact norm tile per group fills a dense one
-static_assert(kOrbCap == kRows * kNrmStride, "compact norm tile = dense norm tile");
+#ifndef SHS_ORB_CAP
+#define SHS_ORB_CAP 1088
+#endif
+constexpr int kOrbCap = SHS_ORB_CAP;  // members per slot (one compact norm tile per group)
 constexpr int kOrbSub = 4;
 constexpr int kOrbPlanRing = 8;
 constexpr uint64_t kOrbWrap = 1ull << 63;
@@ -302,7 +304,8 @@ struct TileSmem {
     static constexpr int kST = kOrb ? SHS_ORB_SLOTS : kStages;
     static constexpr int kNB = kOrb ? SHS_ORB_NORM_BUFS : kNormBufs;
     std::conditional_t<kOrb, OrbSlot, TileStage> stage[kST];
-    double nrm[kProbs ? kNB : 1][2][kRows][kNrmStride];  // [buffer][group][row][col]
+    double nrm[kProbs && !kOrb ? kNB : 1][2][kOrb ? 1 : kRows][kOrb ? 1 : kNrmStride];  // [buffer][group][row][col]
+    double onrm[kOrb ? kNB : 1][2][kOrb ? kOrbCap : 1];  // orbit: [buffer][group][member]
     uint64_t full[kST], empty[kST];
     unsigned long long digits[2][kDigits];
     uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
@@ -867,8 +870,8 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 // the row's members i, i + 32, ... (consecutive smem and ranks)
                 const int b = static_cast<int>(k % kNormBufs);
                 if (k >= kNormBufs) named_sync(kNormEmpty0 + b, kNormSync);
-                double* n0 = &sm.nrm[b][0][0][0];
-                double* n1 = &sm.nrm[b][1][0][0];
+                double* n0 = &sm.onrm[b][0][0];
+                double* n1 = &sm.onrm[b][1][0];
                 const int K = st.nsub;
                 for (int r = warp; r < kRows; r += kConsumerWarps) {
                     const uint32_t e0 = st.soff[r], e1 = st.soff[r + 1];
@@ -1032,7 +1035,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                     named_sync(kNormFull0 + b, kNormSync);
                     const OrbMeta& mt = sm.meta[b];
                     const int K = mt.nsub;
-                    const double* nv = &sm.nrm[b][cg][0][0];
+                    const double* nv = &sm.onrm[b][cg][0];
                     uint32_t e = mt.soff[cr];
                     // fold the next cnt members in order, 8 loads in flight at a time
                     // (padding adds +0.0, which leaves the non-negative sum unchanged)
