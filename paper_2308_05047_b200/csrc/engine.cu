@@ -733,13 +733,23 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         tp.orb = e->orb_rec;
         tp.write = s + 1 < e->t ? 1 : 0;
         const TilePlanHost& pl = e->plans[s];
-        const int g1 = static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
+        // whole bands from the dynamic counter, unless the plan has too few bands
+        // for it to balance; then the split plan's static work items (row spans
+        // cut at 256-block boundaries). Config 4's long-row plans (>= 4 bands per
+        // SM) measured 1% faster whole, n30's few-band ones 6% faster per run split.
+        const bool split = pl.split_tail && pl.ntiles < 4 * static_cast<uint64_t>(e->num_sms);
+        const int g1 = split ? pl.grid : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         const int g2 = static_cast<int>(
             std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
         rc = launch(e, 0, [&] {
-            k_tiled<true, false, true><<<g1, tile_threads<true, false, true>(), tile_smem_bytes<true, true>(),
-                                         e->stream>>>(tp);
-            e->band_issued += pl.ntiles;
+            if (split) {
+                k_tiled<true, true, true><<<g1, tile_threads<true, true, true>(), tile_smem_bytes<true, true>(),
+                                            e->stream>>>(tp);
+            } else {
+                k_tiled<true, false, true><<<g1, tile_threads<true, false, true>(), tile_smem_bytes<true, true>(),
+                                             e->stream>>>(tp);
+                e->band_issued += pl.ntiles;
+            }
             k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
         });
         e->launches++;  // k_tiled + k_tile_fixup in one launch group
@@ -1490,10 +1500,7 @@ void plan_orbit(shs_engine* e) {
     if (e->group || e->N < kOrbitMinN) return;
     std::vector<uint8_t> cap(e->t, 0);
     for (uint32_t s = 1; s < e->t; ++s)
-        // whole bands: the round-robin plans, and split-tail plans with enough
-        // bands for the dynamic band counter to balance (their rows are long)
-        cap[s] = e->a_pows[s] != 1 && e->plans[s].tiled &&
-                 (!e->plans[s].split_tail || e->plans[s].ntiles >= 4 * static_cast<uint64_t>(e->num_sms));
+        cap[s] = e->a_pows[s] != 1 && e->plans[s].tiled;
     bool any = false;
     for (uint32_t s = 1; s < e->t;) {
         uint32_t s1 = s;
@@ -1621,9 +1628,11 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
                                   static_cast<int>(tile_smem_bytes<true>()));
         if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<probs>)");
     }
-    ce = cudaFuncSetAttribute(k_tiled<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(tile_smem_bytes<true, true>()));
-    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<orbit>)");
+    for (auto fn : {k_tiled<true, false, true>, k_tiled<true, true, true>}) {
+        ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tile_smem_bytes<true, true>()));
+        if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tiled<orbit>)");
+    }
     for (auto fn : {k_tiled<false, false>, k_tiled<false, true>}) {
         ce = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(tile_smem_bytes<false>()));

@@ -562,8 +562,8 @@ __device__ __forceinline__ void store_rows(const LaneRows& lr, int lane, uint64_
 
 template <bool kProbs, bool kSplit, bool kOrb = false>
 __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_tiled(TileParams p) {
-    static_assert(!kOrb || (kProbs && !kSplit && kRows == 32 && kCols == 32),
-                  "orbit variant: probs pass, whole bands, 32 x 32 chunks");
+    static_assert(!kOrb || (kProbs && kRows == 32 && kCols == 32),
+                  "orbit variant: probs pass, 32 x 32 chunks");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmem<kProbs, kOrb>& sm = *reinterpret_cast<TileSmem<kProbs, kOrb>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -646,9 +646,11 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
             uint64_t gc = 0;  // plan entries consumed
             for (CtaWork<kSplit> wk(p, sm.bandq, true, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
                 const uint64_t j0 = wk.band() * kRows;
+                const uint64_t lo_col = wk.lo();  // split plans: this CTA's columns of the band
                 LaneRows lr;
-                const uint64_t tend = tile_rows_split(p, j0, lane, lr, 0, ~0ull);
-                const uint64_t nch = (tend + kCols - 1) / kCols;
+                const uint64_t tend = tile_rows_split(p, j0, lane, lr, lo_col, wk.hi());
+                const uint64_t iend = tend > lo_col ? tend : lo_col + 1;  // >= 1 sub-chunk per item
+                const uint64_t nch = (iend - lo_col + kCols - 1) / kCols;
                 uint64_t n = 0;
                 while (n < nch) {
                     const bool mine = static_cast<int>(qs % kOrbGroups) == grp;
@@ -690,6 +692,12 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         if (lane >= o) incl += v;
                     }
                     uint32_t base = incl - rowc;  // this row's next member slot index
+                    uint32_t rowc_before[kOrbSub];  // this row's members in the slot's earlier sub-chunks
+#pragma unroll
+                    for (int jj = 0, acc = 0; jj < kOrbSub; ++jj) {
+                        rowc_before[jj] = acc;
+                        acc += cntj[jj];
+                    }
                     // (one bulk copy per row for the direct side measured slower:
                     // 13.1 vs 11.8 ms at n30, TMA-issue bound)
                     // pass 2: copies, sub-chunk by sub-chunk
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         }
                         const OrbPlan& E = sm.plan[ps];
                         const uint32_t rb = rbj[jj];
-                        const uint64_t i0 = (n + jj) * kCols;
+                        const uint64_t i0 = lo_col + (n + jj) * kCols;
                         const uint32_t wrapc = __ballot_sync(0xffffffffu, (E.crank[lane] & kOrbWrap) != 0) &
                                                (kOrbWarpCols << pw);
                         constexpr int kG = kCols / kGW, kD = kRows / kGW;
@@ -737,7 +745,10 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         }
                         if (pw == 0) {
                             st.rbits[jj][lane] = rb;
-                            if (jj == 0) st.rrank[lane] = E.rrank[lane];
+                            // the row's first members in the slot: the rank of its
+                            // first included position (spans of split plans start mid-row)
+                            const uint32_t before = jj ? rowc_before[jj] : 0u;
+                            if (rb && before == 0) st.rrank[lane] = E.rrank[lane];
                         }
                         base += cntj[jj];
                         __syncwarp();
@@ -748,7 +759,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         if (lane == 31) st.soff[kRows] = static_cast<uint16_t>(incl);
                         if (lane == 0) {
                             st.nsub = static_cast<uint16_t>(K);
-                            st.i0 = static_cast<uint32_t>(n * kCols);
+                            st.i0 = static_cast<uint32_t>(lo_col + n * kCols);
                         }
                     }
                     gc += K;
@@ -971,25 +982,31 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
         // window from two rank records
         const int pwi = warp - (kChainWarp + kChainWarps);
         uint64_t g = 0;
-        for (uint64_t ik = 0;; ++ik) {
-            const uint64_t bb = ik == 0 ? blockIdx.x : sm.bandq[ik % kBandQ];
-            if (bb >= p.ntiles) break;
-            const uint64_t j0 = bb * kRows, j = j0 + lane;
-            const uint64_t len = tile_row_len(j, p);
-            const uint64_t z = len ? mulmod_shoup(j, p.A, p.A_sh, p.N) : 0;
-            const uint64_t nch = (__reduce_max_sync(0xffffffffu, static_cast<uint32_t>(len)) + kCols - 1) / kCols;
+        for (CtaWork<kSplit> wk(p, sm.bandq, false, kProducerWarp, Cfg::kProds); wk.valid(); wk.next(p)) {
+            const uint64_t j0 = wk.band() * kRows;
+            const uint64_t lo_col = wk.lo();
+            LaneRows lr;  // lane: row j0 + lane, its span [lo, hi) of this work item
+            const uint64_t tend = tile_rows_split(p, j0, lane, lr, lo_col, wk.hi());
+            const uint64_t iend = tend > lo_col ? tend : lo_col + 1;
+            const uint64_t nch = (iend - lo_col + kCols - 1) / kCols;
+            const uint64_t z = lr.z[0], rlo = lr.lo[0], rhi = lr.hi[0];
             uint64_t n = (pwi + kOrbPlanWarps - g % kOrbPlanWarps) % kOrbPlanWarps;  // first of mine
             for (; n < nch; n += kOrbPlanWarps) {
                 const uint64_t ge = g + n;  // this entry's index in the CTA's sequence
-                const uint64_t i0 = n * kCols;
+                const uint64_t i0 = lo_col + n * kCols;
                 const uint64_t cs = addmod(j0, mulmod_shoup(i0 + lane, p.m, p.m_sh, p.N), p.N);
                 uint32_t cb, rb = 0;
                 uint64_t cr, rr = 0;
                 orb_window(p.orb, cs, cb, cr);
                 if (cs + (kRows - 1) >= p.N) cr |= kOrbWrap;
-                if (i0 < len) {
-                    orb_window(p.orb, z + i0, rb, rr);
-                    if (len - i0 < kCols) rb &= (1u << (len - i0)) - 1u;
+                if (i0 < rhi && i0 + kCols > rlo) {  // the row's span meets the sub-chunk
+                    uint32_t full;
+                    orb_window(p.orb, z + i0, full, rr);
+                    const uint32_t a0 = rlo > i0 ? static_cast<uint32_t>(rlo - i0) : 0u;
+                    const uint32_t a1 = rhi - i0 < kCols ? static_cast<uint32_t>(rhi - i0) : uint32_t(kCols);
+                    const uint32_t keep = (a1 >= 32 ? ~0u : ((1u << a1) - 1u)) & ~((1u << a0) - 1u);
+                    rb = full & keep;
+                    rr += __popc(full & ((1u << a0) - 1u));  // rank of the span's first position
                 }
                 const int ps = static_cast<int>(ge % kOrbPlanRing);
                 mbar_wait(&sm.planempty[ps], static_cast<uint32_t>((ge / kOrbPlanRing) & 1) ^ 1);
@@ -1029,7 +1046,9 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 // sub-chunk by sub-chunk; positions off the orbit add +0.0 in the
                 // reference, so skipping them leaves every fold unchanged. The head
                 // positions (k_tile_fixup) are stored with zeros off the orbit.
-                const uint64_t nch = (tend + kCols - 1) / kCols;
+                // (split plans: the row's span [c_lo, c_hi) of this work item; c_lo > 0
+                // is a block boundary, hence past the head)
+                const uint64_t nch = (iend - lo_col + kCols - 1) / kCols;
                 for (uint64_t n = 0; n < nch; ++k) {
                     const int b = static_cast<int>(k % kNormBufs);
                     named_sync(kNormFull0 + b, kNormSync);
@@ -1050,12 +1069,13 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         e += cnt;
                     };
                     for (int j = 0; j < K; ++j) {
-                        const uint64_t i0 = (n + j) * kCols;
-                        if (i0 >= c_len) break;
+                        const uint64_t i0 = lo_col + (n + j) * kCols;
+                        if (i0 >= c_hi) break;
+                        if (i0 + kCols <= c_lo) continue;  // before this work item's span
                         uint32_t bits = mt.rbits[j][cr];
-                        const int end = static_cast<int>(min(c_len - i0, uint64_t(kCols)));
-                        int start = 0;
-                        if (i0 < c_head) {
+                        const int end = static_cast<int>(min(c_hi - i0, uint64_t(kCols)));
+                        int start = c_lo > i0 ? static_cast<int>(c_lo - i0) : 0;
+                        if (c_lo == 0 && i0 < c_head) {
                             const int qh = static_cast<int>(min(c_head - i0, uint64_t(end)));
                             double* head = p.head + ((j0 + cr) * 2 + cg) * 256 + i0;
                             for (int cc = 0; cc < qh; ++cc) head[cc] = ((bits >> cc) & 1u) ? nv[e++] : 0.0;
