@@ -270,6 +270,7 @@ struct OrbPlan {
 #define SHS_ORB_GROUPS 1
 #endif
 constexpr int kOrbGroups = SHS_ORB_GROUPS;  // producer groups filling alternate slots
+static_assert(kOrbGroups == 1, "the packing is computed once per slot by producer warp 0");
 #ifndef SHS_ORB_CAP
 #define SHS_ORB_CAP 1088
 #endif
@@ -654,44 +655,80 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                 uint64_t n = 0;
                 while (n < nch) {
                     const bool mine = static_cast<int>(qs % kOrbGroups) == grp;
-                    if (mine) mbar_wait(&sm.empty[stage], phase ^ 1);
                     OrbSlot& st = sm.stage[stage];
-                    // pass 1: how many sub-chunks fit (identical in every warp)
+                    // pass 1 (warp 0 of the group): how many sub-chunks fit, the row
+                    // offsets; published in the slot for the other producer warps
                     uint32_t rbj[kOrbSub], cntj[kOrbSub];
                     int K = 0;
                     uint32_t M = 0;
-                    bool stop = false;
+                    if (mine && pw == 0) {
+                        mbar_wait(&sm.empty[stage], phase ^ 1);
+                        bool stop = false;
 #pragma unroll
-                    for (int jj = 0; jj < kOrbSub; ++jj) {
-                        rbj[jj] = cntj[jj] = 0;
-                        if (!stop && n + jj < nch) {
-                            const uint64_t g = gc + jj;
-                            const int ps = static_cast<int>(g % kOrbPlanRing);
-                            mbar_wait(&sm.planfull[ps], static_cast<uint32_t>((g / kOrbPlanRing) & 1));
-                            const uint32_t rb = sm.plan[ps].rbits[lane];  // row `lane`
-                            const uint32_t c = __popc(rb);
-                            const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
-                            if (jj > 0 && M + tot > kOrbCap) {
-                                stop = true;
-                            } else {
-                                rbj[jj] = rb;
-                                cntj[jj] = c;
-                                M += tot;
-                                K = jj + 1;
+                        for (int jj = 0; jj < kOrbSub; ++jj) {
+                            rbj[jj] = cntj[jj] = 0;
+                            if (!stop && n + jj < nch) {
+                                const uint64_t g = gc + jj;
+                                const int ps = static_cast<int>(g % kOrbPlanRing);
+                                mbar_wait(&sm.planfull[ps], static_cast<uint32_t>((g / kOrbPlanRing) & 1));
+                                const uint32_t rb = sm.plan[ps].rbits[lane];  // row `lane`
+                                const uint32_t c = __popc(rb);
+                                const uint32_t tot = __reduce_add_sync(0xffffffffu, c);
+                                if (jj > 0 && M + tot > kOrbCap) {
+                                    stop = true;
+                                } else {
+                                    rbj[jj] = rb;
+                                    cntj[jj] = c;
+                                    M += tot;
+                                    K = jj + 1;
+                                }
+                            }
+                        }
+                        uint32_t rc = 0;
+#pragma unroll
+                        for (int jj = 0; jj < kOrbSub; ++jj) rc += cntj[jj];
+                        uint32_t inc = rc;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                            if (lane >= o) inc += v;
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < kOrbSub; ++jj)
+                            if (jj < K) st.rbits[jj][lane] = rbj[jj];
+                        st.soff[lane] = static_cast<uint16_t>(inc - rc);
+                        if (lane == 31) st.soff[kRows] = static_cast<uint16_t>(inc);
+                        if (lane == 0) st.nsub = static_cast<uint16_t>(K);
+                    }
+                    if (kOrbGroups == 1) named_sync(kProducerBar, Cfg::kProds);
+                    if (mine && pw != 0) {
+                        K = st.nsub;
+                        M = st.soff[kRows];
+#pragma unroll
+                        for (int jj = 0; jj < kOrbSub; ++jj) {
+                            rbj[jj] = jj < K ? st.rbits[jj][lane] : 0u;
+                            cntj[jj] = __popc(rbj[jj]);
+                        }
+                    }
+                    if (!mine) {  // the other group's slot (kOrbGroups > 1): where it ends
+                        bool stop = false;
+#pragma unroll
+                        for (int jj = 0; jj < kOrbSub; ++jj) {
+                            rbj[jj] = cntj[jj] = 0;
+                            if (!stop && n + jj < nch) {
+                                const uint64_t g = gc + jj;
+                                const int ps = static_cast<int>(g % kOrbPlanRing);
+                                mbar_wait(&sm.planfull[ps], static_cast<uint32_t>((g / kOrbPlanRing) & 1));
+                                const uint32_t tot = __reduce_add_sync(0xffffffffu, __popc(sm.plan[ps].rbits[lane]));
+                                if (jj > 0 && M + tot > kOrbCap) stop = true;
+                                else { M += tot; K = jj + 1; }
                             }
                         }
                     }
-                    // row offsets over the slot: row-major, all sub-chunks of a row together
                     uint32_t rowc = 0;
 #pragma unroll
                     for (int jj = 0; jj < kOrbSub; ++jj) rowc += cntj[jj];
-                    uint32_t incl = rowc;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += v;
-                    }
-                    uint32_t base = incl - rowc;  // this row's next member slot index
+                    uint32_t base = mine ? st.soff[lane] : 0u;  // this row's next member slot index
                     uint32_t rowc_before[kOrbSub];  // this row's members in the slot's earlier sub-chunks
 #pragma unroll
                     for (int jj = 0, acc = 0; jj < kOrbSub; ++jj) {
@@ -744,7 +781,6 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                             }
                         }
                         if (pw == 0) {
-                            st.rbits[jj][lane] = rb;
                             // the row's first members in the slot: the rank of its
                             // first included position (spans of split plans start mid-row)
                             const uint32_t before = jj ? rowc_before[jj] : 0u;
@@ -754,14 +790,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&sm.planempty[ps]);
                     }
-                    if (mine && pw == 0) {
-                        st.soff[lane] = static_cast<uint16_t>(incl - rowc);
-                        if (lane == 31) st.soff[kRows] = static_cast<uint16_t>(incl);
-                        if (lane == 0) {
-                            st.nsub = static_cast<uint16_t>(K);
-                            st.i0 = static_cast<uint32_t>(lo_col + n * kCols);
-                        }
-                    }
+                    if (mine && pw == 0 && lane == 0) st.i0 = static_cast<uint32_t>(lo_col + n * kCols);
                     gc += K;
                     n += K;
                     ++qs;
