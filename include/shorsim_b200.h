@@ -163,7 +163,7 @@ uint32_t shs_engine_stages(const shs_engine* engine);
  * orbit <a> (r = ord_N(a) <= N / 2 for a semiprime), so stages with whole-band
  * tile plans can store and sweep only its r members (both measurement groups
  * written by the probs pass, no collapse pass); bit-identical p0/p1, states and
- * bit strings. On by default from N >= 2^26 (SHS_ORBIT=0 or
+ * bit strings. On by default from N >= 2^22 (SHS_ORBIT=0 or
  * shs_engine_set_orbit(0): dense stages); toggling resets the state. shs_engine_orbit_info:
  * out[0] = r (0: off), out[1] = stages run compressed, out[2] = the first. */
 int shs_engine_set_orbit(shs_engine* engine, int32_t enable);

@@ -1497,7 +1497,10 @@ void plan_orbit(shs_engine* e) {
     e->orb_r = 0;
     const char* env = std::getenv("SHS_ORBIT");  // SHS_ORBIT=0: dense stages only
     e->orb_want = !(env && env[0] == '0');
-    if (e->group || e->N < kOrbitMinN) return;
+    uint64_t min_n = kOrbitMinN;
+    if (const char* mn = std::getenv("SHS_ORBIT_MIN_LOG2"))  // A/B hook
+        min_n = uint64_t(1) << std::min(62, std::atoi(mn));
+    if (e->group || e->N < min_n) return;
     std::vector<uint8_t> cap(e->t, 0);
     for (uint32_t s = 1; s < e->t; ++s)
         cap[s] = e->a_pows[s] != 1 && e->plans[s].tiled;
