@@ -334,6 +334,17 @@ def run_ours(args):
                              "what": "k_tiled<true,false,true> (plan warps, producers, consumers, "
                                      "chains) + k_tile_fixup: both sides of every member read, both "
                                      "groups written, no collapse pass"}
+        try:  # the measured ceiling of this access pattern (scripts/micro/fragment_bw.cu)
+            with open(os.path.join(ROOT, "profiles", "r02", "fragment_bw.jsonl")) as f:
+                pat = [json.loads(x) for x in f if x.strip()]
+            ceil = next(x for x in pat if x["kernel"] == "streams" and x["stream_bytes"] == 512)
+            roofline["orbit"]["pattern_ceiling"] = {
+                "GBps": ceil["GBps"], "frac": achieved / ceil["GBps"],
+                "source": "profiles/r02/fragment_bw.jsonl: 4736 row streams of 512 B reads and "
+                          "2 x 512 B writes per step plus 2 random 256 B gathers, plain loads / "
+                          "stores (DESIGN.md §3d)"}
+        except (OSError, StopIteration, KeyError, ValueError):
+            pass
 
     # the same stages with orbit compression off (the dense kernels), for scale
     dense_stages = None
