@@ -278,7 +278,7 @@ def run_ours(args):
 
     def spec_at(s):
         return spec_on and s + 1 < t
-    # orbit-compressed stages (the default from N >= 2^22): the
+    # orbit-compressed stages (the default from N >= 2^21): the
     # probs pass reads both sides of the r = ord(a) members and writes both
     # groups (64 B per member; 32 on a run's last stage), no collapse pass
     orb = eng.orbit_info()

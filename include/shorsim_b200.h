@@ -154,7 +154,7 @@ int shs_engine_run_sequential(shs_engine* engine, uint64_t seed, uint64_t idx0, 
 int shs_engine_stage_multipliers(const shs_engine* engine, uint64_t* out);
 /* sparse prefix of runs: the first stages computed on the support of the
  * state (2^(s+1) amplitudes after stage s), bit-identical p0/p1 and bit
- * strings; on by default where it applies (N >= 2^22, support <= N / 16, the
+ * strings; on by default where it applies (N >= 2^21, support <= N / 16, the
  * orbit does not wrap). shs_engine_sparse_stages = stages it covers (0: none). */
 int shs_engine_set_sparse(shs_engine* engine, int32_t enable);
 uint32_t shs_engine_sparse_stages(const shs_engine* engine);
@@ -163,7 +163,7 @@ uint32_t shs_engine_stages(const shs_engine* engine);
  * orbit <a> (r = ord_N(a) <= N / 2 for a semiprime), so stages with whole-band
  * tile plans can store and sweep only its r members (both measurement groups
  * written by the probs pass, no collapse pass); bit-identical p0/p1, states and
- * bit strings. On by default from N >= 2^22 (SHS_ORBIT=0 or
+ * bit strings. On by default from N >= 2^21 (SHS_ORBIT=0 or
  * shs_engine_set_orbit(0): dense stages); toggling resets the state. shs_engine_orbit_info:
  * out[0] = r (0: off), out[1] = stages run compressed, out[2] = the first. */
 int shs_engine_set_orbit(shs_engine* engine, int32_t enable);

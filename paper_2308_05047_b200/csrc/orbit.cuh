@@ -25,9 +25,10 @@
 
 namespace shs {
 
-// from 2^22 (config 3, N = 16777207: a run 9.0 -> 6.4 ms; below, the batched /
-// lockstep engines serve the campaign sizes)
-constexpr uint64_t kOrbitMinN = uint64_t(1) << 22;
+// from 2^21 (config 3, N = 16777207: a run 9.0 -> 6.4 ms; N = 4186067: 4.75 ->
+// 4.21 ms); below 2^21 the stages have no tile plans (AUTO tiling), so nothing
+// would run compressed
+constexpr uint64_t kOrbitMinN = uint64_t(1) << 21;
 constexpr int kOrbThreads = 256;
 
 __device__ __forceinline__ uint64_t lowmask64(unsigned o) { return o ? (~0ull >> (64 - o)) : 0ull; }

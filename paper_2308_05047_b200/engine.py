@@ -432,7 +432,7 @@ class IterativeShorEngine:
         return self._lib.shs_engine_sparse_stages(self._h)
 
     def set_orbit(self, enable: bool) -> None:
-        """Orbit-compressed stages (on by default from N >= 2^22): stages with
+        """Orbit-compressed stages (on by default from N >= 2^21): stages with
         whole-band tile plans store and sweep only the r = ord_N(a) members of
         <a>, bit-identical results. Toggling resets the state."""
         _raise(self._lib.shs_engine_set_orbit(self._h, 1 if enable else 0))
