@@ -137,3 +137,29 @@ def test_orbit_low_density_runs_equal_dense(cuda_ok, N, a, r):
     for g, w in zip(got, want):
         assert g.bits.j == w.bits.j and g.j_sampled == w.j_sampled
         assert [x.p1 for x in g.trace] == [x.p1 for x in w.trace]
+
+
+@pytest.mark.parametrize("N,a", [
+    (4186067, 2),      # 2039 * 2053, just below 2^22: compressed from 2^21 (orbit.cuh kOrbitMinN)
+    (16777207, 1234567),  # config 3's size (bench.py config3_error_models)
+])
+def test_orbit_default_on_mid_sizes_equal_dense(cuda_ok, N, a):
+    """The compressed stages are the default from 2^21 (where AUTO tiling gives the
+    stages tile plans); runs under every error kind equal the dense engine's."""
+    import paper_2308_05047_b200 as shs
+    kinds = [shs.ErrorConfig(),
+             shs.ErrorConfig(shs.ErrorKind.quantum_measure, 0.01, shs.PauliProbs(0.005, 0.005, 0.0)),
+             shs.ErrorConfig(shs.ErrorKind.amplitude_init, 0.01),
+             shs.ErrorConfig(shs.ErrorKind.bitflip, 0.01)]
+    for err in kinds:
+        prob = shs.FactoringProblem.make(N, a)
+        eng = shs.IterativeShorEngine(prob, err, shs.SimulatorOptions(qubit_ceiling=64))
+        assert eng.orbit_info()["stages"] > 0  # on by default
+        got = [eng.run(3, i) for i in range(3)]
+        eng.set_orbit(False)
+        want = [eng.run(3, i) for i in range(3)]
+        eng.close()
+        for g, w in zip(got, want):
+            assert g.bits.j == w.bits.j and g.j_sampled == w.j_sampled
+            assert [x.p1 for x in g.trace] == [x.p1 for x in w.trace]
+    gc.collect()
