@@ -275,7 +275,10 @@ static_assert(kOrbGroups == 1, "the packing is computed once per slot by produce
 #define SHS_ORB_CAP 1088
 #endif
 constexpr int kOrbCap = SHS_ORB_CAP;  // members per slot (one compact norm tile per group)
-constexpr int kOrbSub = 4;
+#ifndef SHS_ORB_SUB
+#define SHS_ORB_SUB 4
+#endif
+constexpr int kOrbSub = SHS_ORB_SUB;  // sub-chunks per slot at most
 constexpr int kOrbPlanRing = 8;
 constexpr uint64_t kOrbWrap = 1ull << 63;
 
