@@ -710,6 +710,22 @@ StageScalars host_scalars(const shs_engine* e, uint32_t s, u128 prefix, double i
     return sc;
 }
 
+// k_tile_fixup's grid: one warp per 32 items (k_tile_fixup1) when every such
+// warp fits on the GPU at once, else 8-warp CTAs up to fixup_cap
+int fixup_grid(const shs_engine* e, const TileParams& tp) {
+    const uint64_t w = (2 * tp.H + 31) / 32;
+    if (w <= uint64_t(kFix1Ctas) * e->num_sms && !std::getenv("SHS_FIXUP8")) return static_cast<int>(w);
+    return static_cast<int>(
+        std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
+}
+void launch_fixup(shs_engine* e, const TileParams& tp, int g1, int g2) {
+    unsigned long long* slots = e->partials + uint64_t(g1) * 2 * kDigits;
+    if ((2 * tp.H + 31) / 32 <= uint64_t(kFix1Ctas) * e->num_sms && !std::getenv("SHS_FIXUP8"))
+        k_tile_fixup1<<<g2, 32, kFix1Smem, e->stream>>>(tp, slots);
+    else
+        k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, slots);
+}
+
 // Probs pass of stage s on the current sel (tiled or direct kernels, plus the
 // tiled fixup). Scalars: e->sc, or the device slot `dev` when non-null.
 // *nparts = the exact-accumulator slots it filled.
@@ -739,8 +755,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         // SM) measured 1% faster whole, n30's few-band ones 6% faster per run split.
         const bool split = pl.split_tail && pl.ntiles < 4 * static_cast<uint64_t>(e->num_sms);
         const int g1 = split ? pl.grid : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
-        const int g2 = static_cast<int>(
-            std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
+        const int g2 = fixup_grid(e, tp);
         rc = launch(e, 0, [&] {
             if (split) {
                 k_tiled<true, true, true><<<g1, tile_threads<true, true, true>(), tile_smem_bytes<true, true>(),
@@ -750,7 +765,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
                                              e->stream>>>(tp);
                 e->band_issued += pl.ntiles;
             }
-            k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
+            launch_fixup(e, tp, g1, g2);
         });
         e->launches++;  // k_tiled + k_tile_fixup in one launch group
         *nparts = g1 + g2;
@@ -765,8 +780,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         const TilePlanHost& pl = e->plans[s];
         const int g1 = pl.split_tail ? pl.grid
                                      : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
-        const int g2 = static_cast<int>(
-            std::min<uint64_t>((2 * tp.H + 32 * kFixWarps - 1) / (32 * kFixWarps), static_cast<uint64_t>(e->fixup_cap)));
+        const int g2 = fixup_grid(e, tp);
         rc = launch(e, 0, [&] {
             if (pl.split_tail) {
                 k_tiled<true, true><<<g1, tile_threads<true, true>(), tile_smem_bytes<true>(), e->stream>>>(tp);
@@ -774,7 +788,7 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
                 k_tiled<true, false><<<g1, tile_threads<true, false>(), tile_smem_bytes<true>(), e->stream>>>(tp);
                 e->band_issued += pl.ntiles;
             }
-            k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, e->partials + uint64_t(g1) * 2 * kDigits);
+            launch_fixup(e, tp, g1, g2);
         });
         e->launches++;  // k_tiled + k_tile_fixup: two kernels in one launch group
         *nparts = g1 + g2;
@@ -1644,6 +1658,9 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
     ce = cudaFuncSetAttribute(k_tile_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(kFixSmem));
     if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tile_fixup)");
+    ce = cudaFuncSetAttribute(k_tile_fixup1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kFix1Smem));
+    if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_tile_fixup1)");
     ce = cudaFuncSetAttribute(k_lock_probs_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(kLockWsSmem));
     if (ce != cudaSuccess) return fail(ce, "cudaFuncSetAttribute(k_lock_probs_ws)");

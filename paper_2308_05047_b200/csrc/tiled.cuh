@@ -1284,4 +1284,53 @@ static __global__ void __launch_bounds__(32 * kFixWarps, 2) k_tile_fixup(TilePar
     write_partials(digits, slots + uint64_t(blockIdx.x) * 2 * kDigits, tid);
 }
 
+// k_tile_fixup for plans with few rows (2 H <= 32 x kFix1Ctas x SMs: config 3's
+// 1536-row plans): one warp per CTA stages all of its 32 items' heads in shared
+// memory with one round of 16 B cp.async copies, then each lane folds its item in
+// order. The 8-warp kernel streams the heads slab by slab (32 columns, one slab
+// in flight), a chain of up to 8 memory latencies per warp that set its time
+// when there are too few warps to fill the GPU.
+constexpr int kFix1Stride = 258;  // doubles per staged head (16 B aligned rows)
+constexpr size_t kFix1Smem = sizeof(double) * 32 * kFix1Stride;
+constexpr int kFix1Ctas = 3;      // per SM (66 KB of shared memory each)
+static __global__ void __launch_bounds__(32) k_tile_fixup1(TileParams p, unsigned long long* slots) {
+    extern __shared__ double fix1_buf[];  // [32][kFix1Stride]
+    __shared__ unsigned long long digits[2][kDigits];
+    const int lane = threadIdx.x;
+    for (int i = lane; i < 2 * kDigits; i += 32) (&digits[0][0])[i] = 0ull;
+    __syncwarp();
+    DigitWindow win;
+    window_reset(win);
+    const int g = lane & 1;  // item base + lane has group (base + lane) & 1, base even
+    const uint64_t items = 2 * p.H;
+    for (uint64_t base = uint64_t(blockIdx.x) * 32; base < items; base += uint64_t(gridDim.x) * 32) {
+        const uint64_t idx = base + lane;
+        uint32_t hl = 0;
+        uint64_t z = 0;
+        if (idx < items) {
+            z = mulmod_shoup(idx >> 1, p.A, p.A_sh, p.N);
+            hl = static_cast<uint32_t>((256 - (z & 255)) & 255);
+        }
+        double s = hl ? p.tail[idx] : 0.0;  // tail[j * 2 + g]
+        // item i's first hl values (pairs: the odd one past hl is never read)
+        for (int i = 0; i < 32; ++i) {
+            const uint32_t hli = __shfl_sync(0xffffffffu, hl, i);
+            const double* src = p.head + (base + i) * 256;
+            for (uint32_t c = 2 * lane; c < hli; c += 64) cp_async16(&fix1_buf[i * kFix1Stride + c], src + c);
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const double* row = fix1_buf + lane * kFix1Stride;
+        for (uint32_t c = 0; c < hl; ++c) s = __dadd_rn(s, row[c]);
+        if (hl) {
+            p.S[g * p.nb + (z >> 8)] = s;
+            window_add(win, s, digits[g]);
+        }
+        __syncwarp();  // the row reads end before the next items' copies
+    }
+    window_flush(win, digits[g]);
+    __syncwarp();
+    write_partials(digits, slots + uint64_t(blockIdx.x) * 2 * kDigits, lane);
+}
+
 }  // namespace shs
