@@ -148,7 +148,9 @@ __device__ __forceinline__ void window_add(DigitWindow& w, double v, unsigned lo
 }
 
 // Round an exact digit accumulator (normalised in place) to the nearest double,
-// ties to even; subnormal results keep the 2^-1074 quantum.
+// ties to even; subnormal results keep the 2^-1074 quantum. The mantissa, round
+// and sticky bits are read word-wise (a bit-by-bit walk over shared memory cost
+// ~2 us per call in the single-CTA finalize kernels).
 __device__ __forceinline__ double digits_to_double(unsigned long long* acc) {
     unsigned long long carry = 0;
     for (int i = 0; i < kDigits; ++i) {
@@ -156,20 +158,26 @@ __device__ __forceinline__ double digits_to_double(unsigned long long* acc) {
         acc[i] = v & 0xffffffffull;
         carry = v >> 32;
     }
-    int top = -1;
-    for (int i = kDigits - 1; i >= 0 && top < 0; --i)
-        if (acc[i]) top = i * 32 + 63 - __clzll(acc[i]);
-    if (top < 0) return 0.0;
-    auto bit = [&](int p) -> int {
-        return p >= 0 ? static_cast<int>((acc[p >> 5] >> (p & 31)) & 1ull) : 0;
-    };
+    int ti = kDigits - 1;
+    while (ti >= 0 && !acc[ti]) --ti;
+    if (ti < 0) return 0.0;
+    const int top = ti * 32 + 63 - __clzll(acc[ti]);
     int lsb = top - 52;
-    if (lsb < kAnchor - 1074) lsb = kAnchor - 1074;
-    unsigned long long mant = 0;
-    for (int p = top; p >= lsb; --p) mant = (mant << 1) | static_cast<unsigned long long>(bit(p));
-    int round = bit(lsb - 1);
-    int sticky = 0;
-    for (int p = lsb - 2; p >= 0 && !sticky; --p) sticky = bit(p);
+    if (lsb < kAnchor - 1074) lsb = kAnchor - 1074;  // >= 14: round and sticky bits exist
+    unsigned long long mant = 0;  // bits [lsb, top]
+    if (top >= lsb) {
+        const int k = lsb >> 5, sh = lsb & 31;
+        const unsigned long long lo = acc[k] | (k + 1 < kDigits ? acc[k + 1] << 32 : 0ull);
+        const unsigned long long d2 = k + 2 < kDigits ? acc[k + 2] : 0ull;
+        const unsigned long long w = sh ? (lo >> sh) | (d2 << (64 - sh)) : lo;
+        mant = w & ((2ull << (top - lsb)) - 1ull);
+    }
+    const int pr = lsb - 1;
+    const bool round = (acc[pr >> 5] >> (pr & 31)) & 1ull;
+    const int ps = lsb - 2;  // sticky: any bit in [0, ps]
+    int j = ps >> 5;
+    bool sticky = (acc[j] & ((2ull << (ps & 31)) - 1ull)) != 0;
+    while (!sticky && --j >= 0) sticky = acc[j] != 0;
     if (round && (sticky || (mant & 1ull))) ++mant;
     return scalbn(static_cast<double>(mant), lsb - kAnchor);
 }
