@@ -312,7 +312,8 @@ struct TileSmem {
     double onrm[kOrb ? kNB : 1][2][kOrb ? kOrbCap : 1];  // orbit: [buffer][group][member]
     uint64_t full[kST], empty[kST];
     unsigned long long digits[2][kDigits];
-    uint32_t bandq[16];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16]
+    uint32_t bandq[16 + 1];  // CtaWork<false>: the CTA's k-th band in bandq[k % 16];
+                             // bandq[16]: how many entries P0 has published
     OrbMeta meta[kOrb ? kNB : 1];  // orbit: the slot of each norm tile
     uint64_t planfull[kOrb ? kOrbPlanRing : 1], planempty[kOrb ? kOrbPlanRing : 1];
     alignas(128) OrbPlan plan[kOrb ? kOrbPlanRing : 1];  // bulk-copy destinations: 16 B aligned at least
@@ -438,8 +439,20 @@ struct CtaWork<false> {
             q[0] = static_cast<uint32_t>(b);
             const uint64_t b1 = fetch(p);
             q[1] = static_cast<uint32_t>(b1 < nt ? b1 : nt);
+            publish(2);
         }
         if (producer) named_sync(kProducerBar, nprod);
+    }
+    // Readers outside the producer barrier (the orbit plan warps run up to a
+    // plan ring ahead of the producers, so a band of <= 8 sub-chunks could end
+    // before P0 wrote its successor) wait for P0's count of written entries.
+    __device__ __forceinline__ void publish(uint32_t n) {
+        __threadfence_block();
+        reinterpret_cast<volatile uint32_t*>(q)[kBandQ] = n;
+    }
+    __device__ __forceinline__ void await(uint64_t n) const {
+        while (reinterpret_cast<volatile uint32_t*>(q)[kBandQ] < n) __nanosleep(64);
+        __threadfence_block();
     }
     __device__ __forceinline__ bool valid() const { return b < nt; }
     __device__ __forceinline__ void next(const TileParams& p) {
@@ -449,8 +462,10 @@ struct CtaWork<false> {
                 const uint64_t b2 = fetch(p);
                 q[(k + 2) % kBandQ] = static_cast<uint32_t>(b2 < nt ? b2 : nt);
             }
+            publish(static_cast<uint32_t>(k + 3));
         }
         if (producer) named_sync(kProducerBar, nprod);
+        else await(k + 2);
         ++k;
         b = q[k % kBandQ];
     }
@@ -607,6 +622,7 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
     }
     if (kProbs)
         for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&sm.digits[0][0])[i] = 0ull;
+    if (tid == 0) sm.bandq[kBandQ] = 0;  // CtaWork<false>: nothing published yet
     __syncthreads();
 
     if (warp >= kProducerWarp && warp < kProducerWarp + Cfg::kPW) {
