@@ -148,6 +148,7 @@ struct shs_engine {
     // (both groups written, no collapse pass); each N-amplitude buffer holds a
     // pair of compressed slots (stride orb_pad), the current pair in X
     bool orb_want = true;          // SHS_ORBIT=0 / shs_engine_set_orbit(0): dense only
+    bool pdl = true;               // SHS_PDL=0: orbit stages launched without programmatic dependent launch
     bool orb_ready = false;        // rank records built
     uint64_t orb_r = 0, orb_pad = 0;
     std::vector<uint8_t> orb_use;  // per stage
@@ -757,12 +758,23 @@ int launch_probs_pass(shs_engine* e, uint32_t s, const DevStage* dev, int* npart
         const int g1 = split ? pl.grid : static_cast<int>(std::min<uint64_t>(pl.ntiles, e->tiled_cap));
         const int g2 = fixup_grid(e, tp);
         rc = launch(e, 0, [&] {
+            // programmatic dependent launch: the plan warps overlap the previous
+            // stage's finalize (k_tiled's griddepcontrol.wait guards the rest)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(g1);
+            cfg.dynamicSmemBytes = tile_smem_bytes<true, true>();
+            cfg.stream = e->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = e->pdl ? 1 : 0;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
             if (split) {
-                k_tiled<true, true, true><<<g1, tile_threads<true, true, true>(), tile_smem_bytes<true, true>(),
-                                            e->stream>>>(tp);
+                cfg.blockDim = dim3(tile_threads<true, true, true>());
+                cudaLaunchKernelEx(&cfg, k_tiled<true, true, true>, tp);
             } else {
-                k_tiled<true, false, true><<<g1, tile_threads<true, false, true>(), tile_smem_bytes<true, true>(),
-                                             e->stream>>>(tp);
+                cfg.blockDim = dim3(tile_threads<true, false, true>());
+                cudaLaunchKernelEx(&cfg, k_tiled<true, false, true>, tp);
                 e->band_issued += pl.ntiles;
             }
             launch_fixup(e, tp, g1, g2);
@@ -1674,6 +1686,8 @@ int shs_engine_create(const shs_problem* problem, const shs_error* error,
         e->lock_ws = !(lw && lw[0] == '0');
         const char* sp = std::getenv("SHS_SPEC");  // A/B: 0 = every collapse runs
         e->spec_on = !(sp && sp[0] == '0');
+        const char* pd = std::getenv("SHS_PDL");  // A/B: 0 = plain launches
+        e->pdl = !(pd && pd[0] == '0');
     }
     ce = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return fail(ce, "cudaStreamCreate");

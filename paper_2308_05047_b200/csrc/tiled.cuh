@@ -593,8 +593,14 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
     constexpr int kProducerWarp = Cfg::kProdWarp, kChainWarp = Cfg::kChainWarp0;
     constexpr int kRowsPerConsumer = Cfg::kRowsPerCons, kNormSync = Cfg::kNSync;
     (void)kConsumers;
-    const StageScalars sc = p.dev ? p.dev->sc : p.sc;
-    const int sel = p.dev ? p.dev->sel : p.sel;
+    // the orbit variant may start under programmatic dependent launch while the
+    // previous stage's finalize still runs: its scalars are read after the wait
+    StageScalars sc = p.sc;
+    int sel = p.sel;
+    if (!kOrb && p.dev) {
+        sc = p.dev->sc;
+        sel = p.dev->sel;
+    }
     if (!kProbs && p.spec && sel == 0) {
         // Y already holds h0 (raw, like every collapse output); the dynamic band
         // counter still advances by the ntiles fetches a full launch makes
@@ -624,6 +630,19 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
         for (int i = tid; i < 2 * kDigits; i += blockDim.x) (&sm.digits[0][0])[i] = 0ull;
     if (tid == 0) sm.bandq[kBandQ] = 0;  // CtaWork<false>: nothing published yet
     __syncthreads();
+    if constexpr (kOrb) {
+        // every role but the plan warps (records and the plan only) waits for the
+        // previous kernels' writes before it reads or writes global state
+        const bool plan_warp = !(warp >= kProducerWarp && warp < kProducerWarp + Cfg::kPW) &&
+                               warp >= kConsumerWarps && warp >= kChainWarp + kChainWarps;
+        if (!plan_warp) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (p.dev) {
+                sc = p.dev->sc;
+                sel = p.dev->sel;
+            }
+        }
+    }
 
     if (warp >= kProducerWarp && warp < kProducerWarp + Cfg::kPW) {
         // ------------------------------------------------------------ producers
