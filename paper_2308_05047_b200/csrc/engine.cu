@@ -721,10 +721,21 @@ int fixup_grid(const shs_engine* e, const TileParams& tp) {
 }
 void launch_fixup(shs_engine* e, const TileParams& tp, int g1, int g2) {
     unsigned long long* slots = e->partials + uint64_t(g1) * 2 * kDigits;
-    if ((2 * tp.H + 31) / 32 <= uint64_t(kFix1Ctas) * e->num_sms && !std::getenv("SHS_FIXUP8"))
-        k_tile_fixup1<<<g2, 32, kFix1Smem, e->stream>>>(tp, slots);
-    else
+    if ((2 * tp.H + 31) / 32 <= uint64_t(kFix1Ctas) * e->num_sms && !std::getenv("SHS_FIXUP8")) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g2);
+        cfg.blockDim = dim3(32);
+        cfg.dynamicSmemBytes = kFix1Smem;
+        cfg.stream = e->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = e->pdl ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_tile_fixup1, tp, slots);
+    } else {
         k_tile_fixup<<<g2, 32 * kFixWarps, kFixSmem, e->stream>>>(tp, slots);
+    }
 }
 
 // Probs pass of stage s on the current sel (tiled or direct kernels, plus the
@@ -1121,8 +1132,20 @@ int engine_run_device(shs_engine* e, u64 seed, u64 idx, u128* j_out, u128* js_ou
         }
         ms.rec = e->d_rec;
         rc = launch(e, 1, [&] {
-            k_finalize_measure<<<1, kFinalizeThreads, 0, e->stream>>>(e->partials, nparts, e->S, e->nb,
-                                                                  e->kahan ? 1 : 0, ms);
+            // programmatic dependent of the probs pass's last kernel (k_tile_fixup1
+            // triggers at its start; the others at their end): its first
+            // instruction waits for them
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(1);
+            cfg.blockDim = dim3(kFinalizeThreads);
+            cfg.stream = e->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = e->pdl ? 1 : 0;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, k_finalize_measure, static_cast<const unsigned long long*>(e->partials),
+                               nparts, static_cast<const double*>(e->S), e->nb, e->kahan ? 1 : 0, ms);
         });
         if (rc) return fail(rc);
         if (cudaEventRecord(e->meas_ev[s & 1], e->stream) != cudaSuccess)

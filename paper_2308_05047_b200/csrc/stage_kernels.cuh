@@ -401,8 +401,10 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
                        const double* __restrict__ S, uint64_t nb, int kahan, MeasureStep ms) {
     __shared__ unsigned long long acc[2][kDigits];
     __shared__ double pp[2];
-    // the next stage's orbit kernel may be scheduled now (its plan warps start;
+    // launched as a programmatic dependent of the fixup: wait for the partials;
+    // the next stage's orbit kernel may be scheduled now (its plan warps start,
     // everything else in it waits for this grid: griddepcontrol.wait)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     if (kahan) {
         kahan_combine(S, nb, pp);

@@ -631,6 +631,9 @@ __global__ void __launch_bounds__((tile_threads<kProbs, kSplit, kOrb>()), 1) k_t
     if (tid == 0) sm.bandq[kBandQ] = 0;  // CtaWork<false>: nothing published yet
     __syncthreads();
     if constexpr (kOrb) {
+        // k_tile_fixup1 may be scheduled on SMs this grid leaves (it waits for
+        // the whole grid before reading anything)
+        asm volatile("griddepcontrol.launch_dependents;");
         // every role but the plan warps (records and the plan only) waits for the
         // previous kernels' writes before it reads or writes global state
         const bool plan_warp = !(warp >= kProducerWarp && warp < kProducerWarp + Cfg::kPW) &&
@@ -1332,6 +1335,10 @@ static __global__ void __launch_bounds__(32) k_tile_fixup1(TileParams p, unsigne
     extern __shared__ double fix1_buf[];  // [32][kFix1Stride]
     __shared__ unsigned long long digits[2][kDigits];
     const int lane = threadIdx.x;
+    // launched as a programmatic dependent of k_tiled: wait for its heads,
+    // tails and partials; the finalize may be scheduled right away
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     for (int i = lane; i < 2 * kDigits; i += 32) (&digits[0][0])[i] = 0ull;
     __syncwarp();
     DigitWindow win;
